@@ -1,0 +1,66 @@
+"""Drop-in check: the reference's own 235-test suite, run against this package.
+
+A shim package named ``ppoff`` maps ``ppoff.{costs,ir,builders,offload,sim}`` to
+this package's modules; the reference's out-of-scope consumers (analysis,
+render, cli) are loaded from the read-only reference sources ON TOP of them, so
+they exercise this planner unchanged.  Runs only where /root/reference exists
+(this container); the GPU box relies on tests/golden instead.
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+from conftest import REFERENCE_SRC, ROOT, have_reference
+
+SHIM = textwrap.dedent(
+    f'''
+    import importlib, importlib.util, sys
+    sys.dont_write_bytecode = True
+    from paper_2503_01328_b200 import *  # noqa: F401,F403
+    for _n in ("costs", "ir", "builders", "offload", "sim"):
+        sys.modules["ppoff." + _n] = importlib.import_module("paper_2503_01328_b200." + _n)
+        globals()[_n] = sys.modules["ppoff." + _n]
+
+    def _load(name):
+        spec = importlib.util.spec_from_file_location("ppoff." + name, "{REFERENCE_SRC}/ppoff/" + name + ".py")
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[spec.name] = mod
+        spec.loader.exec_module(mod)
+        return mod
+
+    render = _load("render")
+    analysis = _load("analysis")
+    cli = _load("cli")
+    '''
+)
+
+
+@pytest.mark.skipif(not have_reference(), reason="reference sources not mounted")
+def test_reference_suite_passes_against_this_planner(tmp_path):
+    shim = tmp_path / "shim" / "ppoff"
+    shim.mkdir(parents=True)
+    (shim / "__init__.py").write_text(SHIM)
+    tests = tmp_path / "tests"
+    shutil.copytree(os.path.join(os.path.dirname(REFERENCE_SRC), "tests"), tests)
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", PYTHONPATH=f"{tmp_path / 'shim'}:{ROOT}")
+    probe = subprocess.run(
+        [sys.executable, "-c", "import ppoff.sim, ppoff.analysis; print(ppoff.sim.__file__); print(ppoff.analysis.simulate.__module__)"],
+        cwd=tmp_path, env=env, capture_output=True, text=True, check=True,
+    )
+    assert probe.stdout.split() == [os.path.join(ROOT, "paper_2503_01328_b200", "sim.py"), "paper_2503_01328_b200.sim"]
+    args = [sys.executable, "-m", "pytest", "tests", "-q", "-p", "no:cacheprovider"]
+    try:
+        import xdist  # noqa: F401
+
+        args += ["-n", str(min(8, os.cpu_count() or 1))]
+    except ImportError:
+        pass
+    res = subprocess.run(args, cwd=tmp_path, env=env, capture_output=True, text=True, timeout=1200)
+    tail = res.stdout[-2000:]
+    assert res.returncode == 0, tail
+    assert "235 passed" in tail, tail
