@@ -1,0 +1,170 @@
+/*
+ * ppo_b200.h -- C ABI of libppo_b200.so, the B200 (sm_100a) activation round-trip engine.
+ *
+ * This library is the device half of the drop-in replacement for the reference's
+ * pipeline runner `simulate(sched, plan, ...)` (reference pkg/src/ppoff/sim.py:141-149).
+ * The reference only *models* the path; every entry point below makes one modelled
+ * quantity real and cites the reference line that fixes its semantics:
+ *
+ *   - pinned host pool + D2H/H2D segment copies  <- transfer slots, offload.py:133-220;
+ *     residency rules sim.py:462-487; host bins offload.py:305-340
+ *   - pack (gather into a contiguous slab)         <- the 20bsh payload, costs.py:99-105
+ *   - LayerNorm / GeLU / dropout recompute         <- the 34bsh -> 20bsh coefficient,
+ *                                                     costs.py:1-7,18-20
+ *   - stage-boundary send/recv (NCCL over NVLink)  <- the t_comm lag, costs.py:78,
+ *                                                     ir.py:211-224, sim.py:196-202;
+ *                                                     message size costs.py:108-113
+ *
+ * ABI rules
+ *   - Every function returns 0 on success, a negative PPO_E* code on argument errors,
+ *     or a positive cudaError_t / ncclResult_t (offset by PPO_NCCL_BASE) on runtime
+ *     failure; nothing throws across the ABI.  ppo_last_error() gives a thread-local
+ *     message for the last failure.
+ *   - Pointers are raw device / pinned-host addresses; sizes are bytes or element
+ *     counts as named.  Streams and events are cudaStream_t / cudaEvent_t passed as
+ *     void* (0 = legacy default stream / no event).
+ *   - Everything is stream-ordered; no call blocks the host except ppo_pool_create,
+ *     ppo_pool_destroy and ppo_comm_init / ppo_comm_destroy.
+ *   - Element type of activations is bf16 (uint16_t storage); statistics, weight-side
+ *     reductions and LayerNorm parameters gradients are fp32.
+ */
+#ifndef PPO_B200_H
+#define PPO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPO_ABI_VERSION 1
+
+#define PPO_OK 0
+#define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
+#define PPO_ENOMEM (-2)   /* pool exhausted                                         */
+#define PPO_ESHAPE (-3)   /* unsupported shape (e.g. hidden % 8 != 0, hidden > 8192)*/
+#define PPO_ENOTSUP (-4)  /* feature not compiled in (e.g. NCCL)                    */
+#define PPO_NCCL_BASE 10000
+
+/* ---------------------------------------------------------------- housekeeping */
+int ppo_abi_version(void);
+const char* ppo_last_error(void);
+/* Number of kernels this library has launched since load (for the bench's gpu_launches). */
+uint64_t ppo_kernel_launches(void);
+/* SM count and max shared memory of the current device (grid sizing). */
+int ppo_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------ K2: pinned host pool + copies */
+/* A preallocated, page-locked host arena (cudaHostAlloc, portable + NUMA-local by
+ * first touch from the calling process).  No per-step allocation: slabs are carved
+ * at plan time.  Replaces the modelled host residency of sim.py:462-487. */
+typedef struct ppo_pool ppo_pool;
+int ppo_pool_create(uint64_t bytes, ppo_pool** out);
+int ppo_pool_destroy(ppo_pool* pool);
+void* ppo_pool_base(const ppo_pool* pool);
+uint64_t ppo_pool_bytes(const ppo_pool* pool);
+
+/* One contiguous piece of a transfer: the device slab's [dev, dev+bytes) <-> host bin
+ * [host, host+bytes).  A (stage, microbatch) payload is <= 3 segments, one per
+ * power-of-two host bin (offload.py:305-340). */
+typedef struct {
+  void* dev;
+  void* host;
+  uint64_t bytes;
+} ppo_segment;
+
+#define PPO_D2H 0 /* OFFLOAD transfer, PassKind.OFFLOAD (ir.py:27-32) */
+#define PPO_H2D 1 /* RELOAD  transfer, PassKind.RELOAD                */
+
+/* Enqueue one transfer slot on `copy_stream`: wait on `wait_event` (if non-null),
+ * copy every segment in `direction`, then record `done_event` (if non-null).
+ * The D2H `done_event` is the point at which the device slab may be reused
+ * (sim.py:477-479: residency ends at D2H end); the H2D `wait_event` is the reload
+ * anchor lowered from the slot start (sim.py:177-181). */
+int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_stream,
+                 void* wait_event, void* done_event);
+
+/* ------------------------------------------------------------ K1: pack / gather */
+/* Gather `n` byte ranges into one destination: dst[dst_off[i] .. + bytes[i]) =
+ * src[i][0 .. bytes[i]).  Optional 2-D form: `rows[i]` rows of `row_bytes[i]`
+ * with source pitch `src_pitch[i]` (0 = dense).  16-byte vectorised, persistent
+ * grid (k x SM count).  All addresses and sizes must be 16-byte aligned. */
+typedef struct {
+  const void* src;
+  uint64_t dst_off;
+  uint64_t rows;
+  uint64_t row_bytes;
+  uint64_t src_pitch;
+} ppo_gather_item;
+int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream);
+
+/* ------------------------------------------ K3/K5: fused LayerNorm + dropout */
+/* Philox4x32-10 dropout: element e of a tensor tagged (seed, offset) is kept iff
+ * word (e % 4) of Philox(counter = {e/4 lo, e/4 hi, offset lo, offset hi},
+ * key = {seed lo, seed hi}) >= floor(p * 2^32); kept values are scaled by 1/(1-p).
+ * The mask is never stored: backward replays it. */
+
+/* y = LayerNorm(x) * gamma + beta over rows x hidden (bf16 in/out, fp32 math). */
+int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y,
+                      int64_t rows, int64_t hidden, float eps, void* stream);
+
+/* Residual + dropout + LayerNorm, the forward epilogue of both residual branches:
+ *   out = resid + dropout(branch; seed, offset, p)   (bf16, written to `out`)
+ *   ln  = LayerNorm(out) * gamma + beta              (bf16, optional: ln may be NULL)
+ * `out` is normally a view into the stage's activation slab (h1 of the saved set). */
+int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out,
+                                const float* gamma, const float* beta, void* ln,
+                                int64_t rows, int64_t hidden, float eps, float p,
+                                uint64_t seed, uint64_t offset, void* stream);
+
+/* LayerNorm backward with the statistics recomputed from x (no saved mean/rstd):
+ *   dx = resid_grad + LN_bwd(dy; x, gamma)           (bf16; resid_grad may be NULL)
+ *   dgamma += sum_rows(dy * xhat), dbeta += sum_rows(dy)   (fp32 accumulators)
+ * and, when drop_out != NULL, drop_out = dropout_bwd(dx; drop_seed, drop_offset, p):
+ * the mask replay of the dropout that produced the residual branch feeding x. */
+int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const void* resid_grad,
+                      void* dx, float* dgamma, float* dbeta, int64_t rows, int64_t hidden,
+                      float eps, void* drop_out, float p, uint64_t drop_seed,
+                      uint64_t drop_offset, void* stream);
+
+/* Standalone dropout (forward: y = dropout(x); backward: dx = dropout_bwd(dy) -- the
+ * same mask applied to the gradient). */
+int ppo_dropout(const void* x, void* y, int64_t n, float p, uint64_t seed, uint64_t offset,
+                void* stream);
+
+/* ------------------------------------------------------------- K4: GeLU */
+/* g = gelu_tanh(f)  (forward, fc1-out -> fc2 input). */
+int ppo_gelu_fwd(const void* f, void* g, int64_t n, void* stream);
+/* Backward with recompute, one pass over f:
+ *   g  = gelu_tanh(f)           (the fc2 weight-gradient operand; g may be NULL)
+ *   df = dg * gelu_tanh'(f)     (may alias dg) */
+int ppo_gelu_bwd(const void* f, const void* dg, void* g, void* df, int64_t n, void* stream);
+
+/* Column sums of a rows x cols bf16 matrix accumulated into fp32 `acc` (bias grads,
+ * tests). */
+int ppo_colsum(const void* x, float* acc, int64_t rows, int64_t cols, void* stream);
+
+/* ----------------------------------------------- K8: stage-boundary send/recv */
+/* NCCL communicator of the pipeline (one rank per GPU).  The 128-byte unique id is
+ * produced by rank 0 with ppo_comm_unique_id and broadcast by the host runtime
+ * (torch.distributed store).  send/recv are grouped point-to-point transfers on
+ * `stream`; the forward activation goes stage s -> s+1 and its gradient s+1 -> s,
+ * with the interleaved wrap d-1 -> 0 (ir.py:293). */
+typedef struct ppo_comm ppo_comm;
+int ppo_comm_unique_id(uint8_t id_out[128]);
+int ppo_comm_init(const uint8_t id[128], int nranks, int rank, int device, ppo_comm** out);
+int ppo_comm_destroy(ppo_comm* comm);
+/* n_ops point-to-point operations issued as one NCCL group. */
+typedef struct {
+  int is_send;  /* 1 = send, 0 = recv */
+  int peer;
+  void* buf;
+  uint64_t bytes;
+} ppo_p2p_op;
+int ppo_p2p(ppo_comm* comm, const ppo_p2p_op* ops, int n_ops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPO_B200_H */

@@ -1,0 +1,173 @@
+// Shared helpers of libppo_b200.so: error plumbing, launch accounting, bf16 vectors,
+// Philox4x32-10.  Internal header; the ABI is include/ppo_b200.h.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/ppo_b200.h"
+
+namespace ppo {
+
+int set_error(int code, const char* fmt, ...);
+int cuda_error(cudaError_t err, const char* what);
+int sm_count_current();
+extern std::atomic<uint64_t> g_launches;
+
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+#define PPO_TRY_CUDA(expr)                                  \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return ::ppo::cuda_error(_e, #expr); \
+  } while (0)
+
+// Checks the launch that was just enqueued (configuration errors only).
+#define PPO_LAUNCHED(name)                                  \
+  do {                                                      \
+    ::ppo::count_launch();                                  \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return ::ppo::cuda_error(_e, name); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline cudaEvent_t as_event(void* e) { return reinterpret_cast<cudaEvent_t>(e); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ bf16 x 8
+struct alignas(16) Bf16x8 {
+  __nv_bfloat162 h[4];
+};
+
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&f)[8]) {
+  const Bf16x8& v = reinterpret_cast<const Bf16x8&>(raw);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(v.h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  Bf16x8 v;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v.h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return reinterpret_cast<const uint4&>(v);
+}
+
+// Round-trip through bf16 so math sees exactly what was stored.
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w));
+}
+
+// ------------------------------------------------------------ Philox4x32-10
+struct U32x4 {
+  uint32_t v[4];
+};
+
+__host__ __device__ __forceinline__ void mulhilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+#ifdef __CUDA_ARCH__
+  lo = a * b;
+  hi = __umulhi(a, b);
+#else
+  uint64_t p = (uint64_t)a * (uint64_t)b;
+  lo = (uint32_t)p;
+  hi = (uint32_t)(p >> 32);
+#endif
+}
+
+// counter (c0..c3), key (k0, k1); ten rounds, Random123 constants.
+__host__ __device__ __forceinline__ U32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                        uint32_t c3, uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo(M0, c0, hi0, lo0);
+    mulhilo(M1, c2, hi1, lo1);
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += W0;
+    k1 += W1;
+  }
+  U32x4 out;
+  out.v[0] = c0;
+  out.v[1] = c1;
+  out.v[2] = c2;
+  out.v[3] = c3;
+  return out;
+}
+
+// Keep bits for elements e0 .. e0+7 (e0 % 8 == 0) of tensor (seed, offset).
+__device__ __forceinline__ uint32_t keep_mask8(uint64_t e0, uint64_t seed, uint64_t offset,
+                                               uint32_t threshold) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint64_t ctr = (e0 >> 2) + half;
+    U32x4 r = philox4x32_10((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)offset,
+                            (uint32_t)(offset >> 32), (uint32_t)seed, (uint32_t)(seed >> 32));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bits |= (r.v[i] >= threshold ? 1u : 0u) << (4 * half + i);
+  }
+  return bits;
+}
+
+inline uint32_t dropout_threshold(float p) {
+  double t = (double)p * 4294967296.0;
+  if (t <= 0.0) return 0u;
+  if (t >= 4294967295.0) return 0xFFFFFFFFu;
+  return (uint32_t)t;
+}
+
+// ------------------------------------------------------------ block reductions
+// Sums N values across the block; every thread gets the totals.  `scratch` holds
+// 32*N floats.  Safe to call back to back (ends with a barrier).
+template <int N>
+__device__ __forceinline__ void block_sum(float (&v)[N], float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) scratch[warp * N + i] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float t = 0.f;
+    for (int w = 0; w < nwarps; ++w) t += scratch[w * N + i];
+    v[i] = t;
+  }
+  __syncthreads();
+}
+
+}  // namespace ppo

@@ -1,0 +1,190 @@
+// libppo_b200.so -- housekeeping, pinned host pool (K2), transfer slots (K2), pack (K1).
+//
+// The reference models these as quantities only: the payload bytes
+// (pkg/src/ppoff/costs.py:99-105), the single-stream transfer slots
+// (offload.py:133-220), host bins (offload.py:305-340) and residency
+// (sim.py:462-487).  Here they are real copies on a dedicated copy stream.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "ppo_common.cuh"
+
+namespace ppo {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_error = buf;
+  return code;
+}
+
+int cuda_error(cudaError_t err, const char* what) {
+  return set_error((int)err, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
+}
+
+int sm_count_current() {
+  static thread_local int cached_dev = -1, cached_sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev != cached_dev) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+      cached_sms = sms;
+    cached_dev = dev;
+  }
+  return cached_sms;
+}
+
+// -------------------------------------------------------------------- K1 pack
+constexpr int kMaxGather = 32;
+struct GatherArgs {
+  ppo_gather_item item[kMaxGather];
+  int n;
+};
+
+// Persistent gather: every thread walks each item's 16-byte chunks with a grid
+// stride, four independent 16 B loads in flight before the stores.
+__global__ void __launch_bounds__(256) pack_kernel(GatherArgs args, uint8_t* __restrict__ dst) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (int i = 0; i < args.n; ++i) {
+    const ppo_gather_item it = args.item[i];
+    const uint64_t row_chunks = it.row_bytes >> 4;
+    const uint64_t total = row_chunks * it.rows;
+    const uint64_t pitch = it.src_pitch ? it.src_pitch : it.row_bytes;
+    const uint8_t* src = static_cast<const uint8_t*>(it.src);
+    uint8_t* out = dst + it.dst_off;
+    uint64_t c = tid;
+    for (; c + 3 * nthr < total; c += 4 * nthr) {
+      uint4 v[4];
+      uint64_t dofs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint64_t cc = c + u * nthr;
+        uint64_t r = cc / row_chunks, k = cc - r * row_chunks;
+        v[u] = ld_stream(src + r * pitch + (k << 4));
+        dofs[u] = cc << 4;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) st_stream(out + dofs[u], v[u]);
+    }
+    for (; c < total; c += nthr) {
+      uint64_t r = c / row_chunks, k = c - r * row_chunks;
+      st_stream(out + (c << 4), ld_stream(src + r * pitch + (k << 4)));
+    }
+  }
+}
+
+}  // namespace ppo
+
+using namespace ppo;
+
+extern "C" {
+
+int ppo_abi_version(void) { return PPO_ABI_VERSION; }
+
+const char* ppo_last_error(void) { return t_error.c_str(); }
+
+uint64_t ppo_kernel_launches(void) { return g_launches.load(); }
+
+int ppo_device_info(int device, int* sm_count, int* cc_major, int* cc_minor) {
+  if (!sm_count || !cc_major || !cc_minor) return set_error(PPO_EINVAL, "ppo_device_info: null output");
+  PPO_TRY_CUDA(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device));
+  PPO_TRY_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  PPO_TRY_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  return PPO_OK;
+}
+
+// ------------------------------------------------------------------- pool
+struct ppo_pool {
+  void* base;
+  uint64_t bytes;
+};
+
+int ppo_pool_create(uint64_t bytes, ppo_pool** out) {
+  if (!out || bytes == 0) return set_error(PPO_EINVAL, "ppo_pool_create: bad arguments");
+  *out = nullptr;
+  void* base = nullptr;
+  // Portable so every context of the process may DMA from it; the pages are
+  // first-touched by this process, which the launcher binds to the GPU's NUMA node.
+  PPO_TRY_CUDA(cudaHostAlloc(&base, bytes, cudaHostAllocPortable));
+  ppo_pool* p = static_cast<ppo_pool*>(std::malloc(sizeof(ppo_pool)));
+  if (!p) {
+    cudaFreeHost(base);
+    return set_error(PPO_ENOMEM, "ppo_pool_create: host malloc failed");
+  }
+  p->base = base;
+  p->bytes = bytes;
+  *out = p;
+  return PPO_OK;
+}
+
+int ppo_pool_destroy(ppo_pool* pool) {
+  if (!pool) return PPO_OK;
+  cudaError_t e = cudaFreeHost(pool->base);
+  std::free(pool);
+  if (e != cudaSuccess) return cuda_error(e, "cudaFreeHost");
+  return PPO_OK;
+}
+
+void* ppo_pool_base(const ppo_pool* pool) { return pool ? pool->base : nullptr; }
+
+uint64_t ppo_pool_bytes(const ppo_pool* pool) { return pool ? pool->bytes : 0; }
+
+// --------------------------------------------------------------- K2 transfer
+int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_stream, void* wait_event,
+                 void* done_event) {
+  if (direction != PPO_D2H && direction != PPO_H2D) return set_error(PPO_EINVAL, "ppo_transfer: bad direction");
+  if (nsegs < 0 || (nsegs > 0 && !segs)) return set_error(PPO_EINVAL, "ppo_transfer: bad segments");
+  cudaStream_t s = as_stream(copy_stream);
+  if (wait_event) PPO_TRY_CUDA(cudaStreamWaitEvent(s, as_event(wait_event), 0));
+  const cudaMemcpyKind kind = direction == PPO_D2H ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+  for (int i = 0; i < nsegs; ++i) {
+    if (segs[i].bytes == 0) continue;
+    if (!segs[i].dev || !segs[i].host) return set_error(PPO_EINVAL, "ppo_transfer: null segment %d", i);
+    void* dst = direction == PPO_D2H ? segs[i].host : segs[i].dev;
+    const void* src = direction == PPO_D2H ? segs[i].dev : segs[i].host;
+    PPO_TRY_CUDA(cudaMemcpyAsync(dst, src, segs[i].bytes, kind, s));
+  }
+  if (done_event) PPO_TRY_CUDA(cudaEventRecord(as_event(done_event), s));
+  return PPO_OK;
+}
+
+// ------------------------------------------------------------------ K1 pack
+int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream) {
+  if (n < 0 || n > kMaxGather || (n > 0 && (!items || !dst)))
+    return set_error(PPO_EINVAL, "ppo_pack: bad arguments (n=%d, max %d)", n, kMaxGather);
+  if (n == 0) return PPO_OK;
+  if (!aligned16(dst)) return set_error(PPO_EINVAL, "ppo_pack: destination not 16-byte aligned");
+  GatherArgs args;
+  std::memset(&args, 0, sizeof(args));
+  uint64_t chunks = 0;
+  for (int i = 0; i < n; ++i) {
+    const ppo_gather_item& it = items[i];
+    const uint64_t pitch = it.src_pitch ? it.src_pitch : it.row_bytes;
+    if (!it.src || !aligned16(it.src) || (it.dst_off & 15) || (it.row_bytes & 15) || (pitch & 15))
+      return set_error(PPO_EINVAL, "ppo_pack: item %d not 16-byte aligned", i);
+    args.item[i] = it;
+    chunks += (it.row_bytes >> 4) * it.rows;
+  }
+  args.n = n;
+  if (chunks == 0) return PPO_OK;
+  const int threads = 256;
+  uint64_t want = (chunks + threads * 4 - 1) / (threads * 4);
+  const uint64_t cap = (uint64_t)sm_count_current() * 8;  // 8 CTAs of 256 per SM resident
+  const int blocks = (int)(want < cap ? (want ? want : 1) : cap);
+  pack_kernel<<<blocks, threads, 0, as_stream(stream)>>>(args, static_cast<uint8_t*>(dst));
+  PPO_LAUNCHED("pack_kernel");
+  return PPO_OK;
+}
+
+}  // extern "C"

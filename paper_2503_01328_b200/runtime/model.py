@@ -1,0 +1,308 @@
+"""One pipeline stage of the GPT model, with its saved set laid out in a slab.
+
+Forward writes the 20bsh saved set of every layer straight into the
+(stage, microbatch) slab (``layout.SlabLayout``): the QKV and fc1 GEMMs write
+their outputs into slab views, the fused residual+dropout+LayerNorm kernel
+writes h1 and the next layer's x, and only the attention output / LSE need a
+K1 pack into the slab.  Backward reads the (possibly reloaded) slab, recomputes
+LayerNorm, GeLU and both dropout masks (K3-K5, ``libppo_b200.so``) and never
+needs anything that was not saved -- the recompute scheme of PAPER.md:439 that
+turns the reference's 34bsh coefficient into 20bsh (costs.py:1-7,18-20).
+
+Dense GEMMs run on cuBLAS through torch (bf16 in, fp32 accumulate; weight
+gradients accumulate in fp32), causal attention on cuDNN's fused kernel; the
+embedding and loss head (first/last stage only) use torch ops.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import native
+from .layout import SlabLayout, make_layout
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    n_layers: int = 4
+    hidden: int = 256
+    heads: int = 4
+    seq: int = 512
+    vocab: int = 1024
+    p_drop: float = 0.1
+    dropout_seed: int = 42
+    eps: float = 1e-5
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+
+def dropout_offset(cfg: ModelConfig, iteration: int, layer: int, mb: int, microbatches: int, branch: int) -> int:
+    """Philox offset of one dropout site (branch 0: attention residual, 1: MLP residual)."""
+    return (((iteration * cfg.n_layers + layer) * microbatches + mb) * 2) + branch
+
+
+def init_params(cfg: ModelConfig, seed: int = 1234, names=None) -> dict[str, torch.Tensor]:
+    """Deterministic N(0, 0.02) init on the CPU generator (bf16-representable values).
+
+    Draw order is fixed (embedding, per-layer, head) so every rank reproduces the
+    same weights for the layers it owns without communicating.
+    """
+    h, v, s = cfg.hidden, cfg.vocab, cfg.seq
+    shapes = {"wte": (v, h), "wpe": (s, h)}
+    for l in range(cfg.n_layers):
+        shapes.update({
+            f"l{l}.ln1_g": (h,), f"l{l}.ln1_b": (h,), f"l{l}.w_qkv": (3 * h, h), f"l{l}.w_proj": (h, h),
+            f"l{l}.ln2_g": (h,), f"l{l}.ln2_b": (h,), f"l{l}.w_fc1": (4 * h, h), f"l{l}.w_fc2": (h, 4 * h),
+        })
+    shapes.update({"lnf_g": (h,), "lnf_b": (h,), "w_head": (v, h)})
+    gen = torch.Generator().manual_seed(seed)
+    out = {}
+    for name, shape in shapes.items():
+        if name.endswith("_g"):
+            val = torch.ones(shape)
+        elif name.endswith("_b"):
+            val = torch.zeros(shape)
+        else:
+            std = 0.02 / (2 * cfg.n_layers) ** 0.5 if name.endswith(("w_proj", "w_fc2")) else 0.02
+            val = (torch.randn(shape, generator=gen) * std).bfloat16().float()
+        if names is None or name in names:
+            out[name] = val
+    return out
+
+
+def stage_layers(cfg: ModelConfig, num_stages: int, stage: int) -> list[int]:
+    """Global layer ids of a stage: contiguous, as even as possible."""
+    base, extra = divmod(cfg.n_layers, num_stages)
+    lo = stage * base + min(stage, extra)
+    return list(range(lo, lo + base + (1 if stage < extra else 0)))
+
+
+def _wgrad(acc: torch.Tensor, a_t: torch.Tensor, b: torch.Tensor) -> None:
+    """acc(fp32) += a_t @ b with bf16 operands and fp32 accumulation in cuBLAS."""
+    torch.addmm(acc, a_t, b, out_dtype=torch.float32, out=acc)
+
+
+class SlabView:
+    """Typed tensor views of one slab (device memory owned by the arena)."""
+
+    def __init__(self, layout: SlabLayout, base: torch.Tensor):
+        self.layout = layout
+        self.base = base  # uint8 tensor of layout.slab_bytes
+        self._cache = {}
+
+    def get(self, layer: int, name: str) -> torch.Tensor:
+        key = (layer, name)
+        t = self._cache.get(key)
+        if t is None:
+            slot = self.layout.find(layer, name)
+            raw = self.base[slot.dev_offset: slot.dev_offset + slot.nbytes]
+            t = raw.view(torch.bfloat16 if slot.dtype == "bf16" else torch.float32).view(slot.shape)
+            self._cache[key] = t
+        return t
+
+    def offset(self, layer: int, name: str) -> int:
+        return self.layout.find(layer, name).dev_offset
+
+
+class Stage:
+    """Parameters, gradients, workspace and the F/B passes of one pipeline stage."""
+
+    def __init__(self, cfg: ModelConfig, stage: int, num_stages: int, microbatches: int, device, params=None,
+                 layers: list[int] | None = None, seed: int = 1234):
+        native.require_cuda()
+        self.cfg, self.stage, self.num_stages, self.m = cfg, stage, num_stages, microbatches
+        self.first, self.last = stage == 0, stage == num_stages - 1
+        self.layers = layers if layers is not None else stage_layers(cfg, num_stages, stage)
+        self.device = torch.device(device)
+        self.layout = make_layout(len(self.layers), cfg.seq, cfg.hidden, cfg.heads, head_grad=self.last)
+        names = set()
+        for l in self.layers:
+            names |= {f"l{l}.{k}" for k in ("ln1_g", "ln1_b", "w_qkv", "w_proj", "ln2_g", "ln2_b", "w_fc1", "w_fc2")}
+        if self.first:
+            names |= {"wte", "wpe"}
+        if self.last:
+            names |= {"lnf_g", "lnf_b", "w_head"}
+        src = params if params is not None else init_params(cfg, seed, names)
+        self.w, self.g, self.master = {}, {}, {}
+        for n in sorted(names):
+            t = src[n].to(self.device, torch.float32)
+            self.master[n] = t.clone()
+            is_matrix = t.dim() == 2
+            self.w[n] = t.to(torch.bfloat16) if is_matrix else t.contiguous()
+            self.g[n] = torch.zeros_like(t, dtype=torch.float32)
+        s, h = cfg.seq, cfg.hidden
+        bf = dict(device=self.device, dtype=torch.bfloat16)
+        self.ws = {
+            "ln": torch.empty(s, h, **bf), "a": torch.empty(s, h, **bf), "g": torch.empty(s, 4 * h, **bf),
+            "big": torch.empty(s, 4 * h, **bf), "dm": torch.empty(s, h, **bf), "dh1": torch.empty(s, h, **bf),
+            "da": torch.empty(s, h, **bf), "t": torch.empty(s, h, **bf), "dy": torch.empty(s, h, **bf),
+        }
+        self.loss_sum = torch.zeros((), device=self.device, dtype=torch.float32)
+        self._attn_meta = None
+
+    # ------------------------------------------------------------------ utils
+    def p(self, l: int, k: str) -> torch.Tensor:
+        return self.w[f"l{l}.{k}"]
+
+    def gp(self, l: int, k: str) -> torch.Tensor:
+        return self.g[f"l{l}.{k}"]
+
+    def _qkv_views(self, qkv: torch.Tensor):
+        cfg = self.cfg
+        v = qkv.view(1, cfg.seq, 3, cfg.heads, cfg.head_dim)
+        return [v[:, :, i].transpose(1, 2) for i in range(3)]
+
+    def _offsets(self, l_global: int, mb: int, iteration: int):
+        return (dropout_offset(self.cfg, iteration, l_global, mb, self.m, 0),
+                dropout_offset(self.cfg, iteration, l_global, mb, self.m, 1))
+
+    def zero_grad(self):
+        for t in self.g.values():
+            t.zero_()
+        self.loss_sum.zero_()
+
+    # ---------------------------------------------------------------- forward
+    def embed(self, slab: SlabView, tokens: torch.Tensor):
+        """x0 = wte[tokens] + wpe written into layer 0's x slot (first stage)."""
+        x0 = slab.get(0, "x")
+        torch.add(torch.nn.functional.embedding(tokens, self.w["wte"]), self.w["wpe"], out=x0)
+
+    def forward(self, slab: SlabView, mb: int, iteration: int, out: torch.Tensor | None = None,
+                targets: torch.Tensor | None = None):
+        """Run the stage's layers on the activation already in slab x[0].
+
+        Non-last stages write the stage output into ``out`` (the send buffer);
+        the last stage computes the loss and its output gradient (into the slab's
+        head_dy slot) right away.
+        """
+        cfg, ws = self.cfg, self.ws
+        p, seed, eps = cfg.p_drop, cfg.dropout_seed, cfg.eps
+        n_local = len(self.layers)
+        native.layernorm_fwd(slab.get(0, "x"), self.p(self.layers[0], "ln1_g"), self.p(self.layers[0], "ln1_b"), ws["ln"], eps)
+        for i, l in enumerate(self.layers):
+            off_a, off_m = self._offsets(l, mb, iteration)
+            x, qkv, h1, f = slab.get(i, "x"), slab.get(i, "qkv"), slab.get(i, "h1"), slab.get(i, "f")
+            torch.mm(ws["ln"], self.p(l, "w_qkv").t(), out=qkv)
+            q, k, v = self._qkv_views(qkv)
+            res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+            o_tmp, lse = res[0], res[1]
+            if self._attn_meta is None:
+                self._attn_meta = tuple(res[2:8])
+                self._o_strides = o_tmp.stride()
+                self._lse_shape = tuple(lse.shape)
+            self._pack_attention(slab, i, o_tmp, lse)
+            o = slab.get(i, "o")
+            torch.mm(o, self.p(l, "w_proj").t(), out=ws["a"])
+            native.residual_dropout_ln_fwd(x, ws["a"], h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps)
+            torch.mm(ws["ln"], self.p(l, "w_fc1").t(), out=f)
+            native.gelu_fwd(f, ws["g"])
+            torch.mm(ws["g"], self.p(l, "w_fc2").t(), out=ws["a"])
+            if i + 1 < n_local:
+                nxt = self.layers[i + 1]
+                native.residual_dropout_ln_fwd(h1, ws["a"], slab.get(i + 1, "x"), self.p(nxt, "ln1_g"),
+                                               self.p(nxt, "ln1_b"), ws["ln"], p, seed, off_m, eps)
+            elif self.last:
+                native.residual_dropout_ln_fwd(h1, ws["a"], ws["dy"], self.w["lnf_g"], self.w["lnf_b"], ws["ln"],
+                                               p, seed, off_m, eps)
+                self._head(slab, targets)
+            else:
+                native.residual_dropout_ln_fwd(h1, ws["a"], out, None, None, None, p, seed, off_m, eps)
+
+    def _pack_attention(self, slab: SlabView, i: int, o_tmp: torch.Tensor, lse: torch.Tensor):
+        s, h, H = self.cfg.seq, self.cfg.hidden, self.cfg.heads
+        if not o_tmp.transpose(1, 2).is_contiguous() or not lse.is_contiguous():
+            raise RuntimeError(f"unexpected cuDNN attention layout: o {o_tmp.stride()} lse {lse.stride()}")
+        native.pack(
+            [(o_tmp, slab.offset(i, "o"), 1, 2 * s * h, 0), (lse, slab.offset(i, "lse"), 1, 4 * H * s, 0)],
+            slab.base,
+        )
+
+    def _head(self, slab: SlabView, targets: torch.Tensor):
+        """Loss head of the last stage, forward and backward fused into F.
+
+        ws["dy"] holds y (final layer output), ws["ln"] holds LNf(y).  Writes the
+        gradient of (loss / m) w.r.t. y into the slab's head_dy slot.
+        """
+        ws, cfg = self.ws, self.cfg
+        logits = torch.mm(ws["ln"], self.w["w_head"].t()).float()
+        loss = torch.nn.functional.cross_entropy(logits, targets)
+        self.loss_sum += loss.detach()
+        dlogits = torch.softmax(logits, -1)
+        dlogits[torch.arange(cfg.seq, device=self.device), targets] -= 1.0
+        dlogits = (dlogits / (cfg.seq * self.m)).to(torch.bfloat16)
+        _wgrad(self.g["w_head"], dlogits.t(), ws["ln"])
+        torch.mm(dlogits, self.w["w_head"], out=ws["t"])
+        native.layernorm_bwd(ws["dy"], self.w["lnf_g"], ws["t"], None, slab.get(-1, "head_dy"),
+                             self.g["lnf_g"], self.g["lnf_b"], eps=cfg.eps)
+
+    # --------------------------------------------------------------- backward
+    def backward(self, slab: SlabView, mb: int, iteration: int, dy: torch.Tensor | None = None,
+                 dx_out: torch.Tensor | None = None, tokens: torch.Tensor | None = None):
+        """Backward of the stage from the output gradient ``dy`` (received) or,
+        on the last stage, the head gradient saved in the slab.  Writes the input
+        gradient into ``dx_out`` (send buffer); the first stage scatters it into
+        the embedding gradients instead."""
+        cfg, ws = self.cfg, self.ws
+        p, seed, eps = cfg.p_drop, cfg.dropout_seed, cfg.eps
+        s, h = cfg.seq, cfg.hidden
+        n_local = len(self.layers)
+        dy_cur = slab.get(-1, "head_dy") if self.last else dy
+        top_off_m = self._offsets(self.layers[-1], mb, iteration)[1]
+        native.dropout(dy_cur, ws["dm"], p, seed, top_off_m)
+        for i in range(n_local - 1, -1, -1):
+            l = self.layers[i]
+            off_a, _ = self._offsets(l, mb, iteration)
+            x, qkv, o, lse, h1, f = (slab.get(i, n) for n in ("x", "qkv", "o", "lse", "h1", "f"))
+            dg = ws["big"]
+            # MLP: dg = dm @ Wfc2; g = gelu(f) recomputed; df = dg * gelu'(f)
+            torch.mm(ws["dm"], self.p(l, "w_fc2"), out=dg)
+            native.gelu_bwd(f, dg, ws["g"], dg)
+            _wgrad(self.gp(l, "w_fc2"), ws["dm"].t(), ws["g"])
+            native.layernorm_fwd(h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
+            _wgrad(self.gp(l, "w_fc1"), dg.t(), ws["ln"])
+            torch.mm(dg, self.p(l, "w_fc1"), out=ws["t"])
+            # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay)
+            native.layernorm_bwd(h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"], self.gp(l, "ln2_g"),
+                                 self.gp(l, "ln2_b"), drop_out=ws["da"], p=p, drop_seed=seed, drop_offset=off_a, eps=eps)
+            # attention projection and core
+            _wgrad(self.gp(l, "w_proj"), ws["da"].t(), o)
+            torch.mm(ws["da"], self.p(l, "w_proj"), out=ws["t"])
+            q, k, v = self._qkv_views(qkv)
+            o4 = o.view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
+            do4 = ws["t"].view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
+            lse3 = lse.view(self._lse_shape)
+            cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
+            dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
+                do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
+            native.layernorm_fwd(x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
+            w_qkv, g_qkv = self.p(l, "w_qkv"), self.gp(l, "w_qkv")
+            grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
+            for j, gj in enumerate(grads):
+                _wgrad(g_qkv[j * h:(j + 1) * h], gj.t(), ws["ln"])
+            torch.mm(grads[0], w_qkv[0:h], out=ws["t"])
+            torch.addmm(ws["t"], grads[1], w_qkv[h:2 * h], out=ws["t"])
+            torch.addmm(ws["t"], grads[2], w_qkv[2 * h:3 * h], out=ws["t"])
+            # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay
+            below = i > 0
+            dx_target = ws["dy"] if (below or self.first or dx_out is None) else dx_out
+            drop_below = ws["dm"] if below else None
+            off_below = self._offsets(self.layers[i - 1], mb, iteration)[1] if below else 0
+            native.layernorm_bwd(x, self.p(l, "ln1_g"), ws["t"], ws["dh1"], dx_target, self.gp(l, "ln1_g"),
+                                 self.gp(l, "ln1_b"), drop_out=drop_below, p=p if below else 0.0,
+                                 drop_seed=seed, drop_offset=off_below, eps=eps)
+            dy_cur = dx_target
+        if self.first:
+            self.g["wte"].index_add_(0, tokens, dy_cur.float())
+            self.g["wpe"].add_(dy_cur.float())
+
+    # -------------------------------------------------------------- optimizer
+    def sgd_step(self, lr: float = 1e-4):
+        """Plain SGD on fp32 master weights, then refresh the bf16 copies."""
+        names = sorted(self.master)
+        torch._foreach_add_([self.master[n] for n in names], [self.g[n] for n in names], alpha=-lr)
+        for n in names:
+            self.w[n].copy_(self.master[n])

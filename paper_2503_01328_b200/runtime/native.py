@@ -1,0 +1,271 @@
+"""ctypes binding of ``libppo_b200.so`` (ABI: ``include/ppo_b200.h``).
+
+This is the only door from Python into the device code.  It loads the in-tree
+library and raises ``NativeUnavailable`` when it is missing or the process has
+no CUDA device -- the runtime has no CPU fallback.
+
+Tensor-level helpers take torch tensors (device memory + the current stream are
+PyTorch's; the library only sees raw pointers, sizes and stream handles).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB_PATH = os.path.join(PKG, "libppo_b200.so")
+
+PPO_D2H, PPO_H2D = 0, 1
+PPO_NCCL_BASE = 10000
+
+
+class NativeUnavailable(RuntimeError):
+    """libppo_b200.so (or a CUDA device) is not available: nothing to fall back to."""
+
+
+class PpoError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} failed with code {code}: {msg}")
+        self.code = code
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("dev", ctypes.c_void_p), ("host", ctypes.c_void_p), ("bytes", ctypes.c_uint64)]
+
+
+class GatherItem(ctypes.Structure):
+    _fields_ = [
+        ("src", ctypes.c_void_p),
+        ("dst_off", ctypes.c_uint64),
+        ("rows", ctypes.c_uint64),
+        ("row_bytes", ctypes.c_uint64),
+        ("src_pitch", ctypes.c_uint64),
+    ]
+
+
+class P2POp(ctypes.Structure):
+    _fields_ = [("is_send", ctypes.c_int), ("peer", ctypes.c_int), ("buf", ctypes.c_void_p), ("bytes", ctypes.c_uint64)]
+
+
+_VP, _U64, _I64, _F32, _I32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_float, ctypes.c_int
+_FP = ctypes.POINTER(ctypes.c_float)
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+SIGNATURES = {
+    "ppo_abi_version": [],
+    "ppo_last_error": [],
+    "ppo_kernel_launches": [],
+    "ppo_device_info": [_I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
+    "ppo_pool_create": [_U64, ctypes.POINTER(_VP)],
+    "ppo_pool_destroy": [_VP],
+    "ppo_pool_base": [_VP],
+    "ppo_pool_bytes": [_VP],
+    "ppo_transfer": [_I32, ctypes.POINTER(Segment), _I32, _VP, _VP, _VP],
+    "ppo_pack": [ctypes.POINTER(GatherItem), _I32, _VP, _VP],
+    "ppo_layernorm_fwd": [_VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP],
+    "ppo_residual_dropout_ln_fwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _F32, _U64, _U64, _VP],
+    "ppo_layernorm_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP, _F32, _U64, _U64, _VP],
+    "ppo_dropout": [_VP, _VP, _I64, _F32, _U64, _U64, _VP],
+    "ppo_gelu_fwd": [_VP, _VP, _I64, _VP],
+    "ppo_gelu_bwd": [_VP, _VP, _VP, _VP, _I64, _VP],
+    "ppo_colsum": [_VP, _VP, _I64, _I64, _VP],
+    "ppo_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
+    "ppo_comm_init": [ctypes.POINTER(ctypes.c_uint8), _I32, _I32, _I32, ctypes.POINTER(_VP)],
+    "ppo_comm_destroy": [_VP],
+    "ppo_p2p": [_VP, ctypes.POINTER(P2POp), _I32, _VP],
+}
+_RESTYPES = {
+    "ppo_last_error": ctypes.c_char_p,
+    "ppo_kernel_launches": ctypes.c_uint64,
+    "ppo_pool_base": ctypes.c_void_p,
+    "ppo_pool_bytes": ctypes.c_uint64,
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the library (no CUDA device needed to load; calls need one)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a); there is no CPU fallback"
+            )
+        lib = ctypes.CDLL(path)
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        if lib.ppo_abi_version() != 1:
+            raise NativeUnavailable("libppo_b200.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def check(fn: str, rc: int) -> None:
+    if rc != 0:
+        msg = load().ppo_last_error()
+        raise PpoError(fn, rc, msg.decode() if msg else "")
+
+
+def call(fn: str, *args) -> None:
+    check(fn, getattr(load(), fn)(*args))
+
+
+def kernel_launches() -> int:
+    return int(load().ppo_kernel_launches())
+
+
+# ---------------------------------------------------------------- torch helpers
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the B200 runtime has no CPU fallback")
+    load()
+    return torch
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check_bf16(*ts):
+    import torch
+
+    for t in ts:
+        if t is not None and (t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("expected a contiguous bf16 CUDA tensor")
+
+
+def layernorm_fwd(x, gamma, beta, y, eps=1e-5, stream=None):
+    _check_bf16(x, y)
+    h = x.shape[-1]
+    call("ppo_layernorm_fwd", _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), x.numel() // h, h, eps, _stream(stream))
+
+
+def residual_dropout_ln_fwd(resid, branch, out, gamma, beta, ln, p, seed, offset, eps=1e-5, stream=None):
+    _check_bf16(resid, branch, out, ln)
+    h = resid.shape[-1]
+    call(
+        "ppo_residual_dropout_ln_fwd", _ptr(resid), _ptr(branch), _ptr(out), _ptr(gamma), _ptr(beta), _ptr(ln),
+        resid.numel() // h, h, eps, p, seed, offset, _stream(stream),
+    )
+
+
+def layernorm_bwd(x, gamma, dy, resid_grad, dx, dgamma, dbeta, drop_out=None, p=0.0, drop_seed=0,
+                  drop_offset=0, eps=1e-5, stream=None):
+    _check_bf16(x, dy, resid_grad, dx, drop_out)
+    h = x.shape[-1]
+    call(
+        "ppo_layernorm_bwd", _ptr(x), _ptr(gamma), _ptr(dy), _ptr(resid_grad), _ptr(dx), _ptr(dgamma),
+        _ptr(dbeta), x.numel() // h, h, eps, _ptr(drop_out), p, drop_seed, drop_offset, _stream(stream),
+    )
+
+
+def dropout(x, y, p, seed, offset, stream=None):
+    _check_bf16(x, y)
+    call("ppo_dropout", _ptr(x), _ptr(y), x.numel(), p, seed, offset, _stream(stream))
+
+
+def gelu_fwd(f, g, stream=None):
+    _check_bf16(f, g)
+    call("ppo_gelu_fwd", _ptr(f), _ptr(g), f.numel(), _stream(stream))
+
+
+def gelu_bwd(f, dg, g, df, stream=None):
+    _check_bf16(f, dg, g, df)
+    call("ppo_gelu_bwd", _ptr(f), _ptr(dg), _ptr(g), _ptr(df), f.numel(), _stream(stream))
+
+
+def colsum(x, acc, stream=None):
+    _check_bf16(x)
+    call("ppo_colsum", _ptr(x), _ptr(acc), x.numel() // x.shape[-1], x.shape[-1], _stream(stream))
+
+
+def pack(items, dst, stream=None):
+    """items: list of (src_tensor_or_ptr, dst_offset, rows, row_bytes, src_pitch)."""
+    arr = (GatherItem * len(items))()
+    for i, (src, off, rows, row_bytes, pitch) in enumerate(items):
+        arr[i] = GatherItem(src if isinstance(src, int) else src.data_ptr(), off, rows, row_bytes, pitch)
+    call("ppo_pack", arr, len(items), dst if isinstance(dst, int) else dst.data_ptr(), _stream(stream))
+
+
+def transfer(direction, segments, copy_stream, wait_event=None, done_event=None):
+    """segments: list of (device_ptr, host_ptr, nbytes); events: raw cudaEvent_t ints or None."""
+    arr = (Segment * len(segments))()
+    for i, (d, h, n) in enumerate(segments):
+        arr[i] = Segment(d, h, n)
+    call("ppo_transfer", direction, arr, len(segments), copy_stream, wait_event, done_event)
+
+
+class PinnedPool:
+    """Preallocated page-locked host arena carved into host bins (no per-step alloc)."""
+
+    def __init__(self, nbytes: int):
+        self._h = ctypes.c_void_p()
+        call("ppo_pool_create", int(nbytes), ctypes.byref(self._h))
+        self.base = int(load().ppo_pool_base(self._h))
+        self.nbytes = int(nbytes)
+        self._cursor = 0
+
+    def carve(self, nbytes: int, align: int = 4096) -> int:
+        start = (self._cursor + align - 1) // align * align
+        if start + nbytes > self.nbytes:
+            raise MemoryError(f"pinned pool exhausted: need {nbytes} at {start}, pool {self.nbytes}")
+        self._cursor = start + nbytes
+        return self.base + start
+
+    def close(self):
+        if self._h:
+            call("ppo_pool_destroy", self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NcclComm:
+    """Point-to-point communicator (K8) created from a unique id shared by the host runtime."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        call("ppo_comm_unique_id", buf)
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._h = ctypes.c_void_p()
+        call("ppo_comm_init", buf, nranks, rank, device, ctypes.byref(self._h))
+        self.nranks, self.rank = nranks, rank
+
+    def p2p(self, ops, stream):
+        """ops: list of (is_send, peer, ptr, nbytes); one NCCL group on ``stream`` (raw handle)."""
+        arr = (P2POp * len(ops))()
+        for i, (is_send, peer, ptr, n) in enumerate(ops):
+            arr[i] = P2POp(1 if is_send else 0, peer, ptr, n)
+        call("ppo_p2p", self._h, arr, len(ops), stream)
+
+    def close(self):
+        if self._h:
+            call("ppo_comm_destroy", self._h)
+            self._h = ctypes.c_void_p()

@@ -1,0 +1,149 @@
+"""K1-K5 kernel parity on the B200 against the numpy oracle (oracle/ops.py).
+
+Bars: dropout keep-masks bit-exact (Philox integer compare); pack and the
+offload->reload round trip bit-exact; LayerNorm / GeLU within bf16 output
+rounding (stated per test)."""
+
+import numpy as np
+import pytest
+
+from oracle import ops as ref
+from oracle.philox import keep_mask
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2503_01328_b200.runtime import native  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def bf(x):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(DEV).bfloat16()
+
+
+def npf(t):
+    return t.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("n,p,seed,offset", [(8, 0.1, 42, 0), (4096, 0.1, 42, 7), (1 << 20, 0.5, 2**40 + 3, 2**33 + 5), (64, 0.0, 1, 1)])
+def test_dropout_mask_bit_exact(n, p, seed, offset):
+    x = torch.ones(n, device=DEV, dtype=torch.bfloat16)
+    y = torch.empty_like(x)
+    native.dropout(x, y, p, seed, offset)
+    torch.cuda.synchronize()
+    got = npf(y) != 0
+    assert np.array_equal(got, keep_mask(n, p, seed, offset))
+    if p > 0:
+        kept = npf(y)[got]
+        assert np.all(kept == np.float32(ref.bf16_round(np.float32(1.0 / (1.0 - p)))))
+
+
+@pytest.mark.parametrize("rows,h", [(1, 256), (37, 256), (512, 2048), (64, 5120), (16, 8192), (9, 264)])
+def test_layernorm_fwd(rows, h):
+    rng = np.random.default_rng(rows * h)
+    x = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32) * 3 + 1)
+    gamma = rng.standard_normal(h).astype(np.float32)
+    beta = rng.standard_normal(h).astype(np.float32)
+    y = torch.empty(rows, h, device=DEV, dtype=torch.bfloat16)
+    native.layernorm_fwd(bf(x), torch.from_numpy(gamma).to(DEV), torch.from_numpy(beta).to(DEV), y)
+    want = ref.layernorm(x, gamma, beta)
+    # bf16 output: |err| <= 2^-8 relative of the value (+ tiny fp32 reduction slack)
+    np.testing.assert_allclose(npf(y), want, rtol=2 ** -8, atol=1e-3 * np.abs(gamma).max())
+
+
+@pytest.mark.parametrize("rows,h,p", [(300, 256, 0.1), (128, 2048, 0.1), (33, 4096, 0.0)])
+def test_residual_dropout_ln(rows, h, p):
+    rng = np.random.default_rng(h)
+    resid = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32))
+    branch = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32))
+    gamma = (1 + 0.1 * rng.standard_normal(h)).astype(np.float32)
+    beta = (0.1 * rng.standard_normal(h)).astype(np.float32)
+    out = torch.empty(rows, h, device=DEV, dtype=torch.bfloat16)
+    ln = torch.empty_like(out)
+    native.residual_dropout_ln_fwd(bf(resid), bf(branch), out, torch.from_numpy(gamma).to(DEV),
+                                   torch.from_numpy(beta).to(DEV), ln, p, 42, 99)
+    want_out = ref.residual_dropout(resid, branch, p, 42, 99)
+    # out = bf16(resid + mask*branch*scale): the device may fuse the multiply-add
+    # (one rounding instead of two) -> at most 1 bf16 ulp apart, masks identical
+    assert ref.bf16_ulp_diff(npf(out), want_out).max() <= 1
+    np.testing.assert_allclose(npf(ln), ref.layernorm(npf(out), gamma, beta), rtol=2 ** -7, atol=2e-2)
+
+
+@pytest.mark.parametrize("rows,h,with_resid,p", [(200, 256, True, 0.1), (64, 2048, False, 0.0), (40, 5120, True, 0.1)])
+def test_layernorm_bwd(rows, h, with_resid, p):
+    rng = np.random.default_rng(rows + h)
+    x = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32) * 2)
+    dy = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32))
+    rg = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32))
+    gamma = (1 + 0.1 * rng.standard_normal(h)).astype(np.float32)
+    dx = torch.empty(rows, h, device=DEV, dtype=torch.bfloat16)
+    drop = torch.empty_like(dx) if p > 0 else None
+    dgamma = torch.zeros(h, device=DEV)
+    dbeta = torch.zeros(h, device=DEV)
+    native.layernorm_bwd(bf(x), torch.from_numpy(gamma).to(DEV), bf(dy), bf(rg) if with_resid else None, dx, dgamma,
+                         dbeta, drop_out=drop, p=p, drop_seed=5, drop_offset=11)
+    want_dx, want_dg, want_db = ref.layernorm_bwd(x, gamma, dy)
+    if with_resid:
+        want_dx = want_dx + rg
+    np.testing.assert_allclose(npf(dx), want_dx, rtol=2 ** -7, atol=3e-2)
+    np.testing.assert_allclose(dgamma.cpu().numpy(), want_dg, rtol=1e-3, atol=1e-3 * rows)
+    np.testing.assert_allclose(dbeta.cpu().numpy(), want_db, rtol=1e-3, atol=1e-3 * rows)
+    if drop is not None:
+        # bit-exact: the fused replay equals the standalone dropout of the stored dx
+        alone = torch.empty_like(dx)
+        native.dropout(dx, alone, p, 5, 11)
+        assert torch.equal(alone, drop)
+
+
+@pytest.mark.parametrize("n", [8, 4096, 1 << 20])
+def test_gelu_fwd_bwd(n):
+    rng = np.random.default_rng(n)
+    f = ref.bf16_round(rng.standard_normal(n).astype(np.float32) * 3)
+    dg = ref.bf16_round(rng.standard_normal(n).astype(np.float32))
+    g = torch.empty(n, device=DEV, dtype=torch.bfloat16)
+    native.gelu_fwd(bf(f), g)
+    np.testing.assert_allclose(npf(g), ref.gelu(f), rtol=2 ** -7, atol=1e-6)
+    g2 = torch.empty_like(g)
+    df = bf(dg)
+    native.gelu_bwd(bf(f), df, g2, df)  # df aliases dg (in place)
+    assert torch.equal(g, g2)
+    np.testing.assert_allclose(npf(df), dg * ref.gelu_grad(f), rtol=2 ** -7, atol=1e-5)
+
+
+def test_pack_gather_bit_exact():
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 256, 4096 * 3, dtype=np.uint8)
+    b = rng.integers(0, 256, 64 * 96, dtype=np.uint8)  # 64 rows x 96 B, pitch 96, take 48 B/row
+    ta, tb = torch.from_numpy(a).to(DEV), torch.from_numpy(b).to(DEV)
+    dst = torch.zeros(16384, dtype=torch.uint8, device=DEV)
+    items = [(ta, 0, 1, a.size, 0), (tb, 12288, 64, 48, 96)]
+    native.pack(items, dst)
+    want = ref.pack([(a, 0, 1, a.size, 0), (b, 12288, 64, 48, 96)], 16384)
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+def test_offload_reload_round_trip_bit_exact():
+    """K2: device slab -> pinned bins -> fresh device slab, every byte identical."""
+    from paper_2503_01328_b200.runtime.layout import make_layout
+
+    lay = make_layout(layers=2, seq=512, hidden=256, heads=4, head_grad=True)
+    src = torch.randint(0, 256, (lay.slab_bytes,), dtype=torch.uint8, device=DEV)
+    back = torch.zeros_like(src)
+    pool = native.PinnedPool(lay.host_bytes + 8192)
+    bins = tuple(pool.carve(b) for b in lay.bins)
+    copy = torch.cuda.Stream()
+    done_out, done_in = torch.cuda.Event(), torch.cuda.Event()
+    ready = torch.cuda.Event()
+    ready.record()
+    native.transfer(native.PPO_D2H, lay.segments(src.data_ptr(), bins), copy.cuda_stream, ready.cuda_event, None)
+    done_out.record(copy)
+    native.transfer(native.PPO_H2D, lay.segments(back.data_ptr(), bins), copy.cuda_stream, None, None)
+    done_in.record(copy)
+    done_in.synchronize()
+    assert torch.equal(src, back)
+    assert lay.payload_bytes == 2 * 20 * 512 * 256
+    pool.close()
