@@ -1,0 +1,549 @@
+"""The measured pipeline runner: drop-in for the reference's ``simulate``.
+
+``execute(sched, plan, ...)`` runs a lowered per-rank program (``lower.py``) on
+the B200: compute on one stream, D2H/H2D on a dedicated copy stream (two in
+``stream_mode="dual"``), stage-boundary sends/receives on per-edge streams, all
+ordered by CUDA events -- no host synchronisation inside an iteration.  It
+returns a ``SimTrace`` (reference pkg/src/ppoff/sim.py:44-102) whose times are
+CUDA-event measurements in seconds, so ``peak_memory``, ``bubble_time``,
+``summary()`` and the reference's analysis/render layers consume it unchanged.
+
+Three ways to run a program:
+
+* multi-process, one rank per GPU (``torchrun``), boundary over NCCL (K8)
+  through ``libppo_b200.so`` with one 2-rank communicator per directed edge;
+* ``virtual``: every rank of the schedule in one process on one GPU, boundary
+  through a local channel (used by the single-GPU parity tests);
+* ``emulate``: one rank alone with a loopback boundary (synthetic upstream
+  activation / downstream gradient), the single-GPU benchmark of one rank of a
+  PP=d schedule.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import torch
+
+from ..costs import ModelSpec
+from ..ir import MemoryTimeline
+from ..offload import OffloadPlan
+from ..schedule_types import Pass, PassKind, Schedule
+from ..sim import SimTrace
+from . import native
+from .lower import RING, Program, lower
+from .model import ModelConfig, SlabView, Stage, stage_layers
+
+STREAMS = ("compute", "copy", "copy_h2d", "recv_act", "send_act", "recv_grad", "send_grad")
+TIMED = ("F_start", "F_end", "B_start", "B_end", "D2H", "H2D", "D2H_start", "H2D_start")
+
+
+class DeadlockError(RuntimeError):
+    pass
+
+
+# --------------------------------------------------------------------- transports
+
+
+class LocalTransport:
+    """Boundary channel between virtual ranks living in one process (one GPU).
+
+    A send snapshots the buffer into a fresh channel tensor on the sender's
+    stream; the matching receive (same channel, same index) waits on that copy's
+    event.  Receivers that run ahead of their sender report "not yet" and the
+    cooperative driver switches rank.
+    """
+
+    def __init__(self):
+        self.posted = {}
+        self.sent = {}
+        self.got = {}
+        self.keep = []
+
+    def send(self, rank, op, buf, stream) -> bool:
+        ch = (op.kind[5:].lower(), rank, op.peer)
+        idx = self.sent.get(ch, 0)
+        with torch.cuda.stream(stream):
+            snap = buf.clone()
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.posted[(ch, idx)] = (ev, snap)
+        self.sent[ch] = idx + 1
+        return True
+
+    def recv(self, rank, op, buf, stream) -> bool:
+        ch = (op.kind[5:].lower(), op.peer, rank)
+        idx = self.got.get(ch, 0)
+        item = self.posted.get((ch, idx))
+        if item is None:
+            return False
+        ev, snap = item
+        stream.wait_event(ev)
+        with torch.cuda.stream(stream):
+            buf.copy_(snap)
+        self.keep.append(snap)
+        self.got[ch] = idx + 1
+        return True
+
+    def end_iteration(self):
+        self.posted.clear()
+        self.sent.clear()
+        self.got.clear()
+        self.keep.clear()
+
+
+class NcclTransport:
+    """One 2-rank NCCL communicator per directed pipeline edge and direction.
+
+    Each channel carries one kind of traffic one way (rank ``src`` sends, rank
+    ``dst`` receives) in the same (stage, mb) order on both sides, so no send can
+    wait behind an unrelated receive -- the ring deadlock of a shared
+    communicator cannot form, also across the interleaved wrap d-1 -> 0.
+    """
+
+    def __init__(self, rank: int, world: int, device: int, edges):
+        import torch.distributed as dist
+
+        self.rank = rank
+        self.comms = {}
+        for ch in sorted(set(edges)):  # identical global order on every rank
+            kind, src, dst = ch
+            if rank not in (src, dst):
+                continue
+            key = f"ppo_uid/{kind}/{src}/{dst}"
+            store = _store()
+            if rank == src:
+                uid = native.NcclComm.unique_id()
+                store.set(key, uid.hex())
+            else:
+                uid = bytes.fromhex(store.get(key).decode())
+            self.comms[ch] = native.NcclComm(uid, 2, 0 if rank == src else 1, device)
+        if dist.is_initialized():
+            dist.barrier()
+
+    def send(self, rank, op, buf, stream) -> bool:
+        comm = self.comms[(op.kind[5:].lower(), rank, op.peer)]
+        comm.p2p([(True, 1, buf.data_ptr(), buf.numel() * buf.element_size())], stream.cuda_stream)
+        return True
+
+    def recv(self, rank, op, buf, stream) -> bool:
+        comm = self.comms[(op.kind[5:].lower(), op.peer, rank)]
+        comm.p2p([(False, 0, buf.data_ptr(), buf.numel() * buf.element_size())], stream.cuda_stream)
+        return True
+
+    def end_iteration(self):
+        pass
+
+    def close(self):
+        for c in self.comms.values():
+            c.close()
+        self.comms.clear()
+
+
+def _store():
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise RuntimeError("NCCL transport needs torch.distributed initialised (torchrun)")
+    from torch.distributed.distributed_c10d import _get_default_store
+
+    return _get_default_store()
+
+
+def pipeline_edges(sched: Schedule):
+    edges = []
+    for s in range(sched.num_stages - 1):
+        a, b = sched.placement[s], sched.placement[s + 1]
+        if a != b:
+            edges.append(("act", a, b))
+            edges.append(("grad", b, a))
+    return edges
+
+
+# ---------------------------------------------------------------------- runner
+
+
+@dataclass
+class IterationStats:
+    seconds: float
+    events: dict = field(default_factory=dict)
+
+
+class RankRunner:
+    """Issues one rank's lowered program onto CUDA streams, iteration after iteration."""
+
+    def __init__(self, program: Program, cfg: ModelConfig, sched: Schedule, microbatches: int, device,
+                 transport=None, emulate: bool = False, params=None, seed: int = 1234, optimizer: str = "sgd",
+                 lr: float = 1e-4, verify_roundtrip: bool = False):
+        torch_ = native.require_cuda()
+        self.torch = torch_
+        self.prog, self.cfg, self.sched, self.m = program, cfg, sched, microbatches
+        self.device = torch.device(device)
+        self.rank = program.rank
+        self.transport = transport
+        self.emulate = emulate
+        my_stages = [s for s in range(sched.num_stages) if sched.placement[s] == self.rank]
+        with torch.cuda.device(self.device):
+            self.stages = {
+                s: Stage(cfg, s, sched.num_stages, microbatches, self.device, params=params,
+                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed)
+                for s in my_stages
+            }
+            self.slab_bytes = max(st.layout.slab_bytes for st in self.stages.values())
+            self.host_bytes = max(st.layout.host_bytes for st in self.stages.values())
+            self.arena = torch.empty(max(1, program.n_slabs) * self.slab_bytes, dtype=torch.uint8, device=self.device)
+            self.pool = None
+            self.host_slot_base = []
+            if program.n_host_slots:
+                slot_bytes = (self.host_bytes + 4095) // 4096 * 4096
+                self.pool = native.PinnedPool(program.n_host_slots * slot_bytes)
+                self.host_slot_base = [self.pool.carve(slot_bytes) for _ in range(program.n_host_slots)]
+            s_, h = cfg.seq, cfg.hidden
+            mk = lambda: torch.empty(s_, h, dtype=torch.bfloat16, device=self.device)  # noqa: E731
+            self.rings = {k: [mk() for _ in range(RING)] for k in ("recv_act", "send_act", "recv_grad", "send_grad")}
+            self.scratch_out = mk()
+            gen = torch.Generator(device="cpu").manual_seed(7 + self.rank)
+            self.synthetic_x = (torch.randn(s_, h, generator=gen) * 0.5).to(self.device, torch.bfloat16)
+            self.synthetic_dy = (torch.randn(s_, h, generator=gen) * 1e-3).to(self.device, torch.bfloat16)
+            self.streams = {name: torch.cuda.Stream(self.device) for name in STREAMS}
+            self.events = {}
+            self.views = {}
+        self.optimizer = optimizer
+        self.lr = lr
+        self.verify_roundtrip = verify_roundtrip
+        self.digests = {}  # (stage, mb) -> [digest at F end, digest at B start]
+        self._adam = None
+        self.cursor = 0
+        self.iteration = 0
+        self.tokens = None
+        self.t0 = None
+
+    # -------------------------------------------------------------- plumbing
+    def ev(self, key):
+        e = self.events.get(key)
+        if e is None:
+            timed = key[0] in TIMED
+            e = torch.cuda.Event(enable_timing=timed)
+            self.events[key] = e
+        return e
+
+    def slab(self, idx: int, stage: int) -> SlabView:
+        key = (idx, stage)
+        v = self.views.get(key)
+        if v is None:
+            lay = self.stages[stage].layout
+            base = self.arena[idx * self.slab_bytes: idx * self.slab_bytes + lay.slab_bytes]
+            v = SlabView(lay, base)
+            self.views[key] = v
+        return v
+
+    def host_bins(self, slot: int, stage: int):
+        lay = self.stages[stage].layout
+        base, acc, out = self.host_slot_base[slot], 0, []
+        for b in lay.bins:
+            out.append(base + acc)
+            acc += b
+        return tuple(out)
+
+    # ------------------------------------------------------------ iteration
+    def begin_iteration(self, tokens_dev: torch.Tensor | None):
+        """tokens_dev: [m, s+1] int64 already on this device (first/last stages use it)."""
+        self.cursor = 0
+        self.tokens = tokens_dev
+        comp = self.streams["compute"]
+        comp.wait_stream(torch.cuda.current_stream(self.device))
+        for name, st in self.streams.items():
+            if name != "compute":
+                st.wait_stream(comp)
+        for st in self.stages.values():
+            with torch.cuda.stream(comp):
+                st.zero_grad()
+        self.t0 = torch.cuda.Event(enable_timing=True)
+        self.t0.record(comp)
+
+    def done(self) -> bool:
+        return self.cursor >= len(self.prog.ops)
+
+    def issue_next(self) -> bool:
+        """Issue the next op; False when it must wait for another (virtual) rank."""
+        op = self.prog.ops[self.cursor]
+        stream = self.streams[op.stream]
+        if op.kind in ("RECV_ACT", "RECV_GRAD"):
+            for key in op.waits:
+                stream.wait_event(self.ev(key))
+            buf = self.rings["recv_act" if op.kind == "RECV_ACT" else "recv_grad"][op.ring]
+            if not self.transport.recv(self.rank, op, buf, stream):
+                return False
+            self.ev(op.records[0]).record(stream)
+            self.cursor += 1
+            return True
+        for key in op.waits:
+            stream.wait_event(self.ev(key))
+        if op.kind == "F":
+            self._forward(op, stream)
+        elif op.kind == "B":
+            self._backward(op, stream)
+        elif op.kind in ("OFFLOAD", "RELOAD"):
+            self._transfer(op, stream)
+        elif op.kind in ("SEND_ACT", "SEND_GRAD"):
+            buf = self.rings["send_act" if op.kind == "SEND_ACT" else "send_grad"][op.ring]
+            self.transport.send(self.rank, op, buf, stream)
+            self.ev(op.records[0]).record(stream)
+        else:  # pragma: no cover
+            raise ValueError(op.kind)
+        self.cursor += 1
+        return True
+
+    def _forward(self, op, stream):
+        s, j = op.stage, op.mb
+        st = self.stages[s]
+        self.ev(("F_start", s, j)).record(stream)
+        with torch.cuda.stream(stream):
+            slab = self.slab(op.slab, s)
+            if st.first:
+                st.embed(slab, self.tokens[j, :-1])
+            elif op.ring is not None:
+                slab.get(0, "x").copy_(self.rings["recv_act"][op.ring])
+            else:  # emulated upstream stage
+                slab.get(0, "x").copy_(self.synthetic_x)
+            self.ev(("F_in", s, j)).record(stream)
+            out = None
+            if not st.last:
+                out = self.rings["send_act"][op.send_ring] if op.send_ring is not None else self.scratch_out
+            st.forward(slab, j, self.iteration, out=out, targets=self.tokens[j, 1:] if st.last else None)
+            if self.verify_roundtrip and (s, j) in self.prog.offloaded:
+                self.digests[(s, j)] = [_digest(slab.base), None]
+        self.ev(("F_end", s, j)).record(stream)
+
+    def _backward(self, op, stream):
+        s, j = op.stage, op.mb
+        st = self.stages[s]
+        self.ev(("B_start", s, j)).record(stream)
+        with torch.cuda.stream(stream):
+            slab = self.slab(op.slab, s)
+            if self.verify_roundtrip and (s, j) in self.prog.offloaded:
+                self.digests[(s, j)][1] = _digest(slab.base)
+            dy = None
+            if not st.last:
+                dy = self.rings["recv_grad"][op.ring] if op.ring is not None else self.synthetic_dy
+            dx_out = None
+            if not st.first:
+                dx_out = self.rings["send_grad"][op.send_ring] if op.send_ring is not None else self.scratch_out
+            st.backward(slab, j, self.iteration, dy=dy, dx_out=dx_out, tokens=self.tokens[j, :-1] if st.first else None)
+        self.ev(("B_end", s, j)).record(stream)
+
+    def _transfer(self, op, stream):
+        s, j = op.stage, op.mb
+        lay = self.stages[s].layout
+        slab_ptr = self.arena.data_ptr() + op.slab * self.slab_bytes
+        segs = lay.segments(slab_ptr, self.host_bins(op.host_slot, s))
+        tag = "D2H" if op.kind == "OFFLOAD" else "H2D"
+        self.ev((tag + "_start", s, j)).record(stream)
+        native.transfer(native.PPO_D2H if op.kind == "OFFLOAD" else native.PPO_H2D, segs, stream.cuda_stream)
+        self.ev((tag, s, j)).record(stream)
+
+    def end_iteration(self):
+        comp = self.streams["compute"]
+        for name, st in self.streams.items():
+            if name != "compute":
+                comp.wait_stream(st)
+        with torch.cuda.stream(comp):
+            self._optimizer_step()
+        self.t_end = torch.cuda.Event(enable_timing=True)
+        self.t_end.record(comp)
+        torch.cuda.current_stream(self.device).wait_stream(comp)
+        self.iteration += 1
+
+    def _optimizer_step(self):
+        if self.optimizer == "none":
+            return
+        if self.optimizer == "sgd":
+            for st in self.stages.values():
+                st.sgd_step(self.lr)
+            return
+        if self._adam is None:
+            params = [t for st in self.stages.values() for t in st.master.values()]
+            for p in params:
+                p.requires_grad_(False)
+            self._adam = torch.optim.AdamW(params, lr=self.lr, fused=True)
+            self._adam_pairs = [(st, n) for st in self.stages.values() for n in st.master]
+        for (st, n) in self._adam_pairs:
+            st.master[n].grad = st.g[n]
+        self._adam.step()
+        for (st, n) in self._adam_pairs:
+            st.w[n].copy_(st.master[n])
+
+    def loss_sum(self) -> torch.Tensor | None:
+        for st in self.stages.values():
+            if st.last:
+                return st.loss_sum
+        return None
+
+    # -------------------------------------------------------- measured trace
+    def measured_passes(self) -> list[Pass]:
+        """CUDA-event times (seconds from iteration start) of this rank's passes."""
+        t0 = self.t0
+        sec = lambda ev: Fraction(t0.elapsed_time(ev)) / 1000  # noqa: E731
+        out = []
+        for (kind, s, j) in self.prog.compute_order:
+            a, b = self.events[(f"{kind}_start", s, j)], self.events[(f"{kind}_end", s, j)]
+            st = sec(a)
+            out.append(Pass(PassKind(kind), self.rank, s, j, st, sec(b) - st))
+        for op in self.prog.ops:
+            if op.kind in ("OFFLOAD", "RELOAD"):
+                tag = "D2H" if op.kind == "OFFLOAD" else "H2D"
+                st = sec(self.events[(tag + "_start", op.stage, op.mb)])
+                en = sec(self.events[(tag, op.stage, op.mb)])
+                out.append(Pass(PassKind(op.kind), self.rank, op.stage, op.mb, st, en - st))
+        return out
+
+    def iteration_seconds(self) -> float:
+        return self.t0.elapsed_time(self.t_end) / 1000.0
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool = None
+
+
+def _digest(buf: torch.Tensor) -> torch.Tensor:
+    """Order-independent integer digest of a byte buffer (exact, deterministic)."""
+    words = buf.view(torch.int32).to(torch.int64)
+    weights = torch.arange(words.numel(), device=buf.device, dtype=torch.int64) % 65521 + 1
+    return torch.stack([words.sum(), (words * weights).sum()])
+
+
+def roundtrip_mismatches(runners) -> list:
+    """(rank, stage, mb) whose reloaded slab differs from what was offloaded."""
+    bad = []
+    for r in runners:
+        for (s, j), (a, b) in r.digests.items():
+            if b is None or not torch.equal(a, b):
+                bad.append((r.rank, s, j))
+    return bad
+
+
+def drive(runners: list[RankRunner]):
+    """Cooperatively issue every runner's program (virtual ranks share one host thread)."""
+    while True:
+        progressed = False
+        pending = False
+        for r in runners:
+            while not r.done():
+                if not r.issue_next():
+                    break
+                progressed = True
+            pending |= not r.done()
+        if not pending:
+            return
+        if not progressed:
+            stuck = [(r.rank, r.prog.ops[r.cursor].key) for r in runners if not r.done()]
+            raise DeadlockError(f"virtual pipeline cannot make progress: {stuck}")
+
+
+def measured_trace(sched: Schedule, passes: list[Pass], model: ModelSpec | None = None,
+                   units_bytes: int = 0) -> SimTrace:
+    """Assemble a reference-compatible ``SimTrace`` from measured passes (all ranks)."""
+    ends = {(p.kind, p.stage, p.microbatch): p.end for p in passes}
+    starts = {(p.kind, p.stage, p.microbatch): p.start for p in passes}
+    reload_of = {(p.stage, p.microbatch): (PassKind.RELOAD, p.stage, p.microbatch) for p in passes if p.kind == PassKind.RELOAD}
+    offload_of = {(p.stage, p.microbatch): (PassKind.OFFLOAD, p.stage, p.microbatch) for p in passes if p.kind == PassKind.OFFLOAD}
+    u = sched.units_per_stage
+    dev_events = [[] for _ in range(sched.devices)]
+    host = []
+    present = {p.device for p in passes}
+    for dev in range(sched.devices):
+        if dev not in present:
+            continue
+        for p in sched.device_passes[dev]:
+            pair = (p.stage, p.microbatch)
+            if p.kind == PassKind.F:
+                dev_events[dev].append((starts[(PassKind.F,) + pair], p.stage, u))
+                if pair in reload_of and pair in offload_of:
+                    dev_events[dev].append((ends[offload_of[pair]], p.stage, -u))
+                    dev_events[dev].append((starts[reload_of[pair]], p.stage, u))
+                    host.append((ends[offload_of[pair]], dev, u))
+                    host.append((ends[reload_of[pair]], dev, -u))
+            elif p.kind == PassKind.B:
+                dev_events[dev].append((ends[(PassKind.B,) + pair], p.stage, -u))
+    order = lambda e: (e[0], e[2])  # noqa: E731
+    busy = tuple(sum((p.duration for p in passes if p.device == d and p.kind in (PassKind.F, PassKind.B, PassKind.W)), Fraction(0))
+                 for d in range(sched.devices))
+    return SimTrace(
+        schedule=sched,
+        passes=tuple(sorted(passes, key=lambda p: (p.start, p.device, str(p.kind), p.stage, p.microbatch))),
+        makespan=max((p.end for p in passes), default=Fraction(0)),
+        device_busy=busy,
+        memory=MemoryTimeline(sched.devices, units_bytes, tuple(tuple(sorted(ev, key=order)) for ev in dev_events)),
+        host_events=tuple(sorted(host, key=order)),
+        contention_log=(),
+        bytes_per_unit=units_bytes,
+    )
+
+
+@dataclass
+class RunResult:
+    trace: SimTrace
+    iteration_seconds: list
+    losses: list
+    programs: dict
+    runners: list
+    slab_bytes: int
+    peak_slabs: dict  # rank -> arena slabs (= planned peak units)
+    host_slots: dict
+
+
+def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelConfig, microbatches: int | None = None,
+            mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
+            stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
+            lr: float = 1e-4, verify_roundtrip: bool = False) -> RunResult:
+    """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
+
+    mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
+    boundary) or "nccl" (this process is ``rank`` of a torchrun job).
+    ``tokens``: [m, s+1] int64 host tensor (pinned for the e2e path).
+    """
+    native.require_cuda()
+    m = microbatches or sched.microbatches
+    dev = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+    if mode == "virtual":
+        ranks = list(range(sched.devices))
+    else:
+        ranks = [rank if rank is not None else 0]
+    programs = {r: lower(sched, plan, r, stream_mode=stream_mode, emulate_neighbors=(mode == "emulate")) for r in ranks}
+    transport = None
+    if mode == "virtual":
+        transport = LocalTransport()
+    elif mode == "nccl":
+        import torch.distributed as dist
+
+        transport = NcclTransport(ranks[0], dist.get_world_size(), dev.index, pipeline_edges(sched))
+    runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
+                          params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip) for r in ranks]
+    if tokens is None:
+        gen = torch.Generator().manual_seed(0)
+        tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
+    tokens_dev = torch.empty(tokens.shape, dtype=torch.int64, device=dev)
+    secs, losses = [], []
+    for it in range(warmup + iters):
+        tokens_dev.copy_(tokens, non_blocking=True)
+        for r in runners:
+            r.begin_iteration(tokens_dev)
+        drive(runners)
+        for r in runners:
+            r.end_iteration()
+        if transport is not None:
+            torch.cuda.synchronize(dev)
+            transport.end_iteration()
+        if it >= warmup:
+            torch.cuda.synchronize(dev)
+            secs.append(max(r.iteration_seconds() for r in runners))
+            ls = [r.loss_sum() for r in runners if r.loss_sum() is not None]
+            losses.append(float(ls[0]) / m if ls else None)
+    passes = [p for r in runners for p in r.measured_passes()]
+    slab_bytes = max(r.slab_bytes for r in runners)
+    trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
+    return RunResult(trace, secs, losses, programs, runners, slab_bytes,
+                     {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners})

@@ -1,0 +1,370 @@
+"""Lower (Schedule, OffloadPlan, rank) into a static, event-anchored program.
+
+The reference runner is a clock-driven simulation (pkg/src/ppoff/sim.py:141-413):
+reloads are floored at absolute slot times (sim.py:177-181) and memory is freed
+at D2H end (sim.py:477-479).  A GPU only knows streams and events, so lowering
+turns every time relation into an event relation, using the runner model of
+this package (``sim.simulate``, bit-exact with the reference) as the witness
+timeline:
+
+* compute stream  -- F/B passes in ``Schedule.device_passes`` order (op-order
+  parity: the executed order IS the reference's order).
+* copy stream(s)  -- OFFLOAD/RELOAD in the order the runner model realises them,
+  which equals ``OffloadPlan.streams[d].transfers`` slot order whenever the plan
+  has no late reloads; ``stream_mode="dual"`` splits D2H and H2D.
+* reload anchors  -- a RELOAD waits for the start event of the compute pass that
+  is running at its realised start (or the end event of the last pass that
+  finished before it): the event form of the slot floor.
+* device slabs    -- a fixed arena of K slabs, K = the realised peak residency;
+  each (stage, mb) residency interval gets a slab by greedy interval colouring
+  and waits for the release event (D2H done or B end) of the slab's previous
+  occupant, so the arena can never exceed the planned peak.
+* host slots      -- the same for pinned host bins over [D2H start, H2D end).
+* stage boundary  -- RECV/SEND ops on per-edge channels (2-rank NCCL comms in
+  the multi-process runtime); activations and gradients are staged through
+  rings of R buffers so a send never waits on the consumer's compute.
+
+Every wait points to an event whose witness time is <= the waiter's, so the
+wait graph is acyclic; ``host_order`` topologically sorts all ops so every event
+is recorded on the host before any stream is told to wait for it.
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+from ..offload import OffloadPlan
+from ..schedule_types import PassKind, Schedule
+from ..sim import simulate
+
+F, B, W = PassKind.F, PassKind.B, PassKind.W
+OFF, REL = PassKind.OFFLOAD, PassKind.RELOAD
+
+RING = 2  # boundary buffers per channel direction
+
+
+@dataclass
+class Op:
+    kind: str  # F B RECV_ACT SEND_ACT RECV_GRAD SEND_GRAD OFFLOAD RELOAD
+    stage: int
+    mb: int
+    stream: str  # compute | copy | copy_h2d | recv_act | send_act | recv_grad | send_grad
+    t: Fraction  # witness (modelled) issue time
+    waits: list = field(default_factory=list)
+    records: list = field(default_factory=list)
+    slab: int | None = None
+    host_slot: int | None = None
+    ring: int | None = None
+    peer: int | None = None  # remote rank of a boundary op
+    anchor: tuple | None = None  # reload anchor event
+    send_ring: int | None = None  # ring slot of the boundary send this compute op feeds
+
+    @property
+    def key(self):
+        return (self.kind, self.stage, self.mb)
+
+
+@dataclass
+class Program:
+    rank: int
+    devices: int
+    ops: list  # host issue order
+    n_slabs: int
+    n_host_slots: int
+    offloaded: set
+    witness_makespan: Fraction
+    witness_peak_units: int
+    compute_order: list  # [(kind, stage, mb)] == sched.device_passes[rank]
+    copy_order: dict  # stream -> [(kind, stage, mb)]
+    recv_orders: dict  # channel -> [(stage, mb)]
+    send_orders: dict
+
+    def ops_on(self, stream: str):
+        return [op for op in self.ops if op.stream == stream]
+
+
+def _colour(intervals):
+    """Greedy interval colouring. intervals: list of (start, end, key).
+
+    Frees sort before allocations at equal times (half-open residency, as in
+    ir.py:649).  Returns (assignment key -> (colour, previous occupant key or
+    None), n_colours).
+    """
+    events = []
+    for start, end, key in intervals:
+        events.append((start, 1, key))
+        events.append((end, 0, key))
+    events.sort(key=lambda e: (e[0], e[1]))
+    free: list = []  # heap of colour ids
+    last_holder: dict = {}
+    held: dict = {}
+    assignment = {}
+    n = 0
+    for _t, is_alloc, key in events:
+        if is_alloc:
+            if free:
+                c = heapq.heappop(free)
+            else:
+                c = n
+                n += 1
+            assignment[key] = (c, last_holder.get(c))
+            held[key] = c
+        else:
+            c = held.pop(key)
+            last_holder[c] = key
+            heapq.heappush(free, c)
+    return assignment, n
+
+
+def _anchor_for(t: Fraction, passes):
+    """Event that marks witness time t on a device's compute stream."""
+    before = None
+    for p in passes:
+        if p.start <= t < p.end:
+            return ("start", p.kind, p.stage, p.microbatch)
+        if p.end <= t:
+            before = p
+    if before is not None:
+        return ("end", before.kind, before.stage, before.microbatch)
+    return None
+
+
+def lower(
+    sched: Schedule,
+    plan: OffloadPlan | None,
+    rank: int,
+    stream_mode: str = "single",
+    emulate_neighbors: bool = False,
+) -> Program:
+    """Per-rank program.  ``emulate_neighbors`` drops cross-rank ops (the rank runs
+    alone with a loopback stage boundary, e.g. the single-GPU bench of one rank
+    of a PP=d schedule)."""
+    trace = simulate(sched, plan, stream_mode=stream_mode)
+    timed = {(p.kind, p.stage, p.microbatch): p for p in trace.passes}
+    my_passes = [timed[(p.kind, p.stage, p.microbatch)] for p in sched.device_passes[rank]]
+    if any(p.kind == W for p in my_passes):
+        raise NotImplementedError("split-backward (W) execution is the next row (SURVEY 8f-1)")
+    placement = sched.placement
+    last_stage = sched.num_stages - 1
+    ops: list[Op] = []
+
+    transfers = sorted((p for p in trace.transfer_passes() if p.device == rank), key=lambda p: (p.start, p.kind != OFF))
+    offloaded = {(p.stage, p.microbatch) for p in transfers if p.kind == REL}
+    d2h = {(p.stage, p.microbatch): p for p in transfers if p.kind == OFF}
+    h2d = {(p.stage, p.microbatch): p for p in transfers if p.kind == REL}
+    # a pair offloaded but never reloaded (cannot happen with plan_slots) is not supported
+    assert set(d2h) >= offloaded
+
+    # ---------------------------------------------------------------- slabs
+    intervals = []
+    for p in my_passes:
+        pair = (p.stage, p.microbatch)
+        if p.kind == F:
+            end = d2h[pair].end if pair in offloaded else timed[(B, p.stage, p.microbatch)].end
+            intervals.append((p.start, end, ("F",) + pair))
+            if pair in offloaded:
+                intervals.append((h2d[pair].start, timed[(B, p.stage, p.microbatch)].end, ("R",) + pair))
+    slab_of, n_slabs = _colour(intervals)
+    host_of, n_host = _colour([(d2h[pr].start, h2d[pr].end, ("H",) + pr) for pr in sorted(offloaded)])
+
+    def release_event(holder):
+        """Event that frees a slab held by ``holder`` (("F"|"R", stage, mb))."""
+        if holder is None:
+            return None
+        tag, s, j = holder
+        if tag == "F" and (s, j) in offloaded:
+            return ("D2H", s, j)
+        return ("B_end", s, j)
+
+    # --------------------------------------------------------- boundary rings
+    recv_orders: dict = {}
+    send_orders: dict = {}
+
+    def consumer_of(channel, idx):
+        """Event after which ring slot of the idx-th message on channel is free."""
+        prev = idx - RING
+        if prev < 0:
+            return None
+        s, j = recv_orders[channel][prev]
+        return ("F_in", s, j) if channel[0] == "act" else ("B_end", s, j)
+
+    compute_ops = []
+    for p in my_passes:
+        s, j = p.stage, p.microbatch
+        pair = (s, j)
+        if p.kind == F:
+            op = Op("F", s, j, "compute", p.start)
+            op.records = [("F_start", s, j), ("F_in", s, j), ("F_end", s, j)]
+            op.slab, prev = slab_of[("F",) + pair]
+            rel = release_event(prev)
+            if rel:
+                op.waits.append(rel)
+            if s > 0:
+                src = placement[s - 1]
+                if src == rank and not emulate_neighbors:
+                    raise NotImplementedError("consecutive stages on one device (d=1, v>1) are not lowered")
+                if not emulate_neighbors:
+                    ch = ("act", src, rank)
+                    lst = recv_orders.setdefault(ch, [])
+                    lst.append(pair)
+                    idx = len(lst) - 1
+                    r = Op("RECV_ACT", s, j, "recv_act", p.start, ring=idx % RING, peer=src)
+                    cons = consumer_of(ch, idx)
+                    if cons:
+                        r.waits.append(cons)
+                    r.records = [("RA", s, j)]
+                    ops.append(r)
+                    op.waits.append(("RA", s, j))
+                    op.ring = r.ring
+            compute_ops.append(op)
+            if s < last_stage:
+                dst = placement[s + 1]
+                if not emulate_neighbors and dst != rank:
+                    ch = ("act", rank, dst)
+                    lst = send_orders.setdefault(ch, [])
+                    lst.append(pair)
+                    idx = len(lst) - 1
+                    snd = Op("SEND_ACT", s, j, "send_act", p.end, ring=idx % RING, peer=dst)
+                    snd.waits = [("F_end", s, j)]
+                    snd.records = [("SA", s, j)]
+                    if idx >= RING:
+                        ps, pj = lst[idx - RING]
+                        op.waits.append(("SA", ps, pj))  # F may overwrite this send buffer
+                    op.send_ring = snd.ring
+                    ops.append(snd)
+                elif dst == rank and not emulate_neighbors:
+                    raise NotImplementedError("consecutive stages on one device (d=1, v>1) are not lowered")
+        else:  # B
+            op = Op("B", s, j, "compute", p.start)
+            op.records = [("B_start", s, j), ("B_end", s, j)]
+            if pair in offloaded:
+                op.waits.append(("H2D", s, j))
+                op.slab = slab_of[("R",) + pair][0]
+            else:
+                op.slab = slab_of[("F",) + pair][0]
+            if s < last_stage:
+                src = placement[s + 1]
+                if not emulate_neighbors and src != rank:
+                    ch = ("grad", src, rank)
+                    lst = recv_orders.setdefault(ch, [])
+                    lst.append(pair)
+                    idx = len(lst) - 1
+                    r = Op("RECV_GRAD", s, j, "recv_grad", p.start, ring=idx % RING, peer=src)
+                    cons = consumer_of(ch, idx)
+                    if cons:
+                        r.waits.append(cons)
+                    r.records = [("RG", s, j)]
+                    ops.append(r)
+                    op.waits.append(("RG", s, j))
+                    op.ring = r.ring
+            if s > 0:
+                dst = placement[s - 1]
+                if not emulate_neighbors and dst != rank:
+                    ch = ("grad", rank, dst)
+                    lst = send_orders.setdefault(ch, [])
+                    lst.append(pair)
+                    idx = len(lst) - 1
+                    snd = Op("SEND_GRAD", s, j, "send_grad", p.end, ring=idx % RING, peer=dst)
+                    snd.waits = [("B_end", s, j)]
+                    snd.records = [("SG", s, j)]
+                    if idx >= RING:
+                        ps, pj = lst[idx - RING]
+                        op.waits.append(("SG", ps, pj))
+                    op.send_ring = snd.ring
+                    ops.append(snd)
+            compute_ops.append(op)
+    ops.extend(compute_ops)
+
+    # ------------------------------------------------------------- transfers
+    copy_order: dict = {}
+    for p in transfers:
+        s, j = p.stage, p.microbatch
+        pair = (s, j)
+        if p.kind == OFF:
+            stream = "copy"
+            op = Op("OFFLOAD", s, j, stream, p.start)
+            op.waits = [("F_end", s, j)]
+            op.records = [("D2H", s, j)]
+            op.slab = slab_of[("F",) + pair][0]
+            op.host_slot, prev = host_of[("H",) + pair]
+            if prev is not None:
+                op.waits.append(("H2D", prev[1], prev[2]))
+        else:
+            stream = "copy" if stream_mode == "single" else "copy_h2d"
+            op = Op("RELOAD", s, j, stream, p.start)
+            op.slab, prev = slab_of[("R",) + pair]
+            op.host_slot = host_of[("H",) + pair][0]
+            op.waits = [("D2H", s, j)]
+            rel = release_event(prev)
+            if rel:
+                op.waits.append(rel)
+            anc = _anchor_for(p.start, my_passes)
+            if anc is not None:
+                which, kind, as_, aj = anc
+                op.anchor = ((f"{kind}_start" if which == "start" else f"{kind}_end"), as_, aj)
+                op.waits.append(op.anchor)
+            op.records = [("H2D", s, j)]
+        copy_order.setdefault(stream, []).append((op.kind, s, j))
+        ops.append(op)
+
+    ordered = host_order(ops)
+    # sanity: compute order is exactly the schedule's device order
+    got = [(op.kind, op.stage, op.mb) for op in ordered if op.stream == "compute"]
+    want = [(str(p.kind), p.stage, p.microbatch) for p in sched.device_passes[rank]]
+    assert got == want, "lowering changed the per-device op order"
+    peak = trace.memory.peak(rank)
+    return Program(
+        rank=rank, devices=sched.devices, ops=ordered, n_slabs=n_slabs, n_host_slots=n_host,
+        offloaded=offloaded, witness_makespan=trace.makespan, witness_peak_units=peak,
+        compute_order=want, copy_order=copy_order, recv_orders=recv_orders, send_orders=send_orders,
+    )
+
+
+_KIND_PRIORITY = {"OFFLOAD": 0, "RELOAD": 1, "SEND_ACT": 2, "SEND_GRAD": 2, "RECV_ACT": 3, "RECV_GRAD": 3, "F": 4, "B": 4}
+
+
+def host_order(ops: list[Op]) -> list[Op]:
+    """Topological order: stream FIFO order + record-before-wait, earliest witness time first."""
+    producers = {}
+    for i, op in enumerate(ops):
+        for ev in op.records:
+            producers[ev] = i
+    succ = [[] for _ in ops]
+    indeg = [0] * len(ops)
+    last_on = {}
+    order_in_stream = sorted(range(len(ops)), key=lambda i: (ops[i].stream, _stream_rank(ops, i)))
+    for i in order_in_stream:
+        st = ops[i].stream
+        if st in last_on:
+            succ[last_on[st]].append(i)
+            indeg[i] += 1
+        last_on[st] = i
+    for i, op in enumerate(ops):
+        for ev in op.waits:
+            j = producers.get(ev)
+            if j is None:
+                raise ValueError(f"{op.key} waits on {ev} that no op records")
+            if j != i:
+                succ[j].append(i)
+                indeg[i] += 1
+    heap = [(ops[i].t, _KIND_PRIORITY[ops[i].kind], i) for i in range(len(ops)) if indeg[i] == 0]
+    heapq.heapify(heap)
+    out = []
+    while heap:
+        _t, _k, i = heapq.heappop(heap)
+        out.append(ops[i])
+        for k in succ[i]:
+            indeg[k] -= 1
+            if indeg[k] == 0:
+                heapq.heappush(heap, (ops[k].t, _KIND_PRIORITY[ops[k].kind], k))
+    if len(out) != len(ops):
+        stuck = [ops[i].key for i in range(len(ops)) if indeg[i] > 0][:8]
+        raise RuntimeError(f"lowered program has a wait cycle near {stuck}")
+    return out
+
+
+def _stream_rank(ops, i):
+    """Position of op i within its stream: insertion order (already stream order)."""
+    return i

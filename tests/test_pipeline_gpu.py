@@ -1,0 +1,105 @@
+"""End-to-end pipelined runs on one B200 (all ranks of the schedule as virtual
+ranks in one process, boundary through the local channel).
+
+C1 (BASELINE.json configs[0]): tiny GPT, 4 layers, h=256, s=512, PP=4, 1F1B,
+8 microbatches, full offload at k=1/2 (build_1f1b_full_offload(4, 8, unit, 3/2)).
+Bars:
+* op order executed on every rank == Schedule.device_passes (reference order);
+* copy-stream order == OffloadPlan slot order (no late reloads at k=1/2);
+* every offloaded slab reloads bit-exact (integer digests, in situ);
+* loss within 2% and every gradient within 5% relative L2 of the serial fp32
+  oracle (bf16 activations/GEMM inputs vs fp32 everywhere);
+* offload on vs off: same loss to 1e-3 relative (only nondeterministic atomics
+  and cuDNN's dQ accumulation differ).
+"""
+
+from fractions import Fraction
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2503_01328_b200 as po  # noqa: E402
+from oracle import gpt as oracle_gpt  # noqa: E402
+from paper_2503_01328_b200.runtime import executor as ex  # noqa: E402
+from paper_2503_01328_b200.runtime.model import ModelConfig  # noqa: E402
+
+CFG = ModelConfig(n_layers=4, hidden=256, heads=4, seq=512, vocab=1024)
+OCFG = oracle_gpt.GPTConfig(n_layers=4, hidden=256, heads=4, seq=512, vocab=1024)
+
+
+def rel(a, b):
+    return float((a - b).norm() / (b.norm() + 1e-12))
+
+
+@pytest.fixture(scope="module")
+def oracle_result():
+    tokens = oracle_gpt.make_tokens(OCFG, 8, seed=0)
+    params = oracle_gpt.init_params(OCFG, seed=1234)
+    loss, _, grads = oracle_gpt.forward_backward(OCFG, params, tokens)
+    return tokens, loss, grads
+
+
+def _grads(res):
+    out = {}
+    for r in res.runners:
+        for st in r.stages.values():
+            for k, g in st.g.items():
+                out[k] = g.float().cpu()
+    return out
+
+
+def test_c1_full_offload_matches_oracle(oracle_result):
+    tokens, want_loss, want_grads = oracle_result
+    U = po.PassCosts.unit()
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    res = ex.execute(sched, plan, model=CFG, mode="virtual", tokens=tokens, optimizer="none", verify_roundtrip=True)
+    # op-order parity with the reference schedule and plan
+    for r, prog in res.programs.items():
+        assert prog.compute_order == [(str(p.kind), p.stage, p.microbatch) for p in sched.device_passes[r]]
+        want_copy = [(("OFFLOAD" if t.direction == po.PassKind.OFFLOAD else "RELOAD"), t.stage, t.microbatch)
+                     for t in plan.streams[r].transfers]
+        assert prog.copy_order.get("copy", []) == want_copy
+    assert res.peak_slabs == {0: 2, 1: 2, 2: 2, 3: 1}
+    assert ex.roundtrip_mismatches(res.runners) == []
+    n_offloaded = sum(len(p.offloaded) for p in res.programs.values())
+    assert n_offloaded == 24
+    loss = res.losses[-1]
+    assert abs(loss - want_loss) < 0.02 * abs(want_loss), (loss, want_loss)
+    got = _grads(res)
+    assert set(got) == set(want_grads)
+    for k, g in want_grads.items():
+        assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
+    # measured trace is a SimTrace: the reference's metrics apply
+    pk = po.peak_memory(res.trace)
+    assert [u for u, _ in pk["per_device"]] == [2, 2, 2, 1]
+
+
+def test_c1_offload_equals_no_offload(oracle_result):
+    tokens, _, _ = oracle_result
+    U = po.PassCosts.unit()
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    on = ex.execute(sched, plan, model=CFG, mode="virtual", tokens=tokens, optimizer="none")
+    off = ex.execute(sched, None, model=CFG, mode="virtual", tokens=tokens, optimizer="none")
+    assert off.peak_slabs == {0: 4, 1: 3, 2: 2, 3: 1}
+    assert abs(on.losses[-1] - off.losses[-1]) < 1e-3 * abs(off.losses[-1])
+    g_on, g_off = _grads(on), _grads(off)
+    for k in g_off:
+        assert rel(g_on[k], g_off[k]) < 1e-2, k
+
+
+def test_interleaved_selective_offload_runs():
+    """1F1B-I d=2 v=2 m=4, first local stage offloaded (select_offload_stages on po_block)."""
+    cfg = ModelConfig(n_layers=4, hidden=256, heads=4, seq=512, vocab=1024)
+    U = po.PassCosts.unit()
+    sched = po.build_interleaved_1f1b(2, 2, 4, U)
+    stages = po.select_offload_stages(po.po_block(2, 2, U), 1)
+    plan = po.plan_slots(sched, stages, Fraction(1, 2))
+    res = ex.execute(sched, plan, model=cfg, mode="virtual", optimizer="none", verify_roundtrip=True)
+    assert ex.roundtrip_mismatches(res.runners) == []
+    assert sum(len(p.offloaded) for p in res.programs.values()) > 0
+    off = ex.execute(sched, None, model=cfg, mode="virtual", optimizer="none")
+    assert abs(res.losses[-1] - off.losses[-1]) < 1e-3 * abs(off.losses[-1])
