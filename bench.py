@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the PipeOffload activation round trip on B200 (one JSON line).
+
+Metric (BASELINE.json): tokens/sec and peak activation GB/GPU at PP=1/2/4/8,
+offload overhead vs no-offload.
+
+Workload at --gpus 1 (default): rank 0 of C2 -- the GPT 1.3B shape
+(h=2048, s=4096, 16 heads, 24 layers over PP=8, i.e. embedding + 3 layers on
+rank 0), 1F1B with 32 microbatches, full offload of the merged stage
+(build_1f1b_full_offload), executed by ``execute(..., mode="emulate")``: rank 0's
+lowered program with its stage boundary looped back (synthetic downstream
+gradient).  At --gpus N>1 (torchrun) the same 3-layer stages form a real PP=N
+pipeline over NCCL (weak scaling: per-GPU work fixed).
+
+Every step is one full training iteration of the rank's program: 32 forward +
+32 backward passes, every D2H/H2D of the plan, and an SGD step on fp32 master
+weights.  Activations (0.5 GB per microbatch) far exceed the 126 MB L2.
+
+Besides the headline (full offload, the configured plan) the line reports the
+no-offload baseline and the k-aware selective plan measured in the same run.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from fractions import Fraction
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/sec and peak activation GB/GPU at PP=1/2/4/8, offload overhead vs no-offload"
+
+CONFIGS = {
+    # name: (layers_total, hidden, heads, seq, vocab, pp_for_planning, microbatches)
+    "c2": (24, 2048, 16, 4096, 50304, 8, 32),
+    "c4": (40, 5120, 40, 16384, 50304, 8, 32),
+    "c1": (4, 256, 4, 512, 1024, 4, 8),
+}
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200", "-i", str(self.dev)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured", d
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+# ----------------------------------------------------------------------- reference arm
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU implementation of the path (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    from oracle.pipeline import stage_sample
+
+    L, h, heads, s, _v, pp, m = CONFIGS[args.config]
+    layers = L // pp
+    stage_sample(256, 4, 512, 1, reps=1)  # warm the thread pool
+    vals = []
+    for _ in range(args.warmup):
+        stage_sample(h, heads, s, layers, reps=1)
+    for _ in range(args.steps):
+        vals.append(stage_sample(h, heads, s, layers, reps=1))
+    tps = statistics.median(v["tokens_per_s"] for v in vals)
+    cores = vals[0]["threads"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * s / tps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} rank-0 stage ({layers} layers h={h} s={s}), one microbatch F+B per step"},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": vals[0]["sample"]},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+
+
+def calibrate(stage, torch, native, reps=3):
+    """T_F, T_B of one microbatch of the stage and the D2H/H2D time of its slab."""
+    from paper_2503_01328_b200.runtime.model import SlabView
+
+    dev = stage.device
+    slab_mem = torch.empty(stage.layout.slab_bytes, dtype=torch.uint8, device=dev)
+    slab = SlabView(stage.layout, slab_mem)
+    cfg = stage.cfg
+    tok = torch.randint(0, cfg.vocab, (cfg.seq + 1,), device=dev)
+    out = torch.empty(cfg.seq, cfg.hidden, dtype=torch.bfloat16, device=dev)
+    dy = (torch.randn(cfg.seq, cfg.hidden, device=dev) * 1e-3).bfloat16()
+    tf, tb = [], []
+    for r in range(reps + 1):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        if stage.first:
+            stage.embed(slab, tok[:-1])
+        else:
+            slab.get(0, "x").copy_(dy)
+        stage.forward(slab, 0, 0, out=None if stage.last else out, targets=tok[1:] if stage.last else None)
+        e[1].record()
+        stage.backward(slab, 0, 0, dy=None if stage.last else dy, dx_out=None if stage.first else out,
+                       tokens=tok[:-1] if stage.first else None)
+        e[2].record()
+        torch.cuda.synchronize()
+        if r:
+            tf.append(e[0].elapsed_time(e[1]) / 1e3)
+            tb.append(e[1].elapsed_time(e[2]) / 1e3)
+    lay = stage.layout
+    pool = native.PinnedPool(lay.host_bytes + 4096)
+    bins, acc = [], pool.carve(lay.host_bytes)
+    for b in lay.bins:
+        bins.append(acc)
+        acc += b
+    segs = lay.segments(slab_mem.data_ptr(), tuple(bins))
+    copy = torch.cuda.Stream()
+    d2h, h2d = [], []
+    for r in range(reps + 1):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(copy)
+        native.transfer(native.PPO_D2H, segs, copy.cuda_stream)
+        e[1].record(copy)
+        native.transfer(native.PPO_H2D, segs, copy.cuda_stream)
+        e[2].record(copy)
+        torch.cuda.synchronize()
+        if r:
+            d2h.append(e[0].elapsed_time(e[1]) / 1e3)
+            h2d.append(e[1].elapsed_time(e[2]) / 1e3)
+    pool.close()
+    nbytes = sum(lay.bin_used)
+    return {
+        "t_f": min(tf), "t_b": min(tb), "t_d2h": min(d2h), "t_h2d": min(h2d), "transfer_bytes": nbytes,
+        "d2h_gbs": nbytes / min(d2h) / 1e9, "h2d_gbs": nbytes / min(h2d) / 1e9,
+    }
+
+
+def policy_report(res, sched, plan, m, seq, slab_bytes, rank):
+    it = statistics.median(res.iteration_seconds)
+    wall = statistics.median(res.wall_seconds)
+    prog = res.programs[rank]
+    d2h = [p for p in res.trace.transfer_passes() if p.kind.value == "OFFLOAD"]
+    h2d = [p for p in res.trace.transfer_passes() if p.kind.value == "RELOAD"]
+    gbs = lambda ps: (len(ps) * slab_bytes / float(sum(p.duration for p in ps)) / 1e9) if ps else None  # noqa: E731
+    comp = [p for p in res.trace.compute_passes()]
+    busy = float(sum(p.duration for p in comp))
+    return {
+        "tokens_per_s": m * seq / it,
+        "e2e_tokens_per_s": m * seq / wall,
+        "ms_per_step": 1000 * it,
+        "peak_act_slabs": prog.n_slabs,
+        "peak_act_gb": prog.n_slabs * slab_bytes / 1e9,
+        "host_slots": prog.n_host_slots,
+        "offloaded_pairs": len(prog.offloaded),
+        "late_reloads": len(plan.late_list()) if plan is not None else 0,
+        "d2h_gbs": gbs(d2h),
+        "h2d_gbs": gbs(h2d),
+        "compute_busy_frac": busy / float(res.trace.makespan) if res.trace.makespan else None,
+        "witness_peak_units": prog.witness_peak_units,
+    }
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    from paper_2503_01328_b200 import PassCosts, build_1f1b, measured_pass_costs, plan_slots
+    from paper_2503_01328_b200.policy import choose_offload
+    from paper_2503_01328_b200.runtime import native
+    from paper_2503_01328_b200.runtime.executor import execute
+    from paper_2503_01328_b200.runtime.model import ModelConfig, Stage
+
+    native.require_cuda()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    L, h, heads, s, vocab, pp_plan, m = CONFIGS[args.config]
+    layers_per_stage = L // pp_plan
+    d = pp_plan if world == 1 else world
+    n_layers = layers_per_stage * d
+    cfg = ModelConfig(n_layers=n_layers, hidden=h, heads=heads, seq=s, vocab=vocab)
+    mode = "emulate" if world == 1 else "nccl"
+
+    # ---- calibration: measured T_F, T_B (per stage), T_o (D2H + H2D of one payload)
+    cal_stage = Stage(cfg, min(rank, d - 1) if world > 1 else 0, d, m, dev, layers=list(range(layers_per_stage)))
+    cal = calibrate(cal_stage, torch, native)
+    del cal_stage
+    torch.cuda.empty_cache()
+    costs = measured_pass_costs(cal["t_f"] / layers_per_stage, cal["t_b"] / layers_per_stage, 0.0,
+                                (2 * s * h) / 770e9 + 10e-6)
+    t_o = Fraction(round((cal["t_d2h"] + cal["t_h2d"]) * 1e6), 1_000_000)
+    k_measured = float(t_o / (costs.total * layers_per_stage))
+    sched = build_1f1b(d, layers_per_stage, m, costs)
+    plans = {"none": None, "full": plan_slots(sched, (0,), t_o)}
+    choice = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
+    plans["auto"] = choice.plan
+
+    tokens = torch.randint(0, vocab, (m, s + 1), generator=torch.Generator().manual_seed(0)).pin_memory()
+    results = {}
+    launches = {}
+    clocks = None
+    for name in ("none", "auto", "full"):
+        plan = plans[name]
+        if name == "auto" and plan is None:
+            results[name] = dict(results["none"], note="k-aware policy keeps everything resident at this k")
+            continue
+        if name == "full":
+            sampler = ClockSampler(local_rank)
+            sampler.__enter__()
+        before = native.kernel_launches()
+        res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
+                      warmup=args.warmup, tokens=tokens, optimizer="sgd", probe_kernels=(name == "full"))
+        launches[name] = (native.kernel_launches() - before) / (args.steps + args.warmup)
+        if name == "full":
+            sampler.__exit__()
+            clocks = sampler.summary()
+            probe = res.runners[0].probe_summary()
+        results[name] = policy_report(res, sched, plan, m, s, res.slab_bytes, rank)
+        results[name]["_res"] = res
+        for r in res.runners:
+            r.close()
+    full, none, auto = results["full"], results["none"], results["auto"]
+    slab_bytes = full["_res"].slab_bytes
+    for v in results.values():
+        v.pop("_res", None)
+
+    # ---- roofline of the dominant kernel of the hot path (HBM-bound recompute)
+    hbm_peak, peak_kind, _ = measured_peaks()
+    kname = max(probe, key=lambda k: probe[k]["total_ms"]) if probe else None
+    roofline = None
+    if kname:
+        pk = probe[kname]
+        achieved = pk["bytes_per_launch"] / (pk["avg_ms"] / 1e3) / 1e9
+        roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_kind,
+                    "bytes_per_launch": pk["bytes_per_launch"], "avg_us": pk["avg_ms"] * 1e3,
+                    "launches_per_step": pk["launches"] / max(1, args.steps)}
+    link_peak = max(cal["d2h_gbs"], cal["h2d_gbs"])
+
+    line = {
+        "metric": METRIC,
+        "value": full["tokens_per_s"],
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": full["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic tokens, random-init weights (no checkpoint/dataset)",
+        "config": {
+            "workload": (f"C2 rank-0 program of PP={d} 1F1B, m={m}, full offload (emulated boundary)" if world == 1
+                         else f"PP={world} 1F1B pipeline, {layers_per_stage} layers/stage, m={m}, full offload"),
+            "model": f"GPT-1.3B shape h={h} heads={heads} s={s} vocab={vocab}, {layers_per_stage} layers/stage",
+            "global_batch": m, "seq_len": s, "parallelism": f"pp{d}" + ("-rank0" if world == 1 else ""),
+            "l2": "inputs larger than L2 (0.5 GB saved set per microbatch)",
+        },
+        "e2e": {"value": full["e2e_tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": m * (s + 1) * 8,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": launches.get("full"),
+        "clocks": clocks,
+        "roofline": roofline,
+        "kernels": {k: {"avg_us": round(v["avg_ms"] * 1e3, 2), "launches": v["launches"],
+                        "gbs": round(v["bytes_per_launch"] / v["avg_ms"] / 1e6, 1),
+                        "share_of_step": round(v["total_ms"] / (args.steps * full["ms_per_step"]), 4)}
+                    for k, v in (probe or {}).items()},
+        "host_link": {"bound": "pcie", "d2h_gbs": full["d2h_gbs"], "h2d_gbs": full["h2d_gbs"],
+                      "peak_gbs": link_peak, "frac": (full["d2h_gbs"] or 0) / link_peak if link_peak else None,
+                      "calibration": {k: cal[k] for k in ("d2h_gbs", "h2d_gbs", "transfer_bytes")}},
+        "offload": {
+            "k_measured": k_measured,
+            "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3, "T_o_ms": float(t_o) * 1e3,
+            "slab_bytes": slab_bytes,
+            "no_offload": none, "full": full, "auto": auto,
+            "auto_stride": choice.stride, "auto_modelled_overhead": choice.overhead,
+            "overhead_full_pct": 100 * (none["tokens_per_s"] / full["tokens_per_s"] - 1),
+            "overhead_auto_pct": 100 * (none["tokens_per_s"] / auto["tokens_per_s"] - 1),
+        },
+    }
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(args) if not args.no_cpu_baseline else None
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args):
+    from oracle.pipeline import stage_sample
+
+    L, h, heads, s, _v, pp, _m = CONFIGS[args.config]
+    stage_sample(256, 4, 512, 1)
+    r = stage_sample(h, heads, s, L // pp)
+    return {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+            "sample": r["sample"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

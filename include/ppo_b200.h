@@ -101,9 +101,10 @@ int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream);
 
 /* ------------------------------------------ K3/K5: fused LayerNorm + dropout */
 /* Philox4x32-10 dropout: element e of a tensor tagged (seed, offset) is kept iff
- * word (e % 4) of Philox(counter = {e/4 lo, e/4 hi, offset lo, offset hi},
- * key = {seed lo, seed hi}) >= floor(p * 2^32); kept values are scaled by 1/(1-p).
- * The mask is never stored: backward replays it. */
+ * 16-bit half (e % 2) of word ((e % 8) / 2) of Philox(counter = {e/8 lo, e/8 hi,
+ * offset lo, offset hi}, key = {seed lo, seed hi}) >= floor(p * 2^16); kept values
+ * are scaled by 1/(1-p).  One Philox block per 16-byte bf16x8 vector.  The mask is
+ * never stored: backward replays it. */
 
 /* y = LayerNorm(x) * gamma + beta over rows x hidden (bf16 in/out, fp32 math). */
 int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y,

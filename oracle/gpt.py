@@ -16,12 +16,13 @@ residual branches, causal attention, tanh GeLU):
 
 Dropout element masks come from oracle.philox with offset
 ``dropout_offset(iteration, layer, mb, branch)``, identical to the runtime.
-Weights are drawn once from ``torch.Generator().manual_seed(seed)`` and rounded
-to bf16 so the oracle and the runtime start from identical values.
+Each weight matrix is drawn from its own ``torch.Generator`` seeded with
+(seed, crc32(name)) and rounded to bf16 so the oracle and the runtime start from identical values.
 """
 
 from __future__ import annotations
 
+import zlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -65,7 +66,6 @@ def param_shapes(cfg: GPTConfig):
 
 def init_params(cfg: GPTConfig, seed: int = 1234) -> dict[str, torch.Tensor]:
     """N(0, 0.02) matrices (bf16-rounded, fp32 storage); LayerNorm gamma=1, beta=0."""
-    gen = torch.Generator().manual_seed(seed)
     out = {}
     for name, shape in param_shapes(cfg).items():
         if name.endswith("_g"):
@@ -73,6 +73,7 @@ def init_params(cfg: GPTConfig, seed: int = 1234) -> dict[str, torch.Tensor]:
         elif name.endswith("_b"):
             out[name] = torch.zeros(shape)
         else:
+            gen = torch.Generator().manual_seed(seed * 1_000_003 + zlib.crc32(name.encode()))
             std = 0.02 / (2 * cfg.n_layers) ** 0.5 if name.endswith(("w_proj", "w_fc2")) else 0.02
             out[name] = (torch.randn(shape, generator=gen) * std).bfloat16().float()
     return out
@@ -85,7 +86,8 @@ def make_tokens(cfg: GPTConfig, microbatches: int, seed: int = 0) -> torch.Tenso
 
 def _mask(cfg, iteration, layer, mb, m, branch, shape):
     keep = keep_mask(int(np.prod(shape)), cfg.p_drop, cfg.dropout_seed, dropout_offset(cfg, iteration, layer, mb, m, branch))
-    return torch.from_numpy(keep.reshape(shape)).float() / (1.0 - cfg.p_drop)
+    scale = np.float32(1.0) / np.float32(1.0 - cfg.p_drop)  # fp32 scale, as on device
+    return torch.from_numpy(keep.reshape(shape)).float() * float(scale)
 
 
 def _attention(cfg, qkv):
@@ -102,17 +104,23 @@ def _gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
 
-def microbatch_loss(cfg, params, tokens_mb, mb, m, iteration=0):
-    inp, tgt = tokens_mb[:-1], tokens_mb[1:]
-    x = params["wte"][inp] + params["wpe"]
+def run_layers(cfg, params, x, layers, mb, m, iteration=0):
+    """The transformer layers ``layers`` (global ids) applied to x [s, h]."""
     ln = torch.nn.functional.layer_norm
-    for l in range(cfg.n_layers):
+    for l in layers:
         p = lambda k: params[f"l{l}.{k}"]  # noqa: E731
         a = ln(x, (cfg.hidden,), p("ln1_g"), p("ln1_b"), cfg.eps)
         o = _attention(cfg, a @ p("w_qkv").t())
         h1 = x + (o @ p("w_proj").t()) * _mask(cfg, iteration, l, mb, m, 0, x.shape)
         f = ln(h1, (cfg.hidden,), p("ln2_g"), p("ln2_b"), cfg.eps) @ p("w_fc1").t()
         x = h1 + (_gelu(f) @ p("w_fc2").t()) * _mask(cfg, iteration, l, mb, m, 1, x.shape)
+    return x
+
+
+def microbatch_loss(cfg, params, tokens_mb, mb, m, iteration=0):
+    inp, tgt = tokens_mb[:-1], tokens_mb[1:]
+    ln = torch.nn.functional.layer_norm
+    x = run_layers(cfg, params, params["wte"][inp] + params["wpe"], range(cfg.n_layers), mb, m, iteration)
     logits = ln(x, (cfg.hidden,), params["lnf_g"], params["lnf_b"], cfg.eps) @ params["w_head"].t()
     return torch.nn.functional.cross_entropy(logits, tgt)
 
@@ -125,5 +133,5 @@ def forward_backward(cfg: GPTConfig, params: dict, tokens: torch.Tensor, iterati
     for mb in range(m):
         loss = microbatch_loss(cfg, leaf, tokens[mb], mb, m, iteration)
         (loss / m).backward()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     return float(np.mean(losses)), losses, {k: v.grad.detach() for k, v in leaf.items()}

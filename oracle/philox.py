@@ -1,9 +1,9 @@
 """Philox4x32-10 in numpy (test infrastructure; see oracle/__init__.py).
 
 Matches ``philox4x32_10`` / ``keep_mask8`` in paper_2503_01328_b200/csrc/ppo_common.cuh:
-element e of a tensor tagged (seed, offset) uses word e % 4 of
-Philox(counter = (e//4 lo, e//4 hi, offset lo, offset hi), key = (seed lo, seed hi))
-and is kept iff that word >= floor(p * 2**32).
+element e of a tensor tagged (seed, offset) uses 16-bit half (e % 2) of word
+(e % 8) // 2 of Philox(counter = (e//8 lo, e//8 hi, offset lo, offset hi),
+key = (seed lo, seed hi)) and is kept iff that half >= floor(p * 2**16).
 """
 
 import numpy as np
@@ -28,19 +28,25 @@ def philox4x32_10(c0, c1, c2, c3, k0: int, k1: int):
 
 
 def threshold(p: float) -> int:
-    t = p * 4294967296.0
+    """floor(p * 2**16), clamped to [0, 65535]."""
+    t = p * 65536.0
     if t <= 0:
         return 0
-    if t >= 4294967295.0:
-        return 0xFFFFFFFF
+    if t >= 65535.0:
+        return 65535
     return int(t)
 
 
 def keep_mask(n: int, p: float, seed: int, offset: int) -> np.ndarray:
-    """Boolean keep mask of the first n elements of tensor (seed, offset)."""
-    blocks = (n + 3) // 4
+    """Boolean keep mask of the first n elements of tensor (seed, offset).
+
+    One Philox block per 8 elements; element e uses the 16-bit half (e % 2) of
+    word (e % 8) // 2 (low half first) and is kept iff it is >= threshold(p).
+    """
+    blocks = (n + 7) // 8
     ctr = np.arange(blocks, dtype=np.uint64)
     words = philox4x32_10(ctr & MASK32, ctr >> np.uint64(32), np.full(blocks, offset & 0xFFFFFFFF, np.uint64),
                           np.full(blocks, (offset >> 32) & 0xFFFFFFFF, np.uint64), seed & 0xFFFFFFFF, seed >> 32)
-    stacked = np.stack(words, axis=1).reshape(-1)[:n]
-    return stacked >= np.uint32(threshold(p))
+    w = np.stack(words, axis=1)  # blocks x 4
+    halves = np.stack([w & np.uint32(0xFFFF), w >> np.uint32(16)], axis=2).reshape(-1)[:n]
+    return halves >= np.uint32(threshold(p))

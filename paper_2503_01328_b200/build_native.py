@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libppo_b200.so")
-SOURCES = ["ppo_runtime.cu", "ppo_kernels.cu", "ppo_comm.cu", "ppo_gemm.cu"]
+SOURCES = ["ppo_runtime.cu", "ppo_kernels.cu", "ppo_layernorm.cu", "ppo_comm.cu", "ppo_gemm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose and res.stderr.strip():
-        print(res.stderr[-4000:], file=sys.stderr)
+        print(res.stderr if os.environ.get("PPO_PTXAS_VERBOSE") else res.stderr[-4000:], file=sys.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

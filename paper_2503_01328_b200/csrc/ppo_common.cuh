@@ -122,31 +122,36 @@ __host__ __device__ __forceinline__ U32x4 philox4x32_10(uint32_t c0, uint32_t c1
   return out;
 }
 
-// Keep bits for elements e0 .. e0+7 (e0 % 8 == 0) of tensor (seed, offset).
+// Keep bits for elements e0 .. e0+7 (e0 % 8 == 0) of tensor (seed, offset): one
+// Philox4x32-10 block per 8 elements, one 16-bit lane per element (low half of word
+// i/2 for even i, high half for odd i); kept iff lane >= threshold16 = floor(p * 2^16).
 __device__ __forceinline__ uint32_t keep_mask8(uint64_t e0, uint64_t seed, uint64_t offset,
-                                               uint32_t threshold) {
+                                               uint32_t threshold16) {
+  const uint64_t ctr = e0 >> 3;
+  const U32x4 r = philox4x32_10((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)offset,
+                                (uint32_t)(offset >> 32), (uint32_t)seed, (uint32_t)(seed >> 32));
   uint32_t bits = 0;
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    uint64_t ctr = (e0 >> 2) + half;
-    U32x4 r = philox4x32_10((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)offset,
-                            (uint32_t)(offset >> 32), (uint32_t)seed, (uint32_t)(seed >> 32));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) bits |= (r.v[i] >= threshold ? 1u : 0u) << (4 * half + i);
+  for (int w = 0; w < 4; ++w) {
+    bits |= ((r.v[w] & 0xFFFFu) >= threshold16 ? 1u : 0u) << (2 * w);
+    bits |= ((r.v[w] >> 16) >= threshold16 ? 1u : 0u) << (2 * w + 1);
   }
   return bits;
 }
 
+// floor(p * 2^16), clamped; p in [0, 1).
 inline uint32_t dropout_threshold(float p) {
-  double t = (double)p * 4294967296.0;
+  double t = (double)p * 65536.0;
   if (t <= 0.0) return 0u;
-  if (t >= 4294967295.0) return 0xFFFFFFFFu;
+  if (t >= 65535.0) return 65535u;
   return (uint32_t)t;
 }
 
 // ------------------------------------------------------------ block reductions
 // Sums N values across the block; every thread gets the totals.  `scratch` holds
-// 32*N floats.  Safe to call back to back (ends with a barrier).
+// 33*N floats.  Two barriers: warp partials -> per-value reduction by N threads ->
+// broadcast.  Safe to call back to back (the caller's next write to scratch is
+// after the final barrier of this call).
 template <int N>
 __device__ __forceinline__ void block_sum(float (&v)[N], float* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -156,18 +161,65 @@ __device__ __forceinline__ void block_sum(float (&v)[N], float* scratch) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
   }
+  if (nwarps == 1) return;
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < N; ++i) scratch[warp * N + i] = v[i];
   }
   __syncthreads();
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
+  if (threadIdx.x < N) {
     float t = 0.f;
-    for (int w = 0; w < nwarps; ++w) t += scratch[w * N + i];
-    v[i] = t;
+    for (int w = 0; w < nwarps; ++w) t += scratch[w * N + threadIdx.x];
+    scratch[32 * N + threadIdx.x] = t;
   }
   __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = scratch[32 * N + i];
+  __syncthreads();
+}
+
+// ------------------------------------------------------ TMA bulk copies + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Order earlier generic-proxy shared-memory accesses before later async-proxy (TMA) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 1-D TMA: global -> shared, completion counted on `bar` (bytes % 16 == 0, 16 B aligned).
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 }  // namespace ppo

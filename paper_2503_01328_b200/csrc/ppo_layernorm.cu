@@ -1,0 +1,460 @@
+// libppo_b200.so -- K3: LayerNorm forward / backward with residual-add and Philox dropout
+// fused in, the recomputed "trivial layer" of the 34bsh -> 20bsh saved set
+// (reference pkg/src/ppoff/costs.py:1-7,18-20).
+//
+// Warp-group-per-row design.  A row of h bf16 is owned by W = ceil(h / (256 VPL))
+// warps; lane L of the group holds vectors v = L + 32W*j (j < VPL) of 8 bf16 each, so
+// every warp access is a fully coalesced 512-byte sweep and a lane keeps VPL x (number
+// of input tensors) independent 16-byte loads in flight.  Row statistics need only warp
+// shuffles (plus one named barrier when W > 1) -- no block-wide barrier inside the
+// row loop.  Statistics are one-pass (sum, sum of squares) in fp32.  The LayerNorm
+// parameter gradients accumulate in registers (a lane owns fixed columns), are folded
+// per CTA in shared memory and flushed with 16-byte vector atomics.
+#include "ppo_common.cuh"
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+
+namespace ppo {
+
+constexpr int kMaxHidden = 8192;
+constexpr int kGroupsPerBlock = 4;  // rows processed concurrently by one CTA
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Sum N values over the W warps of a row group; every lane gets the totals.
+template <int W, int N>
+__device__ __forceinline__ void group_sum(float (&v)[N], float* scratch, int group) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  }
+  if constexpr (W > 1) {
+    const int wig = (threadIdx.x >> 5) % W;  // warp index inside the group
+    float* s = scratch + group * W * N;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) s[wig * N + i] = v[i];
+    }
+    named_sync(1 + group, 32 * W);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) t += s[w * N + i];
+      v[i] = t;
+    }
+    named_sync(1 + group, 32 * W);
+  }
+}
+
+// 8 consecutive fp32 parameters through the read-only path (L1-resident after the
+// first row: every CTA reads the same h floats).
+__device__ __forceinline__ void load8f(const float* p, float (&o)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+
+// out = resid + dropout(branch)  (kResidual)  or  v = src  (!kResidual);  ln = LN(v).
+// The next row's vectors are requested before the current row is reduced, so DRAM
+// latency overlaps the shuffle reduction and the stores (register double-buffering).
+template <bool kResidual, int W, int kVecPerLane>
+__global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_fwd_kernel(
+    const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
+    const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
+    int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset, int use_dropout) {
+  extern __shared__ __align__(16) float sm[];
+  float* scratch = sm;
+  const int group = threadIdx.x / (32 * W);
+  const int L = threadIdx.x % (32 * W);
+  const int nvec = hidden >> 3;
+  const float inv_h = 1.f / (float)hidden;
+  const int64_t step = (int64_t)gridDim.x * kGroupsPerBlock;
+  int64_t row = (int64_t)blockIdx.x * kGroupsPerBlock + group;
+  uint4 ra[kVecPerLane], rb[kVecPerLane];
+  auto fetch = [&](int64_t r, uint4 (&a)[kVecPerLane], uint4 (&b)[kVecPerLane]) {
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const int v = L + 32 * W * j;
+      if (v < nvec) {
+        b[j] = ld_stream(src + r * hidden + 8 * v);
+        if (kResidual) a[j] = ld_stream(resid + r * hidden + 8 * v);
+      }
+    }
+  };
+  if (row < rows) fetch(row, ra, rb);
+  for (; row < rows; row += step) {
+    const int64_t rbase = row * hidden;
+    uint4 na[kVecPerLane], nb[kVecPerLane];
+    if (row + step < rows) fetch(row + step, na, nb);
+    float sums[2] = {0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const int v = L + 32 * W * j;
+      if (v >= nvec) continue;
+      float val[8];
+      if (kResidual) {
+        float a[8], b[8];
+        unpack8(ra[j], a);
+        unpack8(rb[j], b);
+        const uint32_t keep = use_dropout ? keep_mask8((uint64_t)(rbase + 8 * v), seed, offset, threshold) : 0xFFu;
+        const float sc = use_dropout ? scale : 1.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) val[i] = a[i] + (((keep >> i) & 1u) ? b[i] * sc : 0.f);
+        rb[j] = pack8(val);  // keep the stored bf16 bits; LN reads exactly what was stored
+        st_stream(out + rbase + 8 * v, rb[j]);
+      }
+      unpack8(rb[j], val);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        sums[0] += val[i];
+        sums[1] += val[i] * val[i];
+      }
+    }
+    if (ln) {
+      group_sum<W, 2>(sums, scratch, group);
+      const float mean = sums[0] * inv_h;
+      const float rstd = rsqrtf(fmaxf(sums[1] * inv_h - mean * mean, 0.f) + eps);
+#pragma unroll
+      for (int j = 0; j < kVecPerLane; ++j) {
+        const int v = L + 32 * W * j;
+        if (v >= nvec) continue;
+        float val[8], g[8], b[8], y[8];
+        unpack8(rb[j], val);
+        load8f(gamma + 8 * v, g);
+        load8f(beta + 8 * v, b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = (val[i] - mean) * rstd * g[i] + b[i];
+        st_stream(ln + rbase + 8 * v, pack8(y));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      ra[j] = na[j];
+      rb[j] = nb[j];
+    }
+  }
+}
+
+// dx = resid_grad + LN_bwd(dy; x) (statistics recomputed from x);
+// dgamma += sum_rows dy*xhat, dbeta += sum_rows dy;  drop_out = dropout_bwd(bf16(dx)).
+// A lane owns the same kVecPerLane x 8 columns on every row it visits, so the
+// parameter-gradient sums live in registers for the whole row loop; at the end the
+// CTA's row groups are folded in shared memory and flushed with one 16-byte vector
+// atomic per 4 columns (one CTA per SM: ~148 atomics per address in total).
+template <int W, int kVecPerLane>
+__global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
+    const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dy,
+    const __nv_bfloat16* __restrict__ resid_grad, __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
+    float* __restrict__ dbeta, int64_t rows, int hidden, float eps, __nv_bfloat16* __restrict__ drop_out,
+    uint32_t threshold, float scale, uint64_t seed, uint64_t offset) {
+  extern __shared__ __align__(16) float sm[];
+  float* s_acc = sm;                 // [2h]: dgamma partials, then dbeta partials
+  float* scratch = sm + 2 * hidden;  // group reductions
+  const int group = threadIdx.x / (32 * W);
+  const int L = threadIdx.x % (32 * W);
+  const int nvec = hidden >> 3;
+  const float inv_h = 1.f / (float)hidden;
+  const bool has_resid = resid_grad != nullptr;
+  const int64_t step = (int64_t)gridDim.x * kGroupsPerBlock;
+  float acc_g[kVecPerLane][8], acc_b[kVecPerLane][8];
+#pragma unroll
+  for (int j = 0; j < kVecPerLane; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc_g[j][i] = acc_b[j][i] = 0.f;
+  uint4 rx[kVecPerLane], rd[kVecPerLane], rr[kVecPerLane];
+  auto fetch = [&](int64_t r, uint4 (&a)[kVecPerLane], uint4 (&b)[kVecPerLane], uint4 (&c)[kVecPerLane]) {
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const int v = L + 32 * W * j;
+      if (v < nvec) {
+        a[j] = ld_stream(x + r * hidden + 8 * v);
+        b[j] = ld_stream(dy + r * hidden + 8 * v);
+        if (has_resid) c[j] = ld_stream(resid_grad + r * hidden + 8 * v);
+      }
+    }
+  };
+  int64_t row = (int64_t)blockIdx.x * kGroupsPerBlock + group;
+  if (row < rows) fetch(row, rx, rd, rr);
+  for (; row < rows; row += step) {
+    const int64_t rbase = row * hidden;
+    uint4 nx[kVecPerLane], nd[kVecPerLane], nr[kVecPerLane];
+    if (row + step < rows) fetch(row + step, nx, nd, nr);
+    float sums[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const int v = L + 32 * W * j;
+      if (v >= nvec) continue;
+      float xv[8], dv[8], g[8];
+      unpack8(rx[j], xv);
+      unpack8(rd[j], dv);
+      load8f(gamma + 8 * v, g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gi = dv[i] * g[i];
+        sums[0] += xv[i];
+        sums[1] += xv[i] * xv[i];
+        sums[2] += gi;
+        sums[3] += gi * xv[i];
+      }
+    }
+    group_sum<W, 4>(sums, scratch, group);
+    const float mean = sums[0] * inv_h;
+    const float rstd = rsqrtf(fmaxf(sums[1] * inv_h - mean * mean, 0.f) + eps);
+    const float mg = sums[2] * inv_h;                        // mean(g)
+    const float mgx = rstd * (sums[3] * inv_h - mean * mg);  // mean(g * xhat)
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const int v = L + 32 * W * j;
+      if (v >= nvec) continue;
+      float xv[8], dv[8], g[8], rg[8], d[8];
+      unpack8(rx[j], xv);
+      unpack8(rd[j], dv);
+      load8f(gamma + 8 * v, g);
+      if (has_resid) unpack8(rr[j], rg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (xv[i] - mean) * rstd;
+        d[i] = rstd * (dv[i] * g[i] - mg - xh * mgx) + (has_resid ? rg[i] : 0.f);
+        acc_g[j][i] += dv[i] * xh;
+        acc_b[j][i] += dv[i];
+      }
+      const uint4 packed = pack8(d);
+      st_stream(dx + rbase + 8 * v, packed);
+      if (drop_out) {
+        unpack8(packed, d);  // the replay applies to the stored bf16 gradient
+        const uint32_t keep = keep_mask8((uint64_t)(rbase + 8 * v), seed, offset, threshold);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d[i] = ((keep >> i) & 1u) ? d[i] * scale : 0.f;
+        st_stream(drop_out + rbase + 8 * v, pack8(d));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      rx[j] = nx[j];
+      rd[j] = nd[j];
+      rr[j] = nr[j];
+    }
+  }
+  // fold the row groups of this CTA in shared memory, one group at a time
+  for (int gi = 0; gi < kGroupsPerBlock; ++gi) {
+    if (group == gi) {
+#pragma unroll
+      for (int j = 0; j < kVecPerLane; ++j) {
+        const int v = L + 32 * W * j;
+        if (v >= nvec) continue;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float pg = gi ? s_acc[8 * v + i] : 0.f;
+          const float pb = gi ? s_acc[hidden + 8 * v + i] : 0.f;
+          s_acc[8 * v + i] = pg + acc_g[j][i];
+          s_acc[hidden + 8 * v + i] = pb + acc_b[j][i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = 4 * threadIdx.x; c < hidden; c += 4 * blockDim.x) {
+    atomicAdd(reinterpret_cast<float4*>(dgamma + c), *reinterpret_cast<const float4*>(s_acc + c));
+    atomicAdd(reinterpret_cast<float4*>(dbeta + c), *reinterpret_cast<const float4*>(s_acc + hidden + c));
+  }
+}
+
+static int check_rows(const char* who, int64_t rows, int64_t hidden) {
+  if (rows < 0 || hidden <= 0 || (hidden & 7) || hidden > kMaxHidden)
+    return set_error(PPO_ESHAPE, "%s: hidden=%lld must be a positive multiple of 8 <= %d", who,
+                     (long long)hidden, kMaxHidden);
+  return PPO_OK;
+}
+
+// Vectors per lane per tensor.  Fewer vectors per lane means more warps per row:
+// these kernels are latency-bound at transformer sizes (one row is a short dependent
+// chain), so parallelism across warps beats per-lane ILP.  PPO_LN_VPL overrides (2/4/8)
+// for A/B runs.
+static int vpl_choice(int64_t hidden, int dflt) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("PPO_LN_VPL");
+    env = e ? atoi(e) : 0;
+  }
+  int v = (env == 2 || env == 4 || env == 8) ? env : dflt;
+  while (v < 8 && (hidden + 256 * v - 1) / (256 * v) > 8) v *= 2;  // at most 8 warps per row
+  return v;
+}
+
+static int warps_per_row(int64_t hidden, int vpl) { return (int)((hidden + 256 * vpl - 1) / (256 * vpl)); }
+
+struct RowLaunch {
+  int grid, block;
+  size_t smem;
+};
+
+// Grid = every row group resident at once when the occupancy allows, else one full
+// wave of resident CTAs (148 SMs x CTAs per SM) looping over the rows.
+template <typename K>
+static int row_launch(K kernel, int64_t rows, int64_t hidden, int vpl, int param_arrays, RowLaunch* l) {
+  const int W = warps_per_row(hidden, vpl);
+  l->block = 32 * W * kGroupsPerBlock;
+  l->smem = (size_t)param_arrays * hidden * sizeof(float) + (size_t)kGroupsPerBlock * W * 4 * sizeof(float);
+  // The occupancy query and smem attribute are host work on every launch otherwise;
+  // cache them per (device, kernel, block, smem).
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kernel), l->block, l->smem);
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) per_sm = it->second;
+  }
+  if (per_sm == 0) {
+    if (l->smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l->smem);
+      if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(smem)");
+    }
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, l->block, l->smem);
+    if (e != cudaSuccess) return cuda_error(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (per_sm < 1) per_sm = 1;
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = per_sm;
+  }
+  const int64_t groups = (rows + kGroupsPerBlock - 1) / kGroupsPerBlock;
+  const int64_t cap = (int64_t)sm_count_current() * (per_sm > 0 ? per_sm : 1);
+  l->grid = (int)(groups < cap ? (groups > 0 ? groups : 1) : cap);
+  return PPO_OK;
+}
+
+
+}  // namespace ppo
+
+using namespace ppo;
+
+extern "C" {
+
+#define PPO_VPL_DISPATCH(VPL_, MACRO) \
+  switch (VPL_) {                     \
+    case 2: MACRO(2) break;           \
+    case 4: MACRO(4) break;           \
+    default: MACRO(8) break;          \
+  }
+
+int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, int64_t rows, int64_t hidden,
+                      float eps, void* stream) {
+  if (int rc = check_rows("ppo_layernorm_fwd", rows, hidden)) return rc;
+  if (!x || !gamma || !beta || !y) return set_error(PPO_EINVAL, "ppo_layernorm_fwd: null pointer");
+  if (rows == 0) return PPO_OK;
+  RowLaunch l;
+  int rc = PPO_OK;
+  const int vpl = vpl_choice(hidden, 4);
+#define PPO_LN_FWD_W(W, V)                                                                                    \
+  if ((rc = row_launch(ln_fwd_kernel<false, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
+  ln_fwd_kernel<false, W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                 \
+      nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta, static_cast<__nv_bfloat16*>(y), rows, \
+      (int)hidden, eps, 0u, 1.f, 0, 0, 0);
+#define PPO_LN_FWD_V(V)                                               \
+  {                                                                   \
+    switch (warps_per_row(hidden, V)) {                               \
+      case 1: PPO_LN_FWD_W(1, V) break;                               \
+      case 2: PPO_LN_FWD_W(2, V) break;                               \
+      case 3: PPO_LN_FWD_W(3, V) break;                               \
+      case 4: PPO_LN_FWD_W(4, V) break;                               \
+      case 5: PPO_LN_FWD_W(5, V) break;                               \
+      case 6: PPO_LN_FWD_W(6, V) break;                               \
+      case 7: PPO_LN_FWD_W(7, V) break;                               \
+      default: PPO_LN_FWD_W(8, V) break;                              \
+    }                                                                 \
+  }
+  PPO_VPL_DISPATCH(vpl, PPO_LN_FWD_V)
+#undef PPO_LN_FWD_V
+#undef PPO_LN_FWD_W
+  PPO_LAUNCHED("ln_fwd_kernel");
+  return PPO_OK;
+}
+
+int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out, const float* gamma,
+                                const float* beta, void* ln, int64_t rows, int64_t hidden, float eps, float p,
+                                uint64_t seed, uint64_t offset, void* stream) {
+  if (int rc = check_rows("ppo_residual_dropout_ln_fwd", rows, hidden)) return rc;
+  if (!resid || !branch || !out || (ln && (!gamma || !beta)))
+    return set_error(PPO_EINVAL, "ppo_residual_dropout_ln_fwd: null pointer");
+  if (!(p >= 0.f && p < 1.f)) return set_error(PPO_EINVAL, "ppo_residual_dropout_ln_fwd: p=%f", p);
+  if (rows == 0) return PPO_OK;
+  RowLaunch l;
+  int rc = PPO_OK;
+  const int vpl = vpl_choice(hidden, 4);
+#define PPO_RES_W(W, V)                                                                                      \
+  if ((rc = row_launch(ln_fwd_kernel<true, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
+  ln_fwd_kernel<true, W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                 \
+      static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),                   \
+      static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps, \
+      dropout_threshold(p), 1.f / (1.f - p), seed, offset, p > 0.f ? 1 : 0);
+#define PPO_RES_V(V)                                                  \
+  {                                                                   \
+    switch (warps_per_row(hidden, V)) {                               \
+      case 1: PPO_RES_W(1, V) break;                                  \
+      case 2: PPO_RES_W(2, V) break;                                  \
+      case 3: PPO_RES_W(3, V) break;                                  \
+      case 4: PPO_RES_W(4, V) break;                                  \
+      case 5: PPO_RES_W(5, V) break;                                  \
+      case 6: PPO_RES_W(6, V) break;                                  \
+      case 7: PPO_RES_W(7, V) break;                                  \
+      default: PPO_RES_W(8, V) break;                                 \
+    }                                                                 \
+  }
+  PPO_VPL_DISPATCH(vpl, PPO_RES_V)
+#undef PPO_RES_V
+#undef PPO_RES_W
+  PPO_LAUNCHED("ln_fwd_kernel<residual>");
+  return PPO_OK;
+}
+
+int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const void* resid_grad, void* dx,
+                      float* dgamma, float* dbeta, int64_t rows, int64_t hidden, float eps, void* drop_out, float p,
+                      uint64_t drop_seed, uint64_t drop_offset, void* stream) {
+  if (int rc = check_rows("ppo_layernorm_bwd", rows, hidden)) return rc;
+  if (!x || !gamma || !dy || !dx || !dgamma || !dbeta) return set_error(PPO_EINVAL, "ppo_layernorm_bwd: null pointer");
+  if (!(p >= 0.f && p < 1.f)) return set_error(PPO_EINVAL, "ppo_layernorm_bwd: p=%f", p);
+  if (rows == 0) return PPO_OK;
+  RowLaunch l;
+  int rc = PPO_OK;
+  if (!aligned16(dgamma) || !aligned16(dbeta))
+    return set_error(PPO_EINVAL, "ppo_layernorm_bwd: dgamma/dbeta must be 16-byte aligned");
+  const int vpl = vpl_choice(hidden, 2);
+#define PPO_LN_BWD_W(W, V)                                                                                     \
+  if ((rc = row_launch(ln_bwd_kernel<W, V>, rows, hidden, V, 2, &l))) return rc;                              \
+  ln_bwd_kernel<W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                         \
+      static_cast<const __nv_bfloat16*>(x), gamma, static_cast<const __nv_bfloat16*>(dy),                     \
+      static_cast<const __nv_bfloat16*>(resid_grad), static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows,    \
+      (int)hidden, eps, static_cast<__nv_bfloat16*>(drop_out), dropout_threshold(p), p > 0.f ? 1.f / (1.f - p) : 1.f, \
+      drop_seed, drop_offset);
+#define PPO_LN_BWD_V(V)                                               \
+  {                                                                   \
+    switch (warps_per_row(hidden, V)) {                               \
+      case 1: PPO_LN_BWD_W(1, V) break;                               \
+      case 2: PPO_LN_BWD_W(2, V) break;                               \
+      case 3: PPO_LN_BWD_W(3, V) break;                               \
+      case 4: PPO_LN_BWD_W(4, V) break;                               \
+      case 5: PPO_LN_BWD_W(5, V) break;                               \
+      case 6: PPO_LN_BWD_W(6, V) break;                               \
+      case 7: PPO_LN_BWD_W(7, V) break;                               \
+      default: PPO_LN_BWD_W(8, V) break;                              \
+    }                                                                 \
+  }
+  PPO_VPL_DISPATCH(vpl, PPO_LN_BWD_V)
+#undef PPO_LN_BWD_V
+#undef PPO_LN_BWD_W
+  PPO_LAUNCHED("ln_bwd_kernel");
+  return PPO_OK;
+}
+
+}  // extern "C"

@@ -375,6 +375,28 @@ class RankRunner:
         for (st, n) in self._adam_pairs:
             st.w[n].copy_(st.master[n])
 
+    def probe_summary(self) -> dict:
+        """Per native kernel: launches, mean/total CUDA-event duration, bytes per launch."""
+        out = {}
+        for st in self.stages.values():
+            for name, (nbytes, pairs) in (st.probe or {}).items():
+                ms = [a.elapsed_time(b) for a, b in pairs]
+                agg = out.setdefault(name, {"bytes_per_launch": nbytes, "launches": 0, "total_ms": 0.0})
+                agg["launches"] += len(ms)
+                agg["total_ms"] += sum(ms)
+        for agg in out.values():
+            agg["avg_ms"] = agg["total_ms"] / max(1, agg["launches"])
+        return out
+
+    def result_scalar(self) -> torch.Tensor:
+        """The step's result read back by the e2e path: the loss on the last stage,
+        otherwise a gradient checksum of the rank's first stage."""
+        ls = self.loss_sum()
+        if ls is not None:
+            return ls
+        st = self.stages[min(self.stages)]
+        return st.g[sorted(st.g)[0]].sum()
+
     def loss_sum(self) -> torch.Tensor | None:
         for st in self.stages.values():
             if st.last:
@@ -493,12 +515,13 @@ class RunResult:
     slab_bytes: int
     peak_slabs: dict  # rank -> arena slabs (= planned peak units)
     host_slots: dict
+    wall_seconds: list  # e2e: host clock per step incl. input H2D and result D2H
 
 
 def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelConfig, microbatches: int | None = None,
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
-            lr: float = 1e-4, verify_roundtrip: bool = False) -> RunResult:
+            lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
@@ -526,24 +549,35 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
     tokens_dev = torch.empty(tokens.shape, dtype=torch.int64, device=dev)
-    secs, losses = [], []
+    secs, losses, walls = [], [], []
+    torch.cuda.synchronize(dev)
     for it in range(warmup + iters):
-        tokens_dev.copy_(tokens, non_blocking=True)
+        if it == warmup and probe_kernels:
+            for r in runners:
+                for st in r.stages.values():
+                    st.probe = {}
+        wall0 = time.perf_counter()
+        tokens_dev.copy_(tokens, non_blocking=True)  # H2D of the step's inputs (pinned host)
         for r in runners:
             r.begin_iteration(tokens_dev)
         drive(runners)
         for r in runners:
             r.end_iteration()
+        result = [r.result_scalar() for r in runners]
+        values = [float(x) for x in result]  # D2H read of the step's result (syncs)
+        wall = time.perf_counter() - wall0
         if transport is not None:
             torch.cuda.synchronize(dev)
             transport.end_iteration()
         if it >= warmup:
             torch.cuda.synchronize(dev)
+            walls.append(wall)
             secs.append(max(r.iteration_seconds() for r in runners))
-            ls = [r.loss_sum() for r in runners if r.loss_sum() is not None]
-            losses.append(float(ls[0]) / m if ls else None)
+            ls = [v for r, v in zip(runners, values) if r.loss_sum() is not None]
+            losses.append(ls[0] / m if ls else None)
     passes = [p for r in runners for p in r.measured_passes()]
     slab_bytes = max(r.slab_bytes for r in runners)
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
     return RunResult(trace, secs, losses, programs, runners, slab_bytes,
-                     {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners})
+                     {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners},
+                     walls)

@@ -16,6 +16,7 @@ embedding and loss head (first/last stage only) use torch ops.
 
 from __future__ import annotations
 
+import zlib
 from dataclasses import dataclass
 
 import torch
@@ -48,8 +49,8 @@ def dropout_offset(cfg: ModelConfig, iteration: int, layer: int, mb: int, microb
 def init_params(cfg: ModelConfig, seed: int = 1234, names=None) -> dict[str, torch.Tensor]:
     """Deterministic N(0, 0.02) init on the CPU generator (bf16-representable values).
 
-    Draw order is fixed (embedding, per-layer, head) so every rank reproduces the
-    same weights for the layers it owns without communicating.
+    Every matrix has its own generator seeded from (seed, crc32(name)), so each
+    rank draws exactly the tensors it owns and all ranks agree without talking.
     """
     h, v, s = cfg.hidden, cfg.vocab, cfg.seq
     shapes = {"wte": (v, h), "wpe": (s, h)}
@@ -59,18 +60,19 @@ def init_params(cfg: ModelConfig, seed: int = 1234, names=None) -> dict[str, tor
             f"l{l}.ln2_g": (h,), f"l{l}.ln2_b": (h,), f"l{l}.w_fc1": (4 * h, h), f"l{l}.w_fc2": (h, 4 * h),
         })
     shapes.update({"lnf_g": (h,), "lnf_b": (h,), "w_head": (v, h)})
-    gen = torch.Generator().manual_seed(seed)
     out = {}
     for name, shape in shapes.items():
+        if names is not None and name not in names:
+            continue
         if name.endswith("_g"):
             val = torch.ones(shape)
         elif name.endswith("_b"):
             val = torch.zeros(shape)
         else:
+            gen = torch.Generator().manual_seed(seed * 1_000_003 + zlib.crc32(name.encode()))
             std = 0.02 / (2 * cfg.n_layers) ** 0.5 if name.endswith(("w_proj", "w_fc2")) else 0.02
             val = (torch.randn(shape, generator=gen) * std).bfloat16().float()
-        if names is None or name in names:
-            out[name] = val
+        out[name] = val
     return out
 
 
@@ -143,6 +145,17 @@ class Stage:
         }
         self.loss_sum = torch.zeros((), device=self.device, dtype=torch.float32)
         self._attn_meta = None
+        self.probe = None  # kernel name -> [bytes_per_launch, [(start_event, end_event), ...]]
+
+    def _k(self, name: str, nbytes: int, fn, *args, **kw):
+        """Launch one native kernel; with probing on, bracket it with CUDA events."""
+        if self.probe is None:
+            return fn(*args, **kw)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn(*args, **kw)
+        b.record()
+        self.probe.setdefault(name, [nbytes, []])[1].append((a, b))
 
     # ------------------------------------------------------------------ utils
     def p(self, l: int, k: str) -> torch.Tensor:
@@ -181,6 +194,7 @@ class Stage:
         """
         cfg, ws = self.cfg, self.ws
         p, seed, eps = cfg.p_drop, cfg.dropout_seed, cfg.eps
+        s, h = cfg.seq, cfg.hidden
         n_local = len(self.layers)
         native.layernorm_fwd(slab.get(0, "x"), self.p(self.layers[0], "ln1_g"), self.p(self.layers[0], "ln1_b"), ws["ln"], eps)
         for i, l in enumerate(self.layers):
@@ -197,9 +211,10 @@ class Stage:
             self._pack_attention(slab, i, o_tmp, lse)
             o = slab.get(i, "o")
             torch.mm(o, self.p(l, "w_proj").t(), out=ws["a"])
-            native.residual_dropout_ln_fwd(x, ws["a"], h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps)
+            self._k("residual_dropout_ln_fwd", 8 * s * h, native.residual_dropout_ln_fwd, x, ws["a"], h1, self.p(l, "ln2_g"),
+                    self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps)
             torch.mm(ws["ln"], self.p(l, "w_fc1").t(), out=f)
-            native.gelu_fwd(f, ws["g"])
+            self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])
             torch.mm(ws["g"], self.p(l, "w_fc2").t(), out=ws["a"])
             if i + 1 < n_local:
                 nxt = self.layers[i + 1]
@@ -216,10 +231,8 @@ class Stage:
         s, h, H = self.cfg.seq, self.cfg.hidden, self.cfg.heads
         if not o_tmp.transpose(1, 2).is_contiguous() or not lse.is_contiguous():
             raise RuntimeError(f"unexpected cuDNN attention layout: o {o_tmp.stride()} lse {lse.stride()}")
-        native.pack(
-            [(o_tmp, slab.offset(i, "o"), 1, 2 * s * h, 0), (lse, slab.offset(i, "lse"), 1, 4 * H * s, 0)],
-            slab.base,
-        )
+        items = [(o_tmp, slab.offset(i, "o"), 1, 2 * s * h, 0), (lse, slab.offset(i, "lse"), 1, 4 * H * s, 0)]
+        self._k("pack", 2 * (2 * s * h + 4 * H * s), native.pack, items, slab.base)
 
     def _head(self, slab: SlabView, targets: torch.Tensor):
         """Loss head of the last stage, forward and backward fused into F.
@@ -260,14 +273,14 @@ class Stage:
             dg = ws["big"]
             # MLP: dg = dm @ Wfc2; g = gelu(f) recomputed; df = dg * gelu'(f)
             torch.mm(ws["dm"], self.p(l, "w_fc2"), out=dg)
-            native.gelu_bwd(f, dg, ws["g"], dg)
+            self._k("gelu_bwd", 32 * s * h, native.gelu_bwd, f, dg, ws["g"], dg)
             _wgrad(self.gp(l, "w_fc2"), ws["dm"].t(), ws["g"])
-            native.layernorm_fwd(h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
+            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
             _wgrad(self.gp(l, "w_fc1"), dg.t(), ws["ln"])
             torch.mm(dg, self.p(l, "w_fc1"), out=ws["t"])
             # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay)
-            native.layernorm_bwd(h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"], self.gp(l, "ln2_g"),
-                                 self.gp(l, "ln2_b"), drop_out=ws["da"], p=p, drop_seed=seed, drop_offset=off_a, eps=eps)
+            self._k("layernorm_bwd", 10 * s * h, native.layernorm_bwd, h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"],
+                    self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=ws["da"], p=p, drop_seed=seed, drop_offset=off_a, eps=eps)
             # attention projection and core
             _wgrad(self.gp(l, "w_proj"), ws["da"].t(), o)
             torch.mm(ws["da"], self.p(l, "w_proj"), out=ws["t"])
@@ -278,7 +291,7 @@ class Stage:
             cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
             dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
                 do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
-            native.layernorm_fwd(x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
+            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
             w_qkv, g_qkv = self.p(l, "w_qkv"), self.gp(l, "w_qkv")
             grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
             for j, gj in enumerate(grads):

@@ -111,7 +111,8 @@ def test_gelu_fwd_bwd(n):
     df = bf(dg)
     native.gelu_bwd(bf(f), df, g2, df)  # df aliases dg (in place)
     assert torch.equal(g, g2)
-    np.testing.assert_allclose(npf(df), dg * ref.gelu_grad(f), rtol=2 ** -7, atol=1e-5)
+    # tanh.approx.f32 (SFU) has ~2^-11 absolute error: atol covers it where gelu' ~ 0
+    np.testing.assert_allclose(npf(df), dg * ref.gelu_grad(f), rtol=2 ** -7, atol=1e-3)
 
 
 def test_pack_gather_bit_exact():
