@@ -262,8 +262,8 @@ def run_b200(args, rank, world, local_rank):
     results = {}
     launches = {}
     clocks = None
-    for name in ("none", "auto", "full"):
-        plan = plans[name]
+    for name in ("none", "auto", "full", "full_dual"):
+        plan = plans["full" if name == "full_dual" else name]
         if name == "auto" and plan is None:
             results[name] = dict(results["none"], note="k-aware policy keeps everything resident at this k")
             continue
@@ -272,7 +272,8 @@ def run_b200(args, rank, world, local_rank):
             sampler.__enter__()
         before = native.kernel_launches()
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
-                      warmup=args.warmup, tokens=tokens, optimizer="sgd", probe_kernels=(name == "full"))
+                      warmup=args.warmup, tokens=tokens, optimizer="sgd", probe_kernels=(name == "full"),
+                      stream_mode="dual" if name == "full_dual" else "single")
         launches[name] = (native.kernel_launches() - before) / (args.steps + args.warmup)
         if name == "full":
             sampler.__exit__()
@@ -282,7 +283,7 @@ def run_b200(args, rank, world, local_rank):
         results[name]["_res"] = res
         for r in res.runners:
             r.close()
-    full, none, auto = results["full"], results["none"], results["auto"]
+    full, none, auto, dual = results["full"], results["none"], results["auto"], results["full_dual"]
     slab_bytes = full["_res"].slab_bytes
     for v in results.values():
         v.pop("_res", None)
@@ -336,10 +337,11 @@ def run_b200(args, rank, world, local_rank):
             "k_measured": k_measured,
             "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3, "T_o_ms": float(t_o) * 1e3,
             "slab_bytes": slab_bytes,
-            "no_offload": none, "full": full, "auto": auto,
+            "no_offload": none, "full": full, "auto": auto, "full_dual_stream": dual,
             "auto_stride": choice.stride, "auto_modelled_overhead": choice.overhead,
             "overhead_full_pct": 100 * (none["tokens_per_s"] / full["tokens_per_s"] - 1),
             "overhead_auto_pct": 100 * (none["tokens_per_s"] / auto["tokens_per_s"] - 1),
+            "overhead_full_dual_pct": 100 * (none["tokens_per_s"] / dual["tokens_per_s"] - 1),
         },
     }
     if rank == 0:
