@@ -10,6 +10,7 @@ PyTorch's; the library only sees raw pointers, sizes and stream handles).
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 import threading
@@ -114,7 +115,11 @@ def check(fn: str, rc: int) -> None:
         raise PpoError(fn, rc, msg.decode() if msg else "")
 
 
+CALLS: collections.Counter = collections.Counter()  # ABI entry point -> calls (launch accounting)
+
+
 def call(fn: str, *args) -> None:
+    CALLS[fn] += 1
     check(fn, getattr(load(), fn)(*args))
 
 
