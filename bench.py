@@ -156,13 +156,12 @@ def calibrate(stage, torch, native, reps=3):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record()
         if stage.first:
-            stage.embed(slab, tok[:-1])
+            stage.embed(slab, tok)
         else:
             slab.get(0, "x").copy_(dy)
-        stage.forward(slab, 0, 0, out=None if stage.last else out, targets=tok[1:] if stage.last else None)
+        stage.forward(slab, 0, 0, out=None if stage.last else out, tokens=tok)
         e[1].record()
-        stage.backward(slab, 0, 0, dy=None if stage.last else dy, dx_out=None if stage.first else out,
-                       tokens=tok[:-1] if stage.first else None)
+        stage.backward(slab, 0, 0, dy=None if stage.last else dy, dx_out=None if stage.first else out, tokens=tok)
         e[2].record()
         torch.cuda.synchronize()
         if r:
@@ -188,10 +187,35 @@ def calibrate(stage, torch, native, reps=3):
         if r:
             d2h.append(e[0].elapsed_time(e[1]) / 1e3)
             h2d.append(e[1].elapsed_time(e[2]) / 1e3)
+    # one-way time while the other direction is busy too (full duplex PCIe)
+    slab2 = torch.empty_like(slab_mem)
+    pool2 = native.PinnedPool(lay.host_bytes + 4096)
+    bins2, acc2 = [], pool2.carve(lay.host_bytes)
+    for b in lay.bins:
+        bins2.append(acc2)
+        acc2 += b
+    segs2 = lay.segments(slab2.data_ptr(), tuple(bins2))
+    copy2 = torch.cuda.Stream()
+    dup = []
+    for r in range(reps + 1):
+        ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        ea[0].record(copy)
+        eb[0].record(copy2)
+        native.transfer(native.PPO_D2H, segs, copy.cuda_stream)
+        native.transfer(native.PPO_H2D, segs2, copy2.cuda_stream)
+        ea[1].record(copy)
+        eb[1].record(copy2)
+        torch.cuda.synchronize()
+        if r:
+            dup.append(max(ea[0].elapsed_time(ea[1]), eb[0].elapsed_time(eb[1])) / 1e3)
+    pool2.close()
     pool.close()
     nbytes = sum(lay.bin_used)
     return {
         "t_f": min(tf), "t_b": min(tb), "t_d2h": min(d2h), "t_h2d": min(h2d), "transfer_bytes": nbytes,
+        "t_duplex": statistics.median(dup), "duplex_gbs_per_direction": nbytes / statistics.median(dup) / 1e9,
         "d2h_gbs": nbytes / min(d2h) / 1e9, "h2d_gbs": nbytes / min(h2d) / 1e9,
     }
 
@@ -273,6 +297,7 @@ def policy_report(res, sched, plan, m, seq, slab_bytes, rank):
         "d2h_gbs": gbs(d2h),
         "h2d_gbs": gbs(h2d),
         "compute_busy_frac": busy / float(res.trace.makespan) if res.trace.makespan else None,
+        "host_issue_ms": 1e3 * statistics.median(res.host_issue_seconds) if res.host_issue_seconds else None,
         "witness_peak_units": prog.witness_peak_units,
     }
 
@@ -281,6 +306,7 @@ def run_b200(args, rank, world, local_rank):
     import torch
 
     from paper_2503_01328_b200 import PassCosts, build_1f1b, measured_pass_costs, plan_slots
+    from paper_2503_01328_b200.offload import plan_slots_duplex
     from paper_2503_01328_b200.policy import choose_offload
     from paper_2503_01328_b200.runtime import native
     from paper_2503_01328_b200.runtime.executor import execute
@@ -310,7 +336,8 @@ def run_b200(args, rank, world, local_rank):
     t_o = Fraction(round((cal["t_d2h"] + cal["t_h2d"]) * 1e6), 1_000_000)
     k_measured = float(t_o / (costs.total * layers_per_stage))
     sched = build_1f1b(d, layers_per_stage, m, costs)
-    plans = {"none": None, "full": plan_slots(sched, (0,), t_o)}
+    plans = {"none": None, "full": plan_slots(sched, (0,), t_o),
+             "full_duplex": plan_slots_duplex(sched, (0,), Fraction(round(cal["t_duplex"] * 1e6), 1_000_000))}
     choice = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
     plans["auto"] = choice.plan
 
@@ -318,7 +345,7 @@ def run_b200(args, rank, world, local_rank):
     results = {}
     launches = {}
     clocks = None
-    for name in ("none", "auto", "full", "full_dual"):
+    for name in ("none", "auto", "full", "full_dual", "full_duplex"):
         plan = plans["full" if name == "full_dual" else name]
         if name == "auto" and plan is None:
             results[name] = dict(results["none"], note="k-aware policy keeps everything resident at this k")
@@ -330,7 +357,7 @@ def run_b200(args, rank, world, local_rank):
         native.CALLS.clear()
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
-                      stream_mode="dual" if name == "full_dual" else "single")
+                      stream_mode="dual" if name in ("full_dual", "full_duplex") else "single")
         launches[name] = (native.kernel_launches() - before) / (args.steps + args.warmup)
         if name == "full":
             sampler.__exit__()
@@ -341,6 +368,7 @@ def run_b200(args, rank, world, local_rank):
         for r in res.runners:
             r.close()
     full, none, auto, dual = results["full"], results["none"], results["auto"], results["full_dual"]
+    duplex = results["full_duplex"]
     slab_bytes = full["_res"].slab_bytes
     for v in results.values():
         v.pop("_res", None)
@@ -399,11 +427,13 @@ def run_b200(args, rank, world, local_rank):
             "k_measured": k_measured,
             "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3, "T_o_ms": float(t_o) * 1e3,
             "slab_bytes": slab_bytes,
-            "no_offload": none, "full": full, "auto": auto, "full_dual_stream": dual,
+            "no_offload": none, "full": full, "auto": auto, "full_dual_stream": dual, "full_duplex_plan": duplex,
             "auto_stride": choice.stride, "auto_modelled_overhead": choice.overhead,
             "overhead_full_pct": 100 * (none["tokens_per_s"] / full["tokens_per_s"] - 1),
             "overhead_auto_pct": 100 * (none["tokens_per_s"] / auto["tokens_per_s"] - 1),
             "overhead_full_dual_pct": 100 * (none["tokens_per_s"] / dual["tokens_per_s"] - 1),
+            "overhead_full_duplex_pct": 100 * (none["tokens_per_s"] / duplex["tokens_per_s"] - 1),
+            "t_duplex_oneway_ms": cal["t_duplex"] * 1e3,
         },
     }
     if rank == 0:

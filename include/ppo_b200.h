@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 1
+#define PPO_ABI_VERSION 2
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -104,7 +104,11 @@ int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream);
  * 16-bit half (e % 2) of word ((e % 8) / 2) of Philox(counter = {e/8 lo, e/8 hi,
  * offset lo, offset hi}, key = {seed lo, seed hi}) >= floor(p * 2^16); kept values
  * are scaled by 1/(1-p).  One Philox block per 16-byte bf16x8 vector.  The mask is
- * never stored: backward replays it. */
+ * never stored: backward replays it.
+ * Every dropout entry point takes the Philox offset as `offset + *offset_base` when
+ * `offset_base` (a device pointer to one uint64) is non-null: the per-(iteration,
+ * microbatch) part then lives in device memory, so one captured CUDA graph of a
+ * forward/backward pass serves every microbatch. */
 
 /* y = LayerNorm(x) * gamma + beta over rows x hidden (bf16 in/out, fp32 math). */
 int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y,
@@ -117,7 +121,8 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
 int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out,
                                 const float* gamma, const float* beta, void* ln,
                                 int64_t rows, int64_t hidden, float eps, float p,
-                                uint64_t seed, uint64_t offset, void* stream);
+                                uint64_t seed, uint64_t offset, const uint64_t* offset_base,
+                                void* stream);
 
 /* LayerNorm backward with the statistics recomputed from x (no saved mean/rstd):
  *   dx = resid_grad + LN_bwd(dy; x, gamma)           (bf16; resid_grad may be NULL)
@@ -127,12 +132,12 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
 int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const void* resid_grad,
                       void* dx, float* dgamma, float* dbeta, int64_t rows, int64_t hidden,
                       float eps, void* drop_out, float p, uint64_t drop_seed,
-                      uint64_t drop_offset, void* stream);
+                      uint64_t drop_offset, const uint64_t* drop_offset_base, void* stream);
 
 /* Standalone dropout (forward: y = dropout(x); backward: dx = dropout_bwd(dy) -- the
  * same mask applied to the gradient). */
 int ppo_dropout(const void* x, void* y, int64_t n, float p, uint64_t seed, uint64_t offset,
-                void* stream);
+                const uint64_t* offset_base, void* stream);
 
 /* ------------------------------------------------------------- K4: GeLU */
 /* g = gelu_tanh(f)  (forward, fc1-out -> fc2 input). */

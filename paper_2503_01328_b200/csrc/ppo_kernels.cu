@@ -11,7 +11,8 @@ namespace ppo {
 __global__ void __launch_bounds__(256) dropout_kernel(const __nv_bfloat16* __restrict__ x,
                                                       __nv_bfloat16* __restrict__ y, int64_t n8,
                                                       uint32_t threshold, float scale, uint64_t seed,
-                                                      uint64_t offset) {
+                                                      uint64_t offset_add, const uint64_t* __restrict__ offset_base) {
+  const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < n8; c0 += 2 * stride) {
     uint4 raw[2];
@@ -148,14 +149,15 @@ using namespace ppo;
 
 extern "C" {
 
-int ppo_dropout(const void* x, void* y, int64_t n, float p, uint64_t seed, uint64_t offset, void* stream) {
+int ppo_dropout(const void* x, void* y, int64_t n, float p, uint64_t seed, uint64_t offset,
+                const uint64_t* offset_base, void* stream) {
   if (!x || !y || n < 0 || (n & 7)) return set_error(PPO_EINVAL, "ppo_dropout: bad arguments (n %% 8 != 0?)");
   if (!(p >= 0.f && p < 1.f)) return set_error(PPO_EINVAL, "ppo_dropout: p=%f", p);
   if (n == 0) return PPO_OK;
   const int64_t n8 = n >> 3;
   dropout_kernel<<<elementwise_grid(n8), 256, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), n8, dropout_threshold(p),
-      1.f / (1.f - p), seed, offset);
+      1.f / (1.f - p), seed, offset, offset_base);
   PPO_LAUNCHED("dropout_kernel");
   return PPO_OK;
 }

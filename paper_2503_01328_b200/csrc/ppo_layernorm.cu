@@ -70,8 +70,10 @@ template <bool kResidual, int W, int kVecPerLane>
 __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_fwd_kernel(
     const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
     const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
-    int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset, int use_dropout) {
+    int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add,
+    const uint64_t* __restrict__ offset_base, int use_dropout) {
   extern __shared__ __align__(16) float sm[];
+  const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
   float* scratch = sm;
   const int group = threadIdx.x / (32 * W);
   const int L = threadIdx.x % (32 * W);
@@ -155,8 +157,9 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dy,
     const __nv_bfloat16* __restrict__ resid_grad, __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
     float* __restrict__ dbeta, int64_t rows, int hidden, float eps, __nv_bfloat16* __restrict__ drop_out,
-    uint32_t threshold, float scale, uint64_t seed, uint64_t offset) {
+    uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add, const uint64_t* __restrict__ offset_base) {
   extern __shared__ __align__(16) float sm[];
+  const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
   float* s_acc = sm;                 // [2h]: dgamma partials, then dbeta partials
   float* scratch = sm + 2 * hidden;  // group reductions
   const int group = threadIdx.x / (32 * W);
@@ -360,7 +363,7 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
   if ((rc = row_launch(ln_fwd_kernel<false, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
   ln_fwd_kernel<false, W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                 \
       nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta, static_cast<__nv_bfloat16*>(y), rows, \
-      (int)hidden, eps, 0u, 1.f, 0, 0, 0);
+      (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0);
 #define PPO_LN_FWD_V(V)                                               \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \
@@ -383,7 +386,7 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
 
 int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out, const float* gamma,
                                 const float* beta, void* ln, int64_t rows, int64_t hidden, float eps, float p,
-                                uint64_t seed, uint64_t offset, void* stream) {
+                                uint64_t seed, uint64_t offset, const uint64_t* offset_base, void* stream) {
   if (int rc = check_rows("ppo_residual_dropout_ln_fwd", rows, hidden)) return rc;
   if (!resid || !branch || !out || (ln && (!gamma || !beta)))
     return set_error(PPO_EINVAL, "ppo_residual_dropout_ln_fwd: null pointer");
@@ -397,7 +400,7 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   ln_fwd_kernel<true, W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                 \
       static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),                   \
       static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps, \
-      dropout_threshold(p), 1.f / (1.f - p), seed, offset, p > 0.f ? 1 : 0);
+      dropout_threshold(p), 1.f / (1.f - p), seed, offset, offset_base, p > 0.f ? 1 : 0);
 #define PPO_RES_V(V)                                                  \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \
@@ -420,7 +423,7 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
 
 int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const void* resid_grad, void* dx,
                       float* dgamma, float* dbeta, int64_t rows, int64_t hidden, float eps, void* drop_out, float p,
-                      uint64_t drop_seed, uint64_t drop_offset, void* stream) {
+                      uint64_t drop_seed, uint64_t drop_offset, const uint64_t* drop_offset_base, void* stream) {
   if (int rc = check_rows("ppo_layernorm_bwd", rows, hidden)) return rc;
   if (!x || !gamma || !dy || !dx || !dgamma || !dbeta) return set_error(PPO_EINVAL, "ppo_layernorm_bwd: null pointer");
   if (!(p >= 0.f && p < 1.f)) return set_error(PPO_EINVAL, "ppo_layernorm_bwd: p=%f", p);
@@ -436,7 +439,7 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
       static_cast<const __nv_bfloat16*>(x), gamma, static_cast<const __nv_bfloat16*>(dy),                     \
       static_cast<const __nv_bfloat16*>(resid_grad), static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows,    \
       (int)hidden, eps, static_cast<__nv_bfloat16*>(drop_out), dropout_threshold(p), p > 0.f ? 1.f / (1.f - p) : 1.f, \
-      drop_seed, drop_offset);
+      drop_seed, drop_offset, drop_offset_base);
 #define PPO_LN_BWD_V(V)                                               \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \

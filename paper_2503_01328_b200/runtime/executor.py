@@ -176,7 +176,7 @@ class RankRunner:
 
     def __init__(self, program: Program, cfg: ModelConfig, sched: Schedule, microbatches: int, device,
                  transport=None, emulate: bool = False, params=None, seed: int = 1234, optimizer: str = "sgd",
-                 lr: float = 1e-4, verify_roundtrip: bool = False):
+                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True):
         torch_ = native.require_cuda()
         self.torch = torch_
         self.prog, self.cfg, self.sched, self.m = program, cfg, sched, microbatches
@@ -213,6 +213,8 @@ class RankRunner:
         self.optimizer = optimizer
         self.lr = lr
         self.verify_roundtrip = verify_roundtrip
+        self.use_graphs = use_graphs
+        self.graphs = {}
         self.digests = {}  # (stage, mb) -> [digest at F end, digest at B start]
         self._adam = None
         self.cursor = 0
@@ -302,8 +304,9 @@ class RankRunner:
         self.ev(("F_start", s, j)).record(stream)
         with torch.cuda.stream(stream):
             slab = self.slab(op.slab, s)
+            st.set_pass_context(j, self.iteration, self.tokens[j])
             if st.first:
-                st.embed(slab, self.tokens[j, :-1])
+                st.embed(slab)
             elif op.ring is not None:
                 slab.get(0, "x").copy_(self.rings["recv_act"][op.ring])
             else:  # emulated upstream stage
@@ -312,7 +315,8 @@ class RankRunner:
             out = None
             if not st.last:
                 out = self.rings["send_act"][op.send_ring] if op.send_ring is not None else self.scratch_out
-            st.forward(slab, j, self.iteration, out=out, targets=self.tokens[j, 1:] if st.last else None)
+            key = ("F", s, op.slab, out.data_ptr() if out is not None else 0)
+            self._run_body(key, lambda: st.forward_body(slab, out), stream)
             if self.verify_roundtrip and (s, j) in self.prog.offloaded:
                 self.digests[(s, j)] = [_digest(slab.base), None]
         self.ev(("F_end", s, j)).record(stream)
@@ -325,14 +329,37 @@ class RankRunner:
             slab = self.slab(op.slab, s)
             if self.verify_roundtrip and (s, j) in self.prog.offloaded:
                 self.digests[(s, j)][1] = _digest(slab.base)
+            st.set_pass_context(j, self.iteration, self.tokens[j] if st.first else None)
             dy = None
             if not st.last:
                 dy = self.rings["recv_grad"][op.ring] if op.ring is not None else self.synthetic_dy
             dx_out = None
             if not st.first:
                 dx_out = self.rings["send_grad"][op.send_ring] if op.send_ring is not None else self.scratch_out
-            st.backward(slab, j, self.iteration, dy=dy, dx_out=dx_out, tokens=self.tokens[j, :-1] if st.first else None)
+            key = ("B", s, op.slab, dy.data_ptr() if dy is not None else 0, dx_out.data_ptr() if dx_out is not None else 0)
+            self._run_body(key, lambda: st.backward_body(slab, dy, dx_out), stream)
         self.ev(("B_end", s, j)).record(stream)
+
+    def _run_body(self, key, body, stream):
+        """Run one F/B pass body; with graphs on, the first run of each (pass, slab,
+        boundary buffer) key is eager and is then captured, later runs replay it.
+        Capture uses the low-level begin/end API (no device synchronisation), so it is
+        safe mid-iteration and across NCCL ranks."""
+        if not self.use_graphs:
+            body()
+            return
+        graph = self.graphs.get(key)
+        if graph is not None:
+            graph.replay()
+            return
+        body()
+        graph = torch.cuda.CUDAGraph()
+        graph.capture_begin(capture_error_mode="thread_local")
+        try:
+            body()
+        finally:
+            graph.capture_end()
+        self.graphs[key] = graph
 
     def _transfer(self, op, stream):
         s, j = op.stage, op.mb
@@ -516,12 +543,14 @@ class RunResult:
     peak_slabs: dict  # rank -> arena slabs (= planned peak units)
     host_slots: dict
     wall_seconds: list  # e2e: host clock per step incl. input H2D and result D2H
+    host_issue_seconds: list = field(default_factory=list)  # host time to enqueue one iteration
 
 
 def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelConfig, microbatches: int | None = None,
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
-            lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False) -> RunResult:
+            lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
+            use_graphs: bool = True) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
@@ -544,12 +573,13 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
 
         transport = NcclTransport(ranks[0], dist.get_world_size(), dev.index, pipeline_edges(sched))
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
-                          params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip) for r in ranks]
+                          params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
+                          use_graphs=use_graphs) for r in ranks]
     if tokens is None:
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
     tokens_dev = torch.empty(tokens.shape, dtype=torch.int64, device=dev)
-    secs, losses, walls = [], [], []
+    secs, losses, walls, host_secs = [], [], [], []
     torch.cuda.synchronize(dev)
     for it in range(warmup + iters):
         if it == warmup and probe_kernels:
@@ -560,7 +590,9 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         tokens_dev.copy_(tokens, non_blocking=True)  # H2D of the step's inputs (pinned host)
         for r in runners:
             r.begin_iteration(tokens_dev)
+        host0 = time.perf_counter()
         drive(runners)
+        host_issue = time.perf_counter() - host0
         for r in runners:
             r.end_iteration()
         result = [r.result_scalar() for r in runners]
@@ -572,6 +604,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         if it >= warmup:
             torch.cuda.synchronize(dev)
             walls.append(wall)
+            host_secs.append(host_issue)
             secs.append(max(r.iteration_seconds() for r in runners))
             ls = [v for r, v in zip(runners, values) if r.loss_sum() is not None]
             losses.append(ls[0] / m if ls else None)
@@ -580,4 +613,4 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
     return RunResult(trace, secs, losses, programs, runners, slab_bytes,
                      {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners},
-                     walls)
+                     walls, host_secs)

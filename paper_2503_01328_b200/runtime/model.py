@@ -144,6 +144,10 @@ class Stage:
             "da": torch.empty(s, h, **bf), "t": torch.empty(s, h, **bf), "dy": torch.empty(s, h, **bf),
         }
         self.loss_sum = torch.zeros((), device=self.device, dtype=torch.float32)
+        # Per-pass context in device memory, so a captured pass (CUDA graph) serves every
+        # microbatch: ctx[0] = Philox offset base of (iteration, mb); tok = token row.
+        self.ctx = torch.zeros(1, device=self.device, dtype=torch.int64)
+        self.tok = torch.zeros(cfg.seq + 1, device=self.device, dtype=torch.int64)
         self._attn_meta = None
         self.probe = None  # kernel name -> [bytes_per_launch, [(start_event, end_event), ...]]
 
@@ -169,9 +173,17 @@ class Stage:
         v = qkv.view(1, cfg.seq, 3, cfg.heads, cfg.head_dim)
         return [v[:, :, i].transpose(1, 2) for i in range(3)]
 
-    def _offsets(self, l_global: int, mb: int, iteration: int):
-        return (dropout_offset(self.cfg, iteration, l_global, mb, self.m, 0),
-                dropout_offset(self.cfg, iteration, l_global, mb, self.m, 1))
+    def _offsets(self, l_global: int):
+        """Per-layer constant parts of the Philox offsets (attention branch, MLP branch);
+        the (iteration, mb) part is ``self.ctx[0]`` (see dropout_offset)."""
+        base = l_global * self.m * 2
+        return base, base + 1
+
+    def set_pass_context(self, mb: int, iteration: int, tokens: torch.Tensor | None = None):
+        """Stream-ordered update of the per-pass device context (eager, never captured)."""
+        self.ctx.fill_(iteration * self.cfg.n_layers * self.m * 2 + mb * 2)
+        if tokens is not None:
+            self.tok.copy_(tokens, non_blocking=True)
 
     def zero_grad(self):
         for t in self.g.values():
@@ -179,14 +191,22 @@ class Stage:
         self.loss_sum.zero_()
 
     # ---------------------------------------------------------------- forward
-    def embed(self, slab: SlabView, tokens: torch.Tensor):
-        """x0 = wte[tokens] + wpe written into layer 0's x slot (first stage)."""
+    def embed(self, slab: SlabView, tokens: torch.Tensor | None = None):
+        """x0 = wte[tokens[:-1]] + wpe written into layer 0's x slot (first stage).
+        ``tokens``: the microbatch's [s+1] token row (None: use the pass context)."""
+        if tokens is not None:
+            self.tok.copy_(tokens, non_blocking=True)
         x0 = slab.get(0, "x")
-        torch.add(torch.nn.functional.embedding(tokens, self.w["wte"]), self.w["wpe"], out=x0)
+        torch.add(torch.nn.functional.embedding(self.tok[:-1], self.w["wte"]), self.w["wpe"], out=x0)
 
     def forward(self, slab: SlabView, mb: int, iteration: int, out: torch.Tensor | None = None,
-                targets: torch.Tensor | None = None):
-        """Run the stage's layers on the activation already in slab x[0].
+                tokens: torch.Tensor | None = None):
+        self.set_pass_context(mb, iteration, tokens)
+        self.forward_body(slab, out)
+
+    def forward_body(self, slab: SlabView, out: torch.Tensor | None = None):
+        """Run the stage's layers on the activation already in slab x[0]; reads only
+        fixed buffers and the pass context, so it can be captured in a CUDA graph.
 
         Non-last stages write the stage output into ``out`` (the send buffer);
         the last stage computes the loss and its output gradient (into the slab's
@@ -198,7 +218,7 @@ class Stage:
         n_local = len(self.layers)
         native.layernorm_fwd(slab.get(0, "x"), self.p(self.layers[0], "ln1_g"), self.p(self.layers[0], "ln1_b"), ws["ln"], eps)
         for i, l in enumerate(self.layers):
-            off_a, off_m = self._offsets(l, mb, iteration)
+            off_a, off_m = self._offsets(l)
             x, qkv, h1, f = slab.get(i, "x"), slab.get(i, "qkv"), slab.get(i, "h1"), slab.get(i, "f")
             torch.mm(ws["ln"], self.p(l, "w_qkv").t(), out=qkv)
             q, k, v = self._qkv_views(qkv)
@@ -212,20 +232,21 @@ class Stage:
             o = slab.get(i, "o")
             torch.mm(o, self.p(l, "w_proj").t(), out=ws["a"])
             self._k("residual_dropout_ln_fwd", 8 * s * h, native.residual_dropout_ln_fwd, x, ws["a"], h1, self.p(l, "ln2_g"),
-                    self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps)
+                    self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps, offset_base=self.ctx)
             torch.mm(ws["ln"], self.p(l, "w_fc1").t(), out=f)
             self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])
             torch.mm(ws["g"], self.p(l, "w_fc2").t(), out=ws["a"])
             if i + 1 < n_local:
                 nxt = self.layers[i + 1]
                 native.residual_dropout_ln_fwd(h1, ws["a"], slab.get(i + 1, "x"), self.p(nxt, "ln1_g"),
-                                               self.p(nxt, "ln1_b"), ws["ln"], p, seed, off_m, eps)
+                                               self.p(nxt, "ln1_b"), ws["ln"], p, seed, off_m, eps, offset_base=self.ctx)
             elif self.last:
                 native.residual_dropout_ln_fwd(h1, ws["a"], ws["dy"], self.w["lnf_g"], self.w["lnf_b"], ws["ln"],
-                                               p, seed, off_m, eps)
-                self._head(slab, targets)
+                                               p, seed, off_m, eps, offset_base=self.ctx)
+                self._head(slab, self.tok[1:])
             else:
-                native.residual_dropout_ln_fwd(h1, ws["a"], out, None, None, None, p, seed, off_m, eps)
+                native.residual_dropout_ln_fwd(h1, ws["a"], out, None, None, None, p, seed, off_m, eps,
+                                               offset_base=self.ctx)
 
     def _pack_attention(self, slab: SlabView, i: int, o_tmp: torch.Tensor, lse: torch.Tensor):
         s, h, H = self.cfg.seq, self.cfg.hidden, self.cfg.heads
@@ -255,6 +276,10 @@ class Stage:
     # --------------------------------------------------------------- backward
     def backward(self, slab: SlabView, mb: int, iteration: int, dy: torch.Tensor | None = None,
                  dx_out: torch.Tensor | None = None, tokens: torch.Tensor | None = None):
+        self.set_pass_context(mb, iteration, tokens)
+        self.backward_body(slab, dy, dx_out)
+
+    def backward_body(self, slab: SlabView, dy: torch.Tensor | None = None, dx_out: torch.Tensor | None = None):
         """Backward of the stage from the output gradient ``dy`` (received) or,
         on the last stage, the head gradient saved in the slab.  Writes the input
         gradient into ``dx_out`` (send buffer); the first stage scatters it into
@@ -264,11 +289,11 @@ class Stage:
         s, h = cfg.seq, cfg.hidden
         n_local = len(self.layers)
         dy_cur = slab.get(-1, "head_dy") if self.last else dy
-        top_off_m = self._offsets(self.layers[-1], mb, iteration)[1]
-        native.dropout(dy_cur, ws["dm"], p, seed, top_off_m)
+        top_off_m = self._offsets(self.layers[-1])[1]
+        native.dropout(dy_cur, ws["dm"], p, seed, top_off_m, offset_base=self.ctx)
         for i in range(n_local - 1, -1, -1):
             l = self.layers[i]
-            off_a, _ = self._offsets(l, mb, iteration)
+            off_a, _ = self._offsets(l)
             x, qkv, o, lse, h1, f = (slab.get(i, n) for n in ("x", "qkv", "o", "lse", "h1", "f"))
             dg = ws["big"]
             # MLP: dg = dm @ Wfc2; g = gelu(f) recomputed; df = dg * gelu'(f)
@@ -280,7 +305,8 @@ class Stage:
             torch.mm(dg, self.p(l, "w_fc1"), out=ws["t"])
             # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay)
             self._k("layernorm_bwd", 10 * s * h, native.layernorm_bwd, h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"],
-                    self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=ws["da"], p=p, drop_seed=seed, drop_offset=off_a, eps=eps)
+                    self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=ws["da"], p=p, drop_seed=seed, drop_offset=off_a, eps=eps,
+                    offset_base=self.ctx)
             # attention projection and core
             _wgrad(self.gp(l, "w_proj"), ws["da"].t(), o)
             torch.mm(ws["da"], self.p(l, "w_proj"), out=ws["t"])
@@ -303,13 +329,13 @@ class Stage:
             below = i > 0
             dx_target = ws["dy"] if (below or self.first or dx_out is None) else dx_out
             drop_below = ws["dm"] if below else None
-            off_below = self._offsets(self.layers[i - 1], mb, iteration)[1] if below else 0
+            off_below = self._offsets(self.layers[i - 1])[1] if below else 0
             native.layernorm_bwd(x, self.p(l, "ln1_g"), ws["t"], ws["dh1"], dx_target, self.gp(l, "ln1_g"),
                                  self.gp(l, "ln1_b"), drop_out=drop_below, p=p if below else 0.0,
-                                 drop_seed=seed, drop_offset=off_below, eps=eps)
+                                 drop_seed=seed, drop_offset=off_below, eps=eps, offset_base=self.ctx)
             dy_cur = dx_target
         if self.first:
-            self.g["wte"].index_add_(0, tokens, dy_cur.float())
+            self.g["wte"].index_add_(0, self.tok[:-1], dy_cur.float())
             self.g["wpe"].add_(dy_cur.float())
 
     # -------------------------------------------------------------- optimizer

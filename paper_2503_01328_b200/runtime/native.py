@@ -66,9 +66,9 @@ SIGNATURES = {
     "ppo_transfer": [_I32, ctypes.POINTER(Segment), _I32, _VP, _VP, _VP],
     "ppo_pack": [ctypes.POINTER(GatherItem), _I32, _VP, _VP],
     "ppo_layernorm_fwd": [_VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP],
-    "ppo_residual_dropout_ln_fwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _F32, _U64, _U64, _VP],
-    "ppo_layernorm_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP, _F32, _U64, _U64, _VP],
-    "ppo_dropout": [_VP, _VP, _I64, _F32, _U64, _U64, _VP],
+    "ppo_residual_dropout_ln_fwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _F32, _U64, _U64, _VP, _VP],
+    "ppo_layernorm_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP, _F32, _U64, _U64, _VP, _VP],
+    "ppo_dropout": [_VP, _VP, _I64, _F32, _U64, _U64, _VP, _VP],
     "ppo_gelu_fwd": [_VP, _VP, _I64, _VP],
     "ppo_gelu_bwd": [_VP, _VP, _VP, _VP, _I64, _VP],
     "ppo_colsum": [_VP, _VP, _I64, _I64, _VP],
@@ -103,7 +103,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 1:
+        if lib.ppo_abi_version() != 2:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -164,28 +164,31 @@ def layernorm_fwd(x, gamma, beta, y, eps=1e-5, stream=None):
     call("ppo_layernorm_fwd", _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), x.numel() // h, h, eps, _stream(stream))
 
 
-def residual_dropout_ln_fwd(resid, branch, out, gamma, beta, ln, p, seed, offset, eps=1e-5, stream=None):
+def residual_dropout_ln_fwd(resid, branch, out, gamma, beta, ln, p, seed, offset, eps=1e-5, stream=None,
+                            offset_base=None):
+    """offset_base: optional 1-element uint64/int64 device tensor added to ``offset``."""
     _check_bf16(resid, branch, out, ln)
     h = resid.shape[-1]
     call(
         "ppo_residual_dropout_ln_fwd", _ptr(resid), _ptr(branch), _ptr(out), _ptr(gamma), _ptr(beta), _ptr(ln),
-        resid.numel() // h, h, eps, p, seed, offset, _stream(stream),
+        resid.numel() // h, h, eps, p, seed, offset, _ptr(offset_base), _stream(stream),
     )
 
 
 def layernorm_bwd(x, gamma, dy, resid_grad, dx, dgamma, dbeta, drop_out=None, p=0.0, drop_seed=0,
-                  drop_offset=0, eps=1e-5, stream=None):
+                  drop_offset=0, eps=1e-5, stream=None, offset_base=None):
     _check_bf16(x, dy, resid_grad, dx, drop_out)
     h = x.shape[-1]
     call(
         "ppo_layernorm_bwd", _ptr(x), _ptr(gamma), _ptr(dy), _ptr(resid_grad), _ptr(dx), _ptr(dgamma),
-        _ptr(dbeta), x.numel() // h, h, eps, _ptr(drop_out), p, drop_seed, drop_offset, _stream(stream),
+        _ptr(dbeta), x.numel() // h, h, eps, _ptr(drop_out), p, drop_seed, drop_offset, _ptr(offset_base),
+        _stream(stream),
     )
 
 
-def dropout(x, y, p, seed, offset, stream=None):
+def dropout(x, y, p, seed, offset, stream=None, offset_base=None):
     _check_bf16(x, y)
-    call("ppo_dropout", _ptr(x), _ptr(y), x.numel(), p, seed, offset, _stream(stream))
+    call("ppo_dropout", _ptr(x), _ptr(y), x.numel(), p, seed, offset, _ptr(offset_base), _stream(stream))
 
 
 def gelu_fwd(f, g, stream=None):

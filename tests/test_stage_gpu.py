@@ -34,9 +34,9 @@ def test_single_stage_loss_and_grads_match_oracle():
     st.zero_grad()
     for mb in range(m):
         tok = tokens[mb].to(DEV)
-        st.embed(slab, tok[:-1])
-        st.forward(slab, mb, 0, targets=tok[1:])
-        st.backward(slab, mb, 0, tokens=tok[:-1])
+        st.embed(slab, tok)
+        st.forward(slab, mb, 0, tokens=tok)
+        st.backward(slab, mb, 0, tokens=tok)
     torch.cuda.synchronize()
     loss = float(st.loss_sum) / m
     assert abs(loss - want_loss) < 2e-2 * abs(want_loss), (loss, want_loss)
