@@ -358,7 +358,11 @@ def run_b200(args, rank, world, local_rank):
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
                       stream_mode="dual" if name in ("full_dual", "full_duplex") else "single")
-        launches[name] = (native.kernel_launches() - before) / (args.steps + args.warmup)
+        # real launches = eager launches + kernels executed by graph replays
+        # (launch calls made while capturing a graph record nodes, they do not run)
+        replayed = sum(r.replayed_native_launches for r in res.runners)
+        captured = sum(sum(r.graph_native_launches.values()) for r in res.runners)
+        launches[name] = (native.kernel_launches() - before - captured + replayed) / (args.steps + args.warmup)
         if name == "full":
             sampler.__exit__()
             clocks = sampler.summary()

@@ -37,7 +37,7 @@ from .lower import RING, Program, lower
 from .model import ModelConfig, SlabView, Stage, stage_layers
 
 STREAMS = ("compute", "copy", "copy_h2d", "recv_act", "send_act", "recv_grad", "send_grad")
-TIMED = ("F_start", "F_end", "B_start", "B_end", "D2H", "H2D", "D2H_start", "H2D_start")
+TIMED = ("F_start", "F_end", "B_start", "B_end", "W_start", "W_end", "D2H", "H2D", "D2H_start", "H2D_start")
 
 
 class DeadlockError(RuntimeError):
@@ -215,6 +215,9 @@ class RankRunner:
         self.verify_roundtrip = verify_roundtrip
         self.use_graphs = use_graphs
         self.graphs = {}
+        self.wbufs = {}
+        self.graph_native_launches = {}  # libppo_b200 kernels inside each captured pass
+        self.replayed_native_launches = 0  # ... executed through graph replays
         self.digests = {}  # (stage, mb) -> [digest at F end, digest at B start]
         self._adam = None
         self.cursor = 0
@@ -287,6 +290,8 @@ class RankRunner:
             self._forward(op, stream)
         elif op.kind == "B":
             self._backward(op, stream)
+        elif op.kind == "W":
+            self._wgrad(op, stream)
         elif op.kind in ("OFFLOAD", "RELOAD"):
             self._transfer(op, stream)
         elif op.kind in ("SEND_ACT", "SEND_GRAD"):
@@ -336,9 +341,31 @@ class RankRunner:
             dx_out = None
             if not st.first:
                 dx_out = self.rings["send_grad"][op.send_ring] if op.send_ring is not None else self.scratch_out
-            key = ("B", s, op.slab, dy.data_ptr() if dy is not None else 0, dx_out.data_ptr() if dx_out is not None else 0)
-            self._run_body(key, lambda: st.backward_body(slab, dy, dx_out), stream)
+            wbuf = self.wbuf(op.wbuf, s) if op.wbuf is not None else None
+            key = ("B", s, op.slab, dy.data_ptr() if dy is not None else 0, dx_out.data_ptr() if dx_out is not None else 0,
+                   op.wbuf)
+            self._run_body(key, lambda: st.backward_body(slab, dy, dx_out, wbuf), stream)
         self.ev(("B_end", s, j)).record(stream)
+
+    def _wgrad(self, op, stream):
+        s, j = op.stage, op.mb
+        st = self.stages[s]
+        self.ev(("W_start", s, j)).record(stream)
+        with torch.cuda.stream(stream):
+            slab = self.slab(op.slab, s)
+            wbuf = self.wbuf(op.wbuf, s)
+            self._run_body(("W", s, op.slab, op.wbuf), lambda: st.wgrad_body(slab, wbuf), stream)
+        self.ev(("W_end", s, j)).record(stream)
+
+    def wbuf(self, idx: int, stage: int) -> dict:
+        """Split-backward gradient buffers of colour ``idx`` (shared by the rank's stages
+        of equal depth; allocated once, before the first use)."""
+        st = self.stages[stage]
+        key = (idx, len(st.layers))
+        b = self.wbufs.get(key)
+        if b is None:
+            b = self.wbufs[key] = st.new_wbuffer()
+        return b
 
     def _run_body(self, key, body, stream):
         """Run one F/B pass body; with graphs on, the first run of each (pass, slab,
@@ -351,15 +378,18 @@ class RankRunner:
         graph = self.graphs.get(key)
         if graph is not None:
             graph.replay()
+            self.replayed_native_launches += self.graph_native_launches[key]
             return
         body()
         graph = torch.cuda.CUDAGraph()
+        before = native.kernel_launches()
         graph.capture_begin(capture_error_mode="thread_local")
         try:
             body()
         finally:
             graph.capture_end()
         self.graphs[key] = graph
+        self.graph_native_launches[key] = native.kernel_launches() - before
 
     def _transfer(self, op, stream):
         s, j = op.stage, op.mb
@@ -437,7 +467,7 @@ class RankRunner:
         sec = lambda ev: Fraction(t0.elapsed_time(ev)) / 1000  # noqa: E731
         out = []
         for (kind, s, j) in self.prog.compute_order:
-            a, b = self.events[(f"{kind}_start", s, j)], self.events[(f"{kind}_end", s, j)]
+            a, b = self.events[(f"{kind}_start", s, j)], self.events[(f"{kind}_end", s, j)]  # F, B or W
             st = sec(a)
             out.append(Pass(PassKind(kind), self.rank, s, j, st, sec(b) - st))
         for op in self.prog.ops:

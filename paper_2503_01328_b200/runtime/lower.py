@@ -60,6 +60,7 @@ class Op:
     peer: int | None = None  # remote rank of a boundary op
     anchor: tuple | None = None  # reload anchor event
     send_ring: int | None = None  # ring slot of the boundary send this compute op feeds
+    wbuf: int | None = None  # split backward: gradient buffer shared by a B and its W
 
     @property
     def key(self):
@@ -73,6 +74,7 @@ class Program:
     ops: list  # host issue order
     n_slabs: int
     n_host_slots: int
+    n_wbufs: int
     offloaded: set
     witness_makespan: Fraction
     witness_peak_units: int
@@ -144,8 +146,10 @@ def lower(
     trace = simulate(sched, plan, stream_mode=stream_mode)
     timed = {(p.kind, p.stage, p.microbatch): p for p in trace.passes}
     my_passes = [timed[(p.kind, p.stage, p.microbatch)] for p in sched.device_passes[rank]]
-    if any(p.kind == W for p in my_passes):
-        raise NotImplementedError("split-backward (W) execution is the next row (SURVEY 8f-1)")
+    split = sched.split_backward
+    # with a split backward the W pass still reads the slab (and the B pass's gradient
+    # buffer): residency ends at W end (the reference's model frees at B end, ir.py:630-655)
+    last_use = W if split else B
     placement = sched.placement
     last_stage = sched.num_stages - 1
     ops: list[Op] = []
@@ -162,11 +166,14 @@ def lower(
     for p in my_passes:
         pair = (p.stage, p.microbatch)
         if p.kind == F:
-            end = d2h[pair].end if pair in offloaded else timed[(B, p.stage, p.microbatch)].end
+            done = timed[(last_use, p.stage, p.microbatch)].end
+            end = d2h[pair].end if pair in offloaded else done
             intervals.append((p.start, end, ("F",) + pair))
             if pair in offloaded:
-                intervals.append((h2d[pair].start, timed[(B, p.stage, p.microbatch)].end, ("R",) + pair))
+                intervals.append((h2d[pair].start, done, ("R",) + pair))
     slab_of, n_slabs = _colour(intervals)
+    wbuf_of, n_wbufs = _colour([(timed[(B,) + pr].start, timed[(W,) + pr].end, ("G",) + pr)
+                                for pr in ((p.stage, p.microbatch) for p in my_passes if p.kind == B)]) if split else ({}, 0)
     host_of, n_host = _colour([(d2h[pr].start, h2d[pr].end, ("H",) + pr) for pr in sorted(offloaded)])
 
     def release_event(holder):
@@ -176,7 +183,7 @@ def lower(
         tag, s, j = holder
         if tag == "F" and (s, j) in offloaded:
             return ("D2H", s, j)
-        return ("B_end", s, j)
+        return (f"{last_use}_end", s, j)
 
     # --------------------------------------------------------- boundary rings
     recv_orders: dict = {}
@@ -236,6 +243,13 @@ def lower(
                     ops.append(snd)
                 elif dst == rank and not emulate_neighbors:
                     raise NotImplementedError("consecutive stages on one device (d=1, v>1) are not lowered")
+        elif p.kind == W:
+            op = Op("W", s, j, "compute", p.start)
+            op.records = [("W_start", s, j), ("W_end", s, j)]
+            op.slab = slab_of[(("R",) if pair in offloaded else ("F",)) + pair][0]
+            op.wbuf = wbuf_of[("G",) + pair][0]
+            compute_ops.append(op)
+            continue
         else:  # B
             op = Op("B", s, j, "compute", p.start)
             op.records = [("B_start", s, j), ("B_end", s, j)]
@@ -244,6 +258,8 @@ def lower(
                 op.slab = slab_of[("R",) + pair][0]
             else:
                 op.slab = slab_of[("F",) + pair][0]
+            if split:
+                op.wbuf = wbuf_of[("G",) + pair][0]
             if s < last_stage:
                 src = placement[s + 1]
                 if not emulate_neighbors and src != rank:
@@ -316,13 +332,13 @@ def lower(
     assert got == want, "lowering changed the per-device op order"
     peak = trace.memory.peak(rank)
     return Program(
-        rank=rank, devices=sched.devices, ops=ordered, n_slabs=n_slabs, n_host_slots=n_host,
+        rank=rank, devices=sched.devices, ops=ordered, n_slabs=n_slabs, n_host_slots=n_host, n_wbufs=n_wbufs,
         offloaded=offloaded, witness_makespan=trace.makespan, witness_peak_units=peak,
         compute_order=want, copy_order=copy_order, recv_orders=recv_orders, send_orders=send_orders,
     )
 
 
-_KIND_PRIORITY = {"OFFLOAD": 0, "RELOAD": 1, "SEND_ACT": 2, "SEND_GRAD": 2, "RECV_ACT": 3, "RECV_GRAD": 3, "F": 4, "B": 4}
+_KIND_PRIORITY = {"OFFLOAD": 0, "RELOAD": 1, "SEND_ACT": 2, "SEND_GRAD": 2, "RECV_ACT": 3, "RECV_GRAD": 3, "F": 4, "B": 4, "W": 4}
 
 
 def host_order(ops: list[Op]) -> list[Op]:

@@ -279,37 +279,57 @@ class Stage:
         self.set_pass_context(mb, iteration, tokens)
         self.backward_body(slab, dy, dx_out)
 
-    def backward_body(self, slab: SlabView, dy: torch.Tensor | None = None, dx_out: torch.Tensor | None = None):
+    def new_wbuffer(self) -> dict:
+        """Gradient tensors a deferred W pass needs (split backward, GIS/PO schedules):
+        per local layer dm [s,h], df [s,4h], da [s,h] and dq/dk/dv [3,s,h] (18bsh bytes)."""
+        s, h = self.cfg.seq, self.cfg.hidden
+        bf = dict(device=self.device, dtype=torch.bfloat16)
+        return {i: {"dm": torch.empty(s, h, **bf), "df": torch.empty(s, 4 * h, **bf), "da": torch.empty(s, h, **bf),
+                    "dqkv": torch.empty(3, s, h, **bf)} for i in range(len(self.layers))}
+
+    def backward_body(self, slab: SlabView, dy: torch.Tensor | None = None, dx_out: torch.Tensor | None = None,
+                      wbuf: dict | None = None):
         """Backward of the stage from the output gradient ``dy`` (received) or,
         on the last stage, the head gradient saved in the slab.  Writes the input
         gradient into ``dx_out`` (send buffer); the first stage scatters it into
-        the embedding gradients instead."""
+        the embedding gradients instead.
+
+        With ``wbuf`` this is the B pass of a split backward (reference PassKind.B with
+        ``split_backward``, ir.py:27-32): activation gradients only; the tensors the
+        weight gradients need are left in ``wbuf`` for ``wgrad_body`` (the W pass), which
+        also owns the LN1/LN2/GeLU recomputes that only weight gradients use."""
         cfg, ws = self.cfg, self.ws
         p, seed, eps = cfg.p_drop, cfg.dropout_seed, cfg.eps
         s, h = cfg.seq, cfg.hidden
         n_local = len(self.layers)
+        split = wbuf is not None
+        dm_of = (lambda i: wbuf[i]["dm"]) if split else (lambda i: ws["dm"])  # noqa: E731
         dy_cur = slab.get(-1, "head_dy") if self.last else dy
         top_off_m = self._offsets(self.layers[-1])[1]
-        native.dropout(dy_cur, ws["dm"], p, seed, top_off_m, offset_base=self.ctx)
+        native.dropout(dy_cur, dm_of(n_local - 1), p, seed, top_off_m, offset_base=self.ctx)
         for i in range(n_local - 1, -1, -1):
             l = self.layers[i]
             off_a, _ = self._offsets(l)
             x, qkv, o, lse, h1, f = (slab.get(i, n) for n in ("x", "qkv", "o", "lse", "h1", "f"))
-            dg = ws["big"]
-            # MLP: dg = dm @ Wfc2; g = gelu(f) recomputed; df = dg * gelu'(f)
-            torch.mm(ws["dm"], self.p(l, "w_fc2"), out=dg)
-            self._k("gelu_bwd", 32 * s * h, native.gelu_bwd, f, dg, ws["g"], dg)
-            _wgrad(self.gp(l, "w_fc2"), ws["dm"].t(), ws["g"])
-            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
-            _wgrad(self.gp(l, "w_fc1"), dg.t(), ws["ln"])
+            dm = dm_of(i)
+            dg = wbuf[i]["df"] if split else ws["big"]
+            da = wbuf[i]["da"] if split else ws["da"]
+            # MLP: dg = dm @ Wfc2; df = dg * gelu'(f) (in place); g = gelu(f) recomputed for dWfc2
+            torch.mm(dm, self.p(l, "w_fc2"), out=dg)
+            self._k("gelu_bwd", 32 * s * h, native.gelu_bwd, f, dg, None if split else ws["g"], dg)
+            if not split:
+                _wgrad(self.gp(l, "w_fc2"), dm.t(), ws["g"])
+                self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
+                _wgrad(self.gp(l, "w_fc1"), dg.t(), ws["ln"])
             torch.mm(dg, self.p(l, "w_fc1"), out=ws["t"])
             # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay)
             self._k("layernorm_bwd", 10 * s * h, native.layernorm_bwd, h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"],
-                    self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=ws["da"], p=p, drop_seed=seed, drop_offset=off_a, eps=eps,
+                    self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=da, p=p, drop_seed=seed, drop_offset=off_a, eps=eps,
                     offset_base=self.ctx)
             # attention projection and core
-            _wgrad(self.gp(l, "w_proj"), ws["da"].t(), o)
-            torch.mm(ws["da"], self.p(l, "w_proj"), out=ws["t"])
+            if not split:
+                _wgrad(self.gp(l, "w_proj"), da.t(), o)
+            torch.mm(da, self.p(l, "w_proj"), out=ws["t"])
             q, k, v = self._qkv_views(qkv)
             o4 = o.view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
             do4 = ws["t"].view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
@@ -317,18 +337,22 @@ class Stage:
             cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
             dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
                 do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
-            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
             w_qkv, g_qkv = self.p(l, "w_qkv"), self.gp(l, "w_qkv")
             grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
-            for j, gj in enumerate(grads):
-                _wgrad(g_qkv[j * h:(j + 1) * h], gj.t(), ws["ln"])
+            if split:
+                for j, gj in enumerate(grads):
+                    wbuf[i]["dqkv"][j].copy_(gj)
+            else:
+                self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
+                for j, gj in enumerate(grads):
+                    _wgrad(g_qkv[j * h:(j + 1) * h], gj.t(), ws["ln"])
             torch.mm(grads[0], w_qkv[0:h], out=ws["t"])
             torch.addmm(ws["t"], grads[1], w_qkv[h:2 * h], out=ws["t"])
             torch.addmm(ws["t"], grads[2], w_qkv[2 * h:3 * h], out=ws["t"])
             # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay
             below = i > 0
             dx_target = ws["dy"] if (below or self.first or dx_out is None) else dx_out
-            drop_below = ws["dm"] if below else None
+            drop_below = dm_of(i - 1) if below else None
             off_below = self._offsets(self.layers[i - 1])[1] if below else 0
             native.layernorm_bwd(x, self.p(l, "ln1_g"), ws["t"], ws["dh1"], dx_target, self.gp(l, "ln1_g"),
                                  self.gp(l, "ln1_b"), drop_out=drop_below, p=p if below else 0.0,
@@ -337,6 +361,24 @@ class Stage:
         if self.first:
             self.g["wte"].index_add_(0, self.tok[:-1], dy_cur.float())
             self.g["wpe"].add_(dy_cur.float())
+
+    def wgrad_body(self, slab: SlabView, wbuf: dict):
+        """W pass of a split backward: weight gradients from the slab (recomputing
+        LN1, LN2 and GeLU) and the gradients the B pass left in ``wbuf``."""
+        cfg, ws = self.cfg, self.ws
+        s, h, eps = cfg.seq, cfg.hidden, cfg.eps
+        for i, l in enumerate(self.layers):
+            x, o, h1, f = (slab.get(i, n) for n in ("x", "o", "h1", "f"))
+            b = wbuf[i]
+            self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])  # GeLU recompute
+            _wgrad(self.gp(l, "w_fc2"), b["dm"].t(), ws["g"])
+            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)
+            _wgrad(self.gp(l, "w_fc1"), b["df"].t(), ws["ln"])
+            _wgrad(self.gp(l, "w_proj"), b["da"].t(), o)
+            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)
+            g_qkv = self.gp(l, "w_qkv")
+            for j in range(3):
+                _wgrad(g_qkv[j * h:(j + 1) * h], b["dqkv"][j].t(), ws["ln"])
 
     # -------------------------------------------------------------- optimizer
     def sgd_step(self, lr: float = 1e-4):

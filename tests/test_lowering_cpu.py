@@ -42,6 +42,7 @@ class CpuWalker:
         self.cursor = 0
         self.grad_out = {}  # (stage, mb) -> input gradient produced by B
         self.live = set()
+        self.wbufs = {}
 
     def done(self):
         return self.cursor >= len(self.prog.ops)
@@ -76,10 +77,20 @@ class CpuWalker:
             g = x + 1.0 if op.stage == last else self.rings["recv_grad"][op.ring]
             gx = 2.0 * g
             self.grad_out[pair] = gx
-            self.live.discard(pair)
-            self.slabs[op.slab] = None
+            if self.sched.split_backward:
+                assert self.wbufs.get(op.wbuf) is None, "gradient buffer still in use"
+                self.wbufs[op.wbuf] = pair
+            else:
+                self.live.discard(pair)
+                self.slabs[op.slab] = None
             if op.stage > 0 and op.send_ring is not None:
                 self.rings["send_grad"][op.send_ring] = gx
+        elif op.kind == "W":
+            assert self.slabs[op.slab][0] == pair, f"W{pair} found slab holding {self.slabs[op.slab][0]}"
+            assert self.wbufs.get(op.wbuf) == pair, f"W{pair} found gradient buffer of {self.wbufs.get(op.wbuf)}"
+            self.wbufs[op.wbuf] = None
+            self.live.discard(pair)
+            self.slabs[op.slab] = None
         elif op.kind in ("SEND_ACT", "SEND_GRAD"):
             ring = "send_act" if op.kind == "SEND_ACT" else "send_grad"
             self.channel.send(op, self.rings[ring][op.ring])
@@ -144,6 +155,9 @@ CASES = [
     ("1f1b-i d4 v2 n1", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(4, 2, U), 1), Fraction(1))))(po.build_interleaved_1f1b(4, 2, 8, U))),
     ("1f1b-i d8 v4 n2", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(8, 4, U), 2), Fraction(3, 2))))(po.build_interleaved_1f1b(8, 4, 16, U))),
     ("1f1b d4 no offload", lambda: (po.build_1f1b(4, 1, 8, U), None)),
+    ("gis d4 v2 n1 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(4, 2, U), 1), Fraction(1))))(po.build_gis(4, 2, 8, U))),
+    ("gis-h d8 v2 n1 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(8, 2, U), 1), Fraction(3, 2))))(po.build_gis_h(8, 2, 16, U))),
+    ("po d8 v2 n2 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(8, 2, U), 2), Fraction(3))))(po.build_po(8, 2, 16, U))),
 ]
 
 

@@ -119,3 +119,23 @@ def test_cuda_graph_replay_matches_eager(oracle_result):
     for a, b in zip(eager.losses, graph.losses):
         assert abs(a - b) < 1e-3 * abs(a), (eager.losses, graph.losses)
     assert graph.losses[-1] < graph.losses[0]  # SGD at lr 1e-2 makes progress
+
+
+@pytest.mark.parametrize("kind", ["gis-h", "po"])
+def test_split_backward_schedules_match_oracle(kind, oracle_result):
+    """GIS-H and PO (the paper's own schedule family) run B and W as separate passes
+    (dgrad now, weight gradients later); with first-local-stage offload they must still
+    reproduce the serial oracle's loss and gradients."""
+    tokens, want_loss, want_grads = oracle_result
+    U = po.PassCosts.unit()
+    sched = (po.build_gis_h if kind == "gis-h" else po.build_po)(2, 2, 8, U)
+    assert sched.split_backward
+    plan = po.plan_slots(sched, po.select_offload_stages(po.po_block(2, 2, U), 1), Fraction(1))
+    res = ex.execute(sched, plan, model=CFG, mode="virtual", tokens=tokens, optimizer="none", verify_roundtrip=True)
+    assert ex.roundtrip_mismatches(res.runners) == []
+    assert sum(p.n_wbufs for p in res.programs.values()) > 0
+    loss = res.losses[-1]
+    assert abs(loss - want_loss) < 0.02 * abs(want_loss), (loss, want_loss)
+    got = _grads(res)
+    for k, g in want_grads.items():
+        assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
