@@ -345,8 +345,8 @@ def run_b200(args, rank, world, local_rank):
     results = {}
     launches = {}
     clocks = None
-    for name in ("none", "auto", "full", "full_dual", "full_duplex"):
-        plan = plans["full" if name == "full_dual" else name]
+    for name in ("none", "none_cublas", "auto", "full", "full_dual", "full_duplex"):
+        plan = plans["full" if name == "full_dual" else ("none" if name == "none_cublas" else name)]
         if name == "auto" and plan is None:
             results[name] = dict(results["none"], note="k-aware policy keeps everything resident at this k")
             continue
@@ -357,7 +357,8 @@ def run_b200(args, rank, world, local_rank):
         native.CALLS.clear()
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
-                      stream_mode="dual" if name in ("full_dual", "full_duplex") else "single")
+                      stream_mode="dual" if name in ("full_dual", "full_duplex") else "single",
+                      gemm="cublas" if name == "none_cublas" else "best")
         # real launches = eager launches + kernels executed by graph replays
         # (launch calls made while capturing a graph record nodes, they do not run)
         replayed = sum(r.replayed_native_launches for r in res.runners)
@@ -373,6 +374,7 @@ def run_b200(args, rank, world, local_rank):
             r.close()
     full, none, auto, dual = results["full"], results["none"], results["auto"], results["full_dual"]
     duplex = results["full_duplex"]
+    none_cublas = results["none_cublas"]
     slab_bytes = full["_res"].slab_bytes
     for v in results.values():
         v.pop("_res", None)
@@ -431,7 +433,8 @@ def run_b200(args, rank, world, local_rank):
             "k_measured": k_measured,
             "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3, "T_o_ms": float(t_o) * 1e3,
             "slab_bytes": slab_bytes,
-            "no_offload": none, "full": full, "auto": auto, "full_dual_stream": dual, "full_duplex_plan": duplex,
+            "no_offload": none, "no_offload_cublas_gemms": none_cublas, "full": full, "auto": auto,
+            "full_dual_stream": dual, "full_duplex_plan": duplex,
             "auto_stride": choice.stride, "auto_modelled_overhead": choice.overhead,
             "overhead_full_pct": 100 * (none["tokens_per_s"] / full["tokens_per_s"] - 1),
             "overhead_auto_pct": 100 * (none["tokens_per_s"] / auto["tokens_per_s"] - 1),

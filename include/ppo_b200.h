@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 2
+#define PPO_ABI_VERSION 3
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -86,16 +86,18 @@ int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_s
                  void* wait_event, void* done_event);
 
 /* ------------------------------------------------------------ K1: pack / gather */
-/* Gather `n` byte ranges into one destination: dst[dst_off[i] .. + bytes[i]) =
- * src[i][0 .. bytes[i]).  Optional 2-D form: `rows[i]` rows of `row_bytes[i]`
- * with source pitch `src_pitch[i]` (0 = dense).  16-byte vectorised, persistent
- * grid (k x SM count).  All addresses and sizes must be 16-byte aligned. */
+/* Gather `n` 2-D byte ranges into one destination: item i copies `rows[i]` rows of
+ * `row_bytes[i]` from src[i] (row pitch `src_pitch[i]`, 0 = dense) to
+ * dst + dst_off[i] (row pitch `dst_pitch[i]`, 0 = dense).  16-byte vectorised,
+ * persistent grid (k x SM count).  All addresses, sizes and pitches 16-byte aligned.
+ * Used for the attention output + LSE into the slab and for concatenating dq/dk/dv. */
 typedef struct {
   const void* src;
   uint64_t dst_off;
   uint64_t rows;
   uint64_t row_bytes;
   uint64_t src_pitch;
+  uint64_t dst_pitch;
 } ppo_gather_item;
 int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream);
 
@@ -150,6 +152,25 @@ int ppo_gelu_bwd(const void* f, const void* dg, void* g, void* df, int64_t n, vo
 /* Column sums of a rows x cols bf16 matrix accumulated into fp32 `acc` (bias grads,
  * tests). */
 int ppo_colsum(const void* x, float* acc, int64_t rows, int64_t cols, void* stream);
+
+/* --------------------------------------------- K6: tcgen05 GEMMs (sm_100a) */
+/* D[M,N] = A[M,K] . B[N,K]^T, bf16 row-major in and out, fp32 accumulation in TMEM;
+ * 2-SM CTA pairs (tcgen05.mma cta_group::2), TMA loads/stores, persistent schedule.
+ * K and N must be multiples of 8.  (FLOP model: costs.py:144-161.) */
+int ppo_gemm_tn(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, void* stream);
+/* fc1 with the GeLU fused into the epilogue: F = A . B^T (pre-activation, the saved
+ * GeLU input) and G = gelu_tanh(F) (the fc2 operand) from one kernel.  `zero_bias` is a
+ * device fp32 vector of N zeros (the epilogue's per-column bias operand). */
+int ppo_gemm_tn_gelu(const void* A, const void* B, void* G, void* F, const float* zero_bias, int64_t M,
+                     int64_t N, int64_t K, void* stream);
+/* Activation gradient: D[M,N] = A[M,K] . B[K,N]  (dX = dY . W with W = [out, in]). */
+int ppo_gemm_nn(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, void* stream);
+/* fc2 dgrad fused with the GeLU backward: D = (A . B) * gelu_tanh'(Z), Z = saved fc1 output. */
+int ppo_gemm_nn_dgelu(const void* A, const void* B, const void* Z, void* D, int64_t M, int64_t N, int64_t K,
+                      void* stream);
+/* Weight gradient: dW[M,N] (fp32) = beta * dW + dY[K,M]^T . X[K,N]  (K = tokens). */
+int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t N, int64_t K, float beta,
+                   void* stream);
 
 /* ----------------------------------------------- K8: stage-boundary send/recv */
 /* NCCL communicator of the pipeline (one rank per GPU).  The 128-byte unique id is

@@ -1,0 +1,32 @@
+// libppo_b200.so -- K6 weight-gradient GEMM on tcgen05 (see ppo_gemm.cuh).
+//   ppo_gemm_wgrad   dW[M,N] (fp32) += dY[K,M]^T . X[K,N]
+// K = tokens; both operands are the row-major activations as saved, read M/N-major by
+// TMA; accumulation stays fp32 across microbatches (epilogue beta = 1, C = D = dW).
+#include "ppo_gemm.cuh"
+
+using namespace ppo;
+using namespace ppo::gemm;
+
+namespace {
+using Acc = cutlass::epilogue::fusion::LinearCombination<float, float, float, float>;
+using Wgrad = Sm100Gemm<ColMajor, RowMajor, float, Acc, TileWide>;
+}  // namespace
+
+extern "C" {
+
+int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t N, int64_t K, float beta,
+                   void* stream) {
+  using G = Wgrad;
+  if (!dY || !X || !dW || !dims_ok(M, N, K)) return set_error(PPO_EINVAL, "ppo_gemm_wgrad: bad arguments");
+  auto [sa, sb, sc, sd] = G::strides(M, N, K);
+  typename G::Args args{cutlass::gemm::GemmUniversalMode::kGemm,
+                        {(int)M, (int)N, (int)K, 1},
+                        {static_cast<const bf16*>(dY), sa, static_cast<const bf16*>(X), sb},
+                        {{}, beta != 0.f ? dW : nullptr, sc, dW, sd},
+                        hw_info()};
+  args.epilogue.thread.alpha = 1.f;
+  args.epilogue.thread.beta = beta;
+  return launch<G>(args, stream, "ppo_gemm_wgrad");
+}
+
+}  // extern "C"

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(256) pack_kernel(GatherArgs args, uint8_t* __r
     const uint64_t row_chunks = it.row_bytes >> 4;
     const uint64_t total = row_chunks * it.rows;
     const uint64_t pitch = it.src_pitch ? it.src_pitch : it.row_bytes;
+    const uint64_t dpitch = it.dst_pitch ? it.dst_pitch : it.row_bytes;
     const uint8_t* src = static_cast<const uint8_t*>(it.src);
     uint8_t* out = dst + it.dst_off;
     uint64_t c = tid;
@@ -72,14 +73,14 @@ __global__ void __launch_bounds__(256) pack_kernel(GatherArgs args, uint8_t* __r
         uint64_t cc = c + u * nthr;
         uint64_t r = cc / row_chunks, k = cc - r * row_chunks;
         v[u] = ld_stream(src + r * pitch + (k << 4));
-        dofs[u] = cc << 4;
+        dofs[u] = r * dpitch + (k << 4);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) st_stream(out + dofs[u], v[u]);
     }
     for (; c < total; c += nthr) {
       uint64_t r = c / row_chunks, k = c - r * row_chunks;
-      st_stream(out + (c << 4), ld_stream(src + r * pitch + (k << 4)));
+      st_stream(out + r * dpitch + (k << 4), ld_stream(src + r * pitch + (k << 4)));
     }
   }
 }
@@ -171,7 +172,8 @@ int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream) {
   for (int i = 0; i < n; ++i) {
     const ppo_gather_item& it = items[i];
     const uint64_t pitch = it.src_pitch ? it.src_pitch : it.row_bytes;
-    if (!it.src || !aligned16(it.src) || (it.dst_off & 15) || (it.row_bytes & 15) || (pitch & 15))
+    if (!it.src || !aligned16(it.src) || (it.dst_off & 15) || (it.row_bytes & 15) || (pitch & 15) ||
+        (it.dst_pitch & 15))
       return set_error(PPO_EINVAL, "ppo_pack: item %d not 16-byte aligned", i);
     args.item[i] = it;
     chunks += (it.row_bytes >> 4) * it.rows;

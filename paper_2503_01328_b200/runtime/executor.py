@@ -176,7 +176,7 @@ class RankRunner:
 
     def __init__(self, program: Program, cfg: ModelConfig, sched: Schedule, microbatches: int, device,
                  transport=None, emulate: bool = False, params=None, seed: int = 1234, optimizer: str = "sgd",
-                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True):
+                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "best"):
         torch_ = native.require_cuda()
         self.torch = torch_
         self.prog, self.cfg, self.sched, self.m = program, cfg, sched, microbatches
@@ -188,7 +188,7 @@ class RankRunner:
         with torch.cuda.device(self.device):
             self.stages = {
                 s: Stage(cfg, s, sched.num_stages, microbatches, self.device, params=params,
-                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed)
+                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm)
                 for s in my_stages
             }
             self.slab_bytes = max(st.layout.slab_bytes for st in self.stages.values())
@@ -580,7 +580,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
-            use_graphs: bool = True) -> RunResult:
+            use_graphs: bool = True, gemm: str = "best") -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
@@ -604,7 +604,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         transport = NcclTransport(ranks[0], dist.get_world_size(), dev.index, pipeline_edges(sched))
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
-                          use_graphs=use_graphs) for r in ranks]
+                          use_graphs=use_graphs, gemm=gemm) for r in ranks]
     if tokens is None:
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)

@@ -9,9 +9,13 @@ LayerNorm, GeLU and both dropout masks (K3-K5, ``libppo_b200.so``) and never
 needs anything that was not saved -- the recompute scheme of PAPER.md:439 that
 turns the reference's 34bsh coefficient into 20bsh (costs.py:1-7,18-20).
 
-Dense GEMMs run on cuBLAS through torch (bf16 in, fp32 accumulate; weight
-gradients accumulate in fp32), causal attention on cuDNN's fused kernel; the
-embedding and loss head (first/last stage only) use torch ops.
+Dense GEMMs run on libppo_b200's tcgen05 kernels (``gemm="tcgen05"``, default):
+fc1 fuses the GeLU into its epilogue (writes f into the slab and g for fc2), the
+fc2 activation-gradient GEMM fuses the GeLU backward (df = (dm @ Wfc2) * gelu'(f)),
+weight gradients accumulate in fp32 inside the GEMM epilogue.  ``gemm="cublas"``
+keeps the library GEMMs as the comparison baseline.  Causal attention runs on
+cuDNN's fused kernel; the embedding and loss head (first/last stage only) use
+torch ops.
 """
 
 from __future__ import annotations
@@ -114,8 +118,14 @@ class Stage:
     """Parameters, gradients, workspace and the F/B passes of one pipeline stage."""
 
     def __init__(self, cfg: ModelConfig, stage: int, num_stages: int, microbatches: int, device, params=None,
-                 layers: list[int] | None = None, seed: int = 1234):
+                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "best"):
         native.require_cuda()
+        if gemm not in ("best", "tcgen05", "cublas"):
+            raise ValueError(f"gemm backend {gemm!r}")
+        # "tcgen05": every GEMM on libppo_b200's kernels (fused GeLU epilogues); "cublas": the
+        # library baseline; "best": ours except narrow-N / deep-K shapes (N <= 2048, K >= 3N)
+        # where cuBLAS nvjet measured ~7% faster (profiles/r1_gemm_tuning.txt).
+        self.gemm = gemm
         self.cfg, self.stage, self.num_stages, self.m = cfg, stage, num_stages, microbatches
         self.first, self.last = stage == 0, stage == num_stages - 1
         self.layers = layers if layers is not None else stage_layers(cfg, num_stages, stage)
@@ -142,7 +152,9 @@ class Stage:
             "ln": torch.empty(s, h, **bf), "a": torch.empty(s, h, **bf), "g": torch.empty(s, 4 * h, **bf),
             "big": torch.empty(s, 4 * h, **bf), "dm": torch.empty(s, h, **bf), "dh1": torch.empty(s, h, **bf),
             "da": torch.empty(s, h, **bf), "t": torch.empty(s, h, **bf), "dy": torch.empty(s, h, **bf),
+            "dqkv": torch.empty(s, 3 * h, **bf),
         }
+        self.zero_bias = torch.zeros(4 * h, device=self.device, dtype=torch.float32)
         self.loss_sum = torch.zeros((), device=self.device, dtype=torch.float32)
         # Per-pass context in device memory, so a captured pass (CUDA graph) serves every
         # microbatch: ctx[0] = Philox offset base of (iteration, mb); tok = token row.
@@ -167,6 +179,62 @@ class Stage:
 
     def gp(self, l: int, k: str) -> torch.Tensor:
         return self.g[f"l{l}.{k}"]
+
+    # ------------------------------------------------------------------ GEMMs
+    def _ours(self, n: int, k: int) -> bool:
+        if self.gemm == "best":
+            return not (n <= 2048 and k >= 3 * n)
+        return self.gemm == "tcgen05"
+
+    def mm_fwd(self, a, w, out):
+        """out = a @ w^T (nn.Linear forward; w is [out, in])."""
+        if self._ours(w.shape[0], w.shape[1]):
+            native.gemm_tn(a, w, out)
+        else:
+            torch.mm(a, w.t(), out=out)
+
+    def mm_fc1_gelu(self, a, w, f_out, g_out):
+        """f = a @ w^T (saved GeLU input) and g = gelu(f) (fc2 operand)."""
+        if self.gemm != "cublas":
+            native.gemm_tn_gelu(a, w, g_out, f_out, self.zero_bias[: w.shape[0]])
+        else:
+            torch.mm(a, w.t(), out=f_out)
+            self._k("gelu_fwd", 4 * f_out.numel(), native.gelu_fwd, f_out, g_out)
+
+    def mm_dgrad(self, dy, w, out):
+        """out = dy @ w (activation gradient of nn.Linear)."""
+        if self._ours(w.shape[1], w.shape[0]):
+            native.gemm_nn(dy, w, out)
+        else:
+            torch.mm(dy, w, out=out)
+
+    def mm_dgrad_dgelu(self, dm, w, f, df_out, g_out):
+        """df = (dm @ w) * gelu'(f); g = gelu(f) recomputed for the fc2 weight gradient
+        (g_out None: skip, the W pass recomputes it)."""
+        if self.gemm != "cublas":
+            native.gemm_nn_dgelu(dm, w, f, df_out)
+            if g_out is not None:
+                self._k("gelu_fwd", 4 * f.numel(), native.gelu_fwd, f, g_out)
+        else:
+            torch.mm(dm, w, out=df_out)
+            self._k("gelu_bwd", 8 * f.numel(), native.gelu_bwd, f, df_out, g_out, df_out)
+
+    def wgrad(self, acc, dy, x):
+        """acc (fp32, [out, in]) += dy^T @ x with dy [tokens, out], x [tokens, in]."""
+        if self.gemm != "cublas":
+            native.gemm_wgrad(dy, x, acc, 1.0)
+        else:
+            _wgrad(acc, dy.t(), x)
+
+    def _gather_dqkv(self, dq, dk, dv, out):
+        """Concatenate the attention input gradients into out [s, 3h] (one K1 launch)."""
+        s, h = self.cfg.seq, self.cfg.hidden
+        parts = [t.transpose(1, 2) for t in (dq, dk, dv)]
+        if all(p_.is_contiguous() for p_ in parts):
+            native.pack([(p_, 2 * h * j, s, 2 * h, 2 * h, 6 * h) for j, p_ in enumerate(parts)], out)
+        else:  # pragma: no cover - cuDNN layout other than [b, s, heads, d]
+            for j, p_ in enumerate(parts):
+                out[:, j * h:(j + 1) * h].copy_(p_.reshape(s, h))
 
     def _qkv_views(self, qkv: torch.Tensor):
         cfg = self.cfg
@@ -220,7 +288,7 @@ class Stage:
         for i, l in enumerate(self.layers):
             off_a, off_m = self._offsets(l)
             x, qkv, h1, f = slab.get(i, "x"), slab.get(i, "qkv"), slab.get(i, "h1"), slab.get(i, "f")
-            torch.mm(ws["ln"], self.p(l, "w_qkv").t(), out=qkv)
+            self.mm_fwd(ws["ln"], self.p(l, "w_qkv"), qkv)
             q, k, v = self._qkv_views(qkv)
             res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
             o_tmp, lse = res[0], res[1]
@@ -230,12 +298,11 @@ class Stage:
                 self._lse_shape = tuple(lse.shape)
             self._pack_attention(slab, i, o_tmp, lse)
             o = slab.get(i, "o")
-            torch.mm(o, self.p(l, "w_proj").t(), out=ws["a"])
+            self.mm_fwd(o, self.p(l, "w_proj"), ws["a"])
             self._k("residual_dropout_ln_fwd", 8 * s * h, native.residual_dropout_ln_fwd, x, ws["a"], h1, self.p(l, "ln2_g"),
                     self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps, offset_base=self.ctx)
-            torch.mm(ws["ln"], self.p(l, "w_fc1").t(), out=f)
-            self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])
-            torch.mm(ws["g"], self.p(l, "w_fc2").t(), out=ws["a"])
+            self.mm_fc1_gelu(ws["ln"], self.p(l, "w_fc1"), f, ws["g"])
+            self.mm_fwd(ws["g"], self.p(l, "w_fc2"), ws["a"])
             if i + 1 < n_local:
                 nxt = self.layers[i + 1]
                 native.residual_dropout_ln_fwd(h1, ws["a"], slab.get(i + 1, "x"), self.p(nxt, "ln1_g"),
@@ -281,11 +348,11 @@ class Stage:
 
     def new_wbuffer(self) -> dict:
         """Gradient tensors a deferred W pass needs (split backward, GIS/PO schedules):
-        per local layer dm [s,h], df [s,4h], da [s,h] and dq/dk/dv [3,s,h] (18bsh bytes)."""
+        per local layer dm [s,h], df [s,4h], da [s,h] and dqkv [s,3h] (18bsh bytes)."""
         s, h = self.cfg.seq, self.cfg.hidden
         bf = dict(device=self.device, dtype=torch.bfloat16)
         return {i: {"dm": torch.empty(s, h, **bf), "df": torch.empty(s, 4 * h, **bf), "da": torch.empty(s, h, **bf),
-                    "dqkv": torch.empty(3, s, h, **bf)} for i in range(len(self.layers))}
+                    "dqkv": torch.empty(s, 3 * h, **bf)} for i in range(len(self.layers))}
 
     def backward_body(self, slab: SlabView, dy: torch.Tensor | None = None, dx_out: torch.Tensor | None = None,
                       wbuf: dict | None = None):
@@ -312,24 +379,24 @@ class Stage:
             off_a, _ = self._offsets(l)
             x, qkv, o, lse, h1, f = (slab.get(i, n) for n in ("x", "qkv", "o", "lse", "h1", "f"))
             dm = dm_of(i)
-            dg = wbuf[i]["df"] if split else ws["big"]
+            df = wbuf[i]["df"] if split else ws["big"]
             da = wbuf[i]["da"] if split else ws["da"]
-            # MLP: dg = dm @ Wfc2; df = dg * gelu'(f) (in place); g = gelu(f) recomputed for dWfc2
-            torch.mm(dm, self.p(l, "w_fc2"), out=dg)
-            self._k("gelu_bwd", 32 * s * h, native.gelu_bwd, f, dg, None if split else ws["g"], dg)
+            dqkv = wbuf[i]["dqkv"] if split else ws["dqkv"]
+            # MLP: df = (dm @ Wfc2) * gelu'(f) in the GEMM epilogue; g = gelu(f) recomputed for dWfc2
+            self.mm_dgrad_dgelu(dm, self.p(l, "w_fc2"), f, df, None if split else ws["g"])
             if not split:
-                _wgrad(self.gp(l, "w_fc2"), dm.t(), ws["g"])
+                self.wgrad(self.gp(l, "w_fc2"), dm, ws["g"])
                 self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
-                _wgrad(self.gp(l, "w_fc1"), dg.t(), ws["ln"])
-            torch.mm(dg, self.p(l, "w_fc1"), out=ws["t"])
+                self.wgrad(self.gp(l, "w_fc1"), df, ws["ln"])
+            self.mm_dgrad(df, self.p(l, "w_fc1"), ws["t"])
             # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay)
             self._k("layernorm_bwd", 10 * s * h, native.layernorm_bwd, h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"],
                     self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=da, p=p, drop_seed=seed, drop_offset=off_a, eps=eps,
                     offset_base=self.ctx)
             # attention projection and core
             if not split:
-                _wgrad(self.gp(l, "w_proj"), da.t(), o)
-            torch.mm(da, self.p(l, "w_proj"), out=ws["t"])
+                self.wgrad(self.gp(l, "w_proj"), da, o)
+            self.mm_dgrad(da, self.p(l, "w_proj"), ws["t"])
             q, k, v = self._qkv_views(qkv)
             o4 = o.view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
             do4 = ws["t"].view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
@@ -337,18 +404,11 @@ class Stage:
             cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
             dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
                 do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
-            w_qkv, g_qkv = self.p(l, "w_qkv"), self.gp(l, "w_qkv")
-            grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
-            if split:
-                for j, gj in enumerate(grads):
-                    wbuf[i]["dqkv"][j].copy_(gj)
-            else:
+            self._gather_dqkv(dq, dk, dv, dqkv)
+            if not split:
                 self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
-                for j, gj in enumerate(grads):
-                    _wgrad(g_qkv[j * h:(j + 1) * h], gj.t(), ws["ln"])
-            torch.mm(grads[0], w_qkv[0:h], out=ws["t"])
-            torch.addmm(ws["t"], grads[1], w_qkv[h:2 * h], out=ws["t"])
-            torch.addmm(ws["t"], grads[2], w_qkv[2 * h:3 * h], out=ws["t"])
+                self.wgrad(self.gp(l, "w_qkv"), dqkv, ws["ln"])
+            self.mm_dgrad(dqkv, self.p(l, "w_qkv"), ws["t"])
             # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay
             below = i > 0
             dx_target = ws["dy"] if (below or self.first or dx_out is None) else dx_out
@@ -371,14 +431,12 @@ class Stage:
             x, o, h1, f = (slab.get(i, n) for n in ("x", "o", "h1", "f"))
             b = wbuf[i]
             self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])  # GeLU recompute
-            _wgrad(self.gp(l, "w_fc2"), b["dm"].t(), ws["g"])
+            self.wgrad(self.gp(l, "w_fc2"), b["dm"], ws["g"])
             self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)
-            _wgrad(self.gp(l, "w_fc1"), b["df"].t(), ws["ln"])
-            _wgrad(self.gp(l, "w_proj"), b["da"].t(), o)
+            self.wgrad(self.gp(l, "w_fc1"), b["df"], ws["ln"])
+            self.wgrad(self.gp(l, "w_proj"), b["da"], o)
             self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)
-            g_qkv = self.gp(l, "w_qkv")
-            for j in range(3):
-                _wgrad(g_qkv[j * h:(j + 1) * h], b["dqkv"][j].t(), ws["ln"])
+            self.wgrad(self.gp(l, "w_qkv"), b["dqkv"], ws["ln"])
 
     # -------------------------------------------------------------- optimizer
     def sgd_step(self, lr: float = 1e-4):

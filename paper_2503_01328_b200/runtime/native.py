@@ -43,6 +43,7 @@ class GatherItem(ctypes.Structure):
         ("rows", ctypes.c_uint64),
         ("row_bytes", ctypes.c_uint64),
         ("src_pitch", ctypes.c_uint64),
+        ("dst_pitch", ctypes.c_uint64),
     ]
 
 
@@ -72,6 +73,11 @@ SIGNATURES = {
     "ppo_gelu_fwd": [_VP, _VP, _I64, _VP],
     "ppo_gelu_bwd": [_VP, _VP, _VP, _VP, _I64, _VP],
     "ppo_colsum": [_VP, _VP, _I64, _I64, _VP],
+    "ppo_gemm_tn": [_VP, _VP, _VP, _I64, _I64, _I64, _VP],
+    "ppo_gemm_tn_gelu": [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
+    "ppo_gemm_nn": [_VP, _VP, _VP, _I64, _I64, _I64, _VP],
+    "ppo_gemm_nn_dgelu": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
+    "ppo_gemm_wgrad": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
     "ppo_comm_init": [ctypes.POINTER(ctypes.c_uint8), _I32, _I32, _I32, ctypes.POINTER(_VP)],
     "ppo_comm_destroy": [_VP],
@@ -103,7 +109,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 2:
+        if lib.ppo_abi_version() != 3:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -201,16 +207,74 @@ def gelu_bwd(f, dg, g, df, stream=None):
     call("ppo_gelu_bwd", _ptr(f), _ptr(dg), _ptr(g), _ptr(df), f.numel(), _stream(stream))
 
 
+def gemm_tn(a, b, d, stream=None):
+    """d[M,N] = a[M,K] @ b[N,K]^T on tcgen05 (bf16 in/out, fp32 accumulation in TMEM)."""
+    _check_bf16(a, b, d)
+    M, K = a.shape
+    N = b.shape[0]
+    if b.shape[1] != K or tuple(d.shape) != (M, N):
+        raise ValueError(f"gemm_tn shapes: a {tuple(a.shape)} b {tuple(b.shape)} d {tuple(d.shape)}")
+    call("ppo_gemm_tn", _ptr(a), _ptr(b), _ptr(d), M, N, K, _stream(stream))
+
+
+def gemm_tn_gelu(a, b, g, f, zero_bias, stream=None):
+    """f = a @ b^T (pre-activation, bf16) and g = gelu_tanh(f) from one tcgen05 GEMM."""
+    _check_bf16(a, b, g, f)
+    M, K = a.shape
+    N = b.shape[0]
+    if b.shape[1] != K or tuple(g.shape) != (M, N) or tuple(f.shape) != (M, N) or zero_bias.numel() != N:
+        raise ValueError("gemm_tn_gelu shapes")
+    call("ppo_gemm_tn_gelu", _ptr(a), _ptr(b), _ptr(g), _ptr(f), _ptr(zero_bias), M, N, K, _stream(stream))
+
+
+def gemm_nn(a, b, d, stream=None):
+    """d[M,N] = a[M,K] @ b[K,N] on tcgen05 (activation gradients: dX = dY @ W)."""
+    _check_bf16(a, b, d)
+    M, K = a.shape
+    N = b.shape[1]
+    if b.shape[0] != K or tuple(d.shape) != (M, N):
+        raise ValueError(f"gemm_nn shapes: a {tuple(a.shape)} b {tuple(b.shape)} d {tuple(d.shape)}")
+    call("ppo_gemm_nn", _ptr(a), _ptr(b), _ptr(d), M, N, K, _stream(stream))
+
+
+def gemm_nn_dgelu(a, b, z, d, stream=None):
+    """d = (a @ b) * gelu_tanh'(z): fc2 dgrad fused with the GeLU backward."""
+    _check_bf16(a, b, z, d)
+    M, K = a.shape
+    N = b.shape[1]
+    if b.shape[0] != K or tuple(d.shape) != (M, N) or tuple(z.shape) != (M, N):
+        raise ValueError("gemm_nn_dgelu shapes")
+    call("ppo_gemm_nn_dgelu", _ptr(a), _ptr(b), _ptr(z), _ptr(d), M, N, K, _stream(stream))
+
+
+def gemm_wgrad(dy, x, dw, beta=1.0, stream=None):
+    """dw[M,N] (fp32) = beta * dw + dy[K,M]^T @ x[K,N] on tcgen05 (K = tokens)."""
+    _check_bf16(dy, x)
+    K, M = dy.shape
+    N = x.shape[1]
+    if x.shape[0] != K or tuple(dw.shape) != (M, N) or dw.dtype != _torch().float32 or not dw.is_contiguous():
+        raise ValueError(f"gemm_wgrad shapes: dy {tuple(dy.shape)} x {tuple(x.shape)} dw {tuple(dw.shape)}")
+    call("ppo_gemm_wgrad", _ptr(dy), _ptr(x), _ptr(dw), M, N, K, beta, _stream(stream))
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
 def colsum(x, acc, stream=None):
     _check_bf16(x)
     call("ppo_colsum", _ptr(x), _ptr(acc), x.numel() // x.shape[-1], x.shape[-1], _stream(stream))
 
 
 def pack(items, dst, stream=None):
-    """items: list of (src_tensor_or_ptr, dst_offset, rows, row_bytes, src_pitch)."""
+    """items: list of (src_tensor_or_ptr, dst_offset, rows, row_bytes, src_pitch[, dst_pitch])."""
     arr = (GatherItem * len(items))()
-    for i, (src, off, rows, row_bytes, pitch) in enumerate(items):
-        arr[i] = GatherItem(src if isinstance(src, int) else src.data_ptr(), off, rows, row_bytes, pitch)
+    for i, it in enumerate(items):
+        src, off, rows, row_bytes, pitch = it[:5]
+        dpitch = it[5] if len(it) > 5 else 0
+        arr[i] = GatherItem(src if isinstance(src, int) else src.data_ptr(), off, rows, row_bytes, pitch, dpitch)
     call("ppo_pack", arr, len(items), dst if isinstance(dst, int) else dst.data_ptr(), _stream(stream))
 
 

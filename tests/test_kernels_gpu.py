@@ -148,3 +148,39 @@ def test_offload_reload_round_trip_bit_exact():
     assert torch.equal(src, back)
     assert lay.payload_bytes == 2 * 20 * 512 * 256
     pool.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 768, 256), (4096, 2048, 2048), (256, 1024, 512)])
+def test_tcgen05_gemms_match_fp32(M, N, K):
+    """K6: the tcgen05 GEMMs (TN fwd, NN dgrad, fp32-accumulating wgrad, fused GeLU /
+    dGeLU epilogues) against fp32 references; bf16 outputs -> rel. L2 < 5e-3 (1e-2 with
+    the SFU tanh of the fused activations)."""
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    a = (torch.randn(M, K, generator=g) * 0.5).to(DEV).bfloat16()
+    w = (torch.randn(N, K, generator=g) * 0.05).to(DEV).bfloat16()
+
+    def rel(x, y):
+        return float((x.float() - y).norm() / y.norm())
+
+    d = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    native.gemm_tn(a, w, d)
+    want = a.float() @ w.float().t()
+    assert rel(d, want) < 5e-3
+    f, gg = torch.empty_like(d), torch.empty_like(d)
+    native.gemm_tn_gelu(a, w, gg, f, torch.zeros(N, device=DEV))
+    assert rel(f, want) < 5e-3
+    assert rel(gg, torch.from_numpy(ref.gelu(want.cpu().numpy())).to(DEV)) < 1e-2
+    # NN: d2[M,K] = d[M,N] @ w[N,K]
+    d2 = torch.empty(M, K, device=DEV, dtype=torch.bfloat16)
+    native.gemm_nn(d, w, d2)
+    assert rel(d2, d.float() @ w.float()) < 5e-3
+    # fused dGeLU: (d @ w) * gelu'(z)
+    z = torch.randn(M, K, generator=g).to(DEV).bfloat16()
+    native.gemm_nn_dgelu(d, w, z, d2)
+    dz = torch.from_numpy(ref.gelu_grad(z.float().cpu().numpy())).to(DEV)
+    assert rel(d2, (d.float() @ w.float()) * dz) < 1e-2
+    # wgrad: acc[N,K] += d[M,N]^T @ a[M,K] (fp32 accumulation, beta = 1)
+    acc = torch.randn(N, K, device=DEV)
+    want = acc + d.float().t() @ a.float()
+    native.gemm_wgrad(d, a, acc, 1.0)
+    assert rel(acc, want) < 1e-4
