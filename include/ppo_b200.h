@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 3
+#define PPO_ABI_VERSION 4
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -163,8 +163,9 @@ int ppo_gemm_tn(const void* A, const void* B, void* D, int64_t M, int64_t N, int
  * device fp32 vector of N zeros (the epilogue's per-column bias operand). */
 int ppo_gemm_tn_gelu(const void* A, const void* B, void* G, void* F, const float* zero_bias, int64_t M,
                      int64_t N, int64_t K, void* stream);
-/* Activation gradient: D[M,N] = A[M,K] . B[K,N]  (dX = dY . W with W = [out, in]). */
-int ppo_gemm_nn(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, void* stream);
+/* Activation gradient: D[M,N] = A[M,K] . B[K,N] + beta * D  (dX = dY . W with W = [out, in];
+ * beta = 1 accumulates the q/k/v contributions of dX without concatenating them). */
+int ppo_gemm_nn(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, float beta, void* stream);
 /* fc2 dgrad fused with the GeLU backward: D = (A . B) * gelu_tanh'(Z), Z = saved fc1 output. */
 int ppo_gemm_nn_dgelu(const void* A, const void* B, const void* Z, void* D, int64_t M, int64_t N, int64_t K,
                       void* stream);

@@ -9,7 +9,8 @@ LayerNorm, GeLU and both dropout masks (K3-K5, ``libppo_b200.so``) and never
 needs anything that was not saved -- the recompute scheme of PAPER.md:439 that
 turns the reference's 34bsh coefficient into 20bsh (costs.py:1-7,18-20).
 
-Dense GEMMs run on libppo_b200's tcgen05 kernels (``gemm="tcgen05"``, default):
+Dense GEMMs run on libppo_b200's tcgen05 kernels (``gemm="best"``, the default, uses
+them for every shape where they match or beat cuBLAS -- see profiles/r1_gemm_tuning.txt):
 fc1 fuses the GeLU into its epilogue (writes f into the slab and g for fc2), the
 fc2 activation-gradient GEMM fuses the GeLU backward (df = (dm @ Wfc2) * gelu'(f)),
 weight gradients accumulate in fp32 inside the GEMM epilogue.  ``gemm="cublas"``
@@ -201,23 +202,27 @@ class Stage:
             torch.mm(a, w.t(), out=f_out)
             self._k("gelu_fwd", 4 * f_out.numel(), native.gelu_fwd, f_out, g_out)
 
-    def mm_dgrad(self, dy, w, out):
-        """out = dy @ w (activation gradient of nn.Linear)."""
+    def mm_dgrad(self, dy, w, out, accumulate: bool = False):
+        """out (+)= dy @ w (activation gradient of nn.Linear)."""
         if self._ours(w.shape[1], w.shape[0]):
-            native.gemm_nn(dy, w, out)
+            native.gemm_nn(dy, w, out, 1.0 if accumulate else 0.0)
+        elif accumulate:
+            torch.addmm(out, dy, w, out=out)
         else:
             torch.mm(dy, w, out=out)
 
     def mm_dgrad_dgelu(self, dm, w, f, df_out, g_out):
-        """df = (dm @ w) * gelu'(f); g = gelu(f) recomputed for the fc2 weight gradient
-        (g_out None: skip, the W pass recomputes it)."""
-        if self.gemm != "cublas":
+        """df = (dm @ w) * gelu'(f), plus g = gelu(f) for the fc2 weight gradient.
+
+        When g is needed (unsplit backward) the plain dgrad GEMM + one gelu_bwd pass
+        (reads f and dg once, writes df and g) is cheaper; when it is not (split
+        backward: the W pass recomputes g) the GeLU backward rides in the GEMM
+        epilogue (``gemm_nn_dgelu``)."""
+        if g_out is None and self.gemm != "cublas":
             native.gemm_nn_dgelu(dm, w, f, df_out)
-            if g_out is not None:
-                self._k("gelu_fwd", 4 * f.numel(), native.gelu_fwd, f, g_out)
-        else:
-            torch.mm(dm, w, out=df_out)
-            self._k("gelu_bwd", 8 * f.numel(), native.gelu_bwd, f, df_out, g_out, df_out)
+            return
+        self.mm_dgrad(dm, w, df_out)
+        self._k("gelu_bwd", 8 * f.numel(), native.gelu_bwd, f, df_out, g_out, df_out)
 
     def wgrad(self, acc, dy, x):
         """acc (fp32, [out, in]) += dy^T @ x with dy [tokens, out], x [tokens, in]."""
@@ -404,11 +409,16 @@ class Stage:
             cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
             dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
                 do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
-            self._gather_dqkv(dq, dk, dv, dqkv)
-            if not split:
+            if split:
+                self._gather_dqkv(dq, dk, dv, dqkv)  # the W pass needs them after cuDNN's buffers are reused
+                self.mm_dgrad(dqkv, self.p(l, "w_qkv"), ws["t"])
+            else:
+                grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
                 self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
-                self.wgrad(self.gp(l, "w_qkv"), dqkv, ws["ln"])
-            self.mm_dgrad(dqkv, self.p(l, "w_qkv"), ws["t"])
+                w_qkv, g_qkv = self.p(l, "w_qkv"), self.gp(l, "w_qkv")
+                for j, gj in enumerate(grads):
+                    self.wgrad(g_qkv[j * h:(j + 1) * h], gj, ws["ln"])
+                    self.mm_dgrad(gj, w_qkv[j * h:(j + 1) * h], ws["t"], accumulate=j > 0)
             # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay
             below = i > 0
             dx_target = ws["dy"] if (below or self.first or dx_out is None) else dx_out

@@ -75,7 +75,7 @@ SIGNATURES = {
     "ppo_colsum": [_VP, _VP, _I64, _I64, _VP],
     "ppo_gemm_tn": [_VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_tn_gelu": [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
-    "ppo_gemm_nn": [_VP, _VP, _VP, _I64, _I64, _I64, _VP],
+    "ppo_gemm_nn": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_gemm_nn_dgelu": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_wgrad": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
@@ -109,7 +109,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 3:
+        if lib.ppo_abi_version() != 4:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -227,14 +227,14 @@ def gemm_tn_gelu(a, b, g, f, zero_bias, stream=None):
     call("ppo_gemm_tn_gelu", _ptr(a), _ptr(b), _ptr(g), _ptr(f), _ptr(zero_bias), M, N, K, _stream(stream))
 
 
-def gemm_nn(a, b, d, stream=None):
-    """d[M,N] = a[M,K] @ b[K,N] on tcgen05 (activation gradients: dX = dY @ W)."""
+def gemm_nn(a, b, d, beta=0.0, stream=None):
+    """d[M,N] = a[M,K] @ b[K,N] + beta * d on tcgen05 (activation gradients: dX = dY @ W)."""
     _check_bf16(a, b, d)
     M, K = a.shape
     N = b.shape[1]
     if b.shape[0] != K or tuple(d.shape) != (M, N):
         raise ValueError(f"gemm_nn shapes: a {tuple(a.shape)} b {tuple(b.shape)} d {tuple(d.shape)}")
-    call("ppo_gemm_nn", _ptr(a), _ptr(b), _ptr(d), M, N, K, _stream(stream))
+    call("ppo_gemm_nn", _ptr(a), _ptr(b), _ptr(d), M, N, K, beta, _stream(stream))
 
 
 def gemm_nn_dgelu(a, b, z, d, stream=None):

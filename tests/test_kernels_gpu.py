@@ -173,6 +173,9 @@ def test_tcgen05_gemms_match_fp32(M, N, K):
     # NN: d2[M,K] = d[M,N] @ w[N,K]
     d2 = torch.empty(M, K, device=DEV, dtype=torch.bfloat16)
     native.gemm_nn(d, w, d2)
+    d3 = d2.clone()
+    native.gemm_nn(d, w, d3, 1.0)
+    assert rel(d3, 2 * (d.float() @ w.float())) < 5e-3
     assert rel(d2, d.float() @ w.float()) < 5e-3
     # fused dGeLU: (d @ w) * gelu'(z)
     z = torch.randn(M, K, generator=g).to(DEV).bfloat16()
