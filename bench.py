@@ -111,6 +111,20 @@ def measured_peaks():
         return 6650.0, "fallback", {}
 
 
+def workload_config(config: str, world: int) -> dict:
+    """The `config` object both arms print (same workload, same metric)."""
+    L, h, heads, s, vocab, pp, m = CONFIGS[config]
+    layers = L // pp
+    d = pp if world == 1 else world
+    return {
+        "workload": (f"{config.upper()} rank-0 program of PP={d} 1F1B, m={m}, full offload (emulated boundary)"
+                     if world == 1 else f"PP={world} 1F1B pipeline, {layers} layers/stage, m={m}, full offload"),
+        "model": f"GPT shape h={h} heads={heads} s={s} vocab={vocab}, {layers} layers/stage",
+        "global_batch": m, "seq_len": s, "parallelism": f"pp{d}" + ("-rank0" if world == 1 else ""),
+        "l2": "inputs larger than L2 (the saved set of one microbatch exceeds 126 MB)",
+    }
+
+
 # ----------------------------------------------------------------------- reference arm
 
 
@@ -134,7 +148,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * s / tps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} rank-0 stage ({layers} layers h={h} s={s}), one microbatch F+B per step"},
+        "config": dict(workload_config(args.config, world),
+                       reference_step=f"one microbatch F+B of the {layers}-layer stage on the host cores (bounded sample)"),
         "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": vals[0]["sample"]},
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -393,12 +408,19 @@ def run_b200(args, rank, world, local_rank):
     kname = max(kstats, key=lambda k: kstats[k]["avg_us"] * per_step[k])
     pk = kstats[kname]
     achieved = pk["bytes_per_launch"] / (pk["avg_us"] / 1e6) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(kname, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_kind,
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_kind,
                 "bytes_per_launch": pk["bytes_per_launch"], "avg_us": pk["avg_us"],
                 "launches_per_step": pk["launches_per_step"], "share_of_step": pk["share_of_step"],
                 "method": "CUDA-graph replay of 16 launches on rotating inputs (> L2) at the workload shape; "
-                          "CUDA events on the launching stream; traffic: see profiles/ (ncu --set full)"}
+                          "CUDA events on the launching stream; traffic: ncu --set full capture committed in "
+                          "profiles/ncu_traffic.json (per launch)"}
     link_peak = max(cal["d2h_gbs"], cal["h2d_gbs"])
 
     line = {
@@ -414,13 +436,7 @@ def run_b200(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic tokens, random-init weights (no checkpoint/dataset)",
-        "config": {
-            "workload": (f"C2 rank-0 program of PP={d} 1F1B, m={m}, full offload (emulated boundary)" if world == 1
-                         else f"PP={world} 1F1B pipeline, {layers_per_stage} layers/stage, m={m}, full offload"),
-            "model": f"GPT-1.3B shape h={h} heads={heads} s={s} vocab={vocab}, {layers_per_stage} layers/stage",
-            "global_batch": m, "seq_len": s, "parallelism": f"pp{d}" + ("-rank0" if world == 1 else ""),
-            "l2": "inputs larger than L2 (0.5 GB saved set per microbatch)",
-        },
+        "config": workload_config(args.config, world),
         "e2e": {"value": full["e2e_tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": m * (s + 1) * 8,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": launches.get("full"),
