@@ -159,86 +159,6 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------------------- B200 arm
 
 
-def calibrate(stage, torch, native, reps=3):
-    """T_F, T_B of one microbatch of the stage and the D2H/H2D time of its slab."""
-    from paper_2503_01328_b200.runtime.model import SlabView
-
-    dev = stage.device
-    slab_mem = torch.empty(stage.layout.slab_bytes, dtype=torch.uint8, device=dev)
-    slab = SlabView(stage.layout, slab_mem)
-    cfg = stage.cfg
-    tok = torch.randint(0, cfg.vocab, (cfg.seq + 1,), device=dev)
-    out = torch.empty(cfg.seq, cfg.hidden, dtype=torch.bfloat16, device=dev)
-    dy = (torch.randn(cfg.seq, cfg.hidden, device=dev) * 1e-3).bfloat16()
-    tf, tb = [], []
-    for r in range(reps + 1):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record()
-        if stage.first:
-            stage.embed(slab, tok)
-        else:
-            slab.get(0, "x").copy_(dy)
-        stage.forward(slab, 0, 0, out=None if stage.last else out, tokens=tok)
-        e[1].record()
-        stage.backward(slab, 0, 0, dy=None if stage.last else dy, dx_out=None if stage.first else out, tokens=tok)
-        e[2].record()
-        torch.cuda.synchronize()
-        if r:
-            tf.append(e[0].elapsed_time(e[1]) / 1e3)
-            tb.append(e[1].elapsed_time(e[2]) / 1e3)
-    lay = stage.layout
-    pool = native.PinnedPool(lay.host_bytes + 4096)
-    bins, acc = [], pool.carve(lay.host_bytes)
-    for b in lay.bins:
-        bins.append(acc)
-        acc += b
-    segs = lay.segments(slab_mem.data_ptr(), tuple(bins))
-    copy = torch.cuda.Stream()
-    d2h, h2d = [], []
-    for r in range(reps + 1):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record(copy)
-        native.transfer(native.PPO_D2H, segs, copy.cuda_stream)
-        e[1].record(copy)
-        native.transfer(native.PPO_H2D, segs, copy.cuda_stream)
-        e[2].record(copy)
-        torch.cuda.synchronize()
-        if r:
-            d2h.append(e[0].elapsed_time(e[1]) / 1e3)
-            h2d.append(e[1].elapsed_time(e[2]) / 1e3)
-    # one-way time while the other direction is busy too (full duplex PCIe)
-    slab2 = torch.empty_like(slab_mem)
-    pool2 = native.PinnedPool(lay.host_bytes + 4096)
-    bins2, acc2 = [], pool2.carve(lay.host_bytes)
-    for b in lay.bins:
-        bins2.append(acc2)
-        acc2 += b
-    segs2 = lay.segments(slab2.data_ptr(), tuple(bins2))
-    copy2 = torch.cuda.Stream()
-    dup = []
-    for r in range(reps + 1):
-        ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        torch.cuda.synchronize()
-        ea[0].record(copy)
-        eb[0].record(copy2)
-        native.transfer(native.PPO_D2H, segs, copy.cuda_stream)
-        native.transfer(native.PPO_H2D, segs2, copy2.cuda_stream)
-        ea[1].record(copy)
-        eb[1].record(copy2)
-        torch.cuda.synchronize()
-        if r:
-            dup.append(max(ea[0].elapsed_time(ea[1]), eb[0].elapsed_time(eb[1])) / 1e3)
-    pool2.close()
-    pool.close()
-    nbytes = sum(lay.bin_used)
-    return {
-        "t_f": min(tf), "t_b": min(tb), "t_d2h": min(d2h), "t_h2d": min(h2d), "transfer_bytes": nbytes,
-        "t_duplex": statistics.median(dup), "duplex_gbs_per_direction": nbytes / statistics.median(dup) / 1e9,
-        "d2h_gbs": nbytes / min(d2h) / 1e9, "h2d_gbs": nbytes / min(h2d) / 1e9,
-    }
-
-
 def measure_kernels(s, h, heads, dev, torch, native, launches=16, sets=4):
     """Device time per launch of each recompute / pack kernel at the workload shape.
 
@@ -328,6 +248,7 @@ def run_b200(args, rank, world, local_rank):
     from paper_2503_01328_b200.offload import plan_slots_duplex
     from paper_2503_01328_b200.policy import choose_offload
     from paper_2503_01328_b200.runtime import native
+    from paper_2503_01328_b200.runtime.calibrate import calibrate
     from paper_2503_01328_b200.runtime.executor import execute
     from paper_2503_01328_b200.runtime.model import ModelConfig, Stage
 
@@ -347,7 +268,7 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- calibration: measured T_F, T_B (per stage), T_o (D2H + H2D of one payload)
     cal_stage = Stage(cfg, min(rank, d - 1) if world > 1 else 0, d, m, dev, layers=list(range(layers_per_stage)))
-    cal = calibrate(cal_stage, torch, native)
+    cal = calibrate(cal_stage)
     del cal_stage
     torch.cuda.empty_cache()
     costs = measured_pass_costs(cal["t_f"] / layers_per_stage, cal["t_b"] / layers_per_stage, 0.0,

@@ -1,0 +1,39 @@
+"""CLI (reference flag names, cli.py:328-367): ``plan`` on CPU, ``run`` on the B200."""
+
+import json
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+
+def test_plan_writes_reference_files(tmp_path):
+    out = tmp_path / "o"
+    res = subprocess.run([sys.executable, "-m", "paper_2503_01328_b200", "plan", "--schedule", "1f1b", "--d", "4",
+                          "--m", "8", "--offload", "full", "--t-o", "1/2", "--out", str(out)],
+                         cwd=ROOT, capture_output=True, text=True, check=True)
+    summary = json.loads(res.stdout)
+    assert summary["peak_units"] == [2, 2, 2, 1]  # C1 golden: SURVEY App. A.3
+    assert summary["makespan"] == 33.0
+    text = (out / "1f1b.schedule").read_text()
+    import paper_2503_01328_b200 as po
+
+    assert po.emit_schedule(po.parse_schedule(text)) == text
+    assert (out / "1f1b.plan").read_text().startswith("# plan t_o=")
+
+
+@pytest.mark.gpu
+def test_run_virtual_pipeline(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("needs a CUDA device")
+    out = tmp_path / "r"
+    res = subprocess.run([sys.executable, "-m", "paper_2503_01328_b200", "run", "--schedule", "gis-h", "--d", "2",
+                          "--v", "2", "--m", "4", "--layers", "4", "--offload", "1", "--iters", "1", "--warmup", "1",
+                          "--out", str(out)], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    summary = json.loads(res.stdout.strip().splitlines()[-1])
+    assert summary["tokens_per_s"] > 0 and summary["schedule"] == "gis-h"
+    assert (out / "gis-h-trace.csv").read_text().startswith("device,stage,microbatch,kind")

@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+from paper_2503_01328_b200.runtime.calibrate import calibrate  # noqa: E402
 from paper_2503_01328_b200 import (build_interleaved_1f1b, measured_pass_costs, plan_slots, po_block,  # noqa: E402
                                    select_offload_stages, simulate, peak_memory)
 from paper_2503_01328_b200.policy import choose_offload  # noqa: E402
@@ -43,7 +43,7 @@ def main():
     per_chunk = a.layers // (a.d * a.v)
     cfg = ModelConfig(n_layers=a.layers, hidden=a.h, heads=a.h // 128, seq=a.s, vocab=1024)
     st = Stage(cfg, 1, a.d * a.v, a.m, dev, layers=list(range(per_chunk)))
-    cal = bench.calibrate(st, torch, native)
+    cal = calibrate(st)
     del st
     torch.cuda.empty_cache()
     costs = measured_pass_costs(cal["t_f"], cal["t_b"], 0.0, (2 * a.s * a.h) / 770e9 + 10e-6)

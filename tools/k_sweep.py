@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+from paper_2503_01328_b200.runtime.calibrate import calibrate  # noqa: E402
 from paper_2503_01328_b200 import build_1f1b, measured_pass_costs, plan_slots  # noqa: E402
 from paper_2503_01328_b200.policy import choose_offload  # noqa: E402
 from paper_2503_01328_b200.runtime import native  # noqa: E402
@@ -32,7 +32,7 @@ def run_point(h, s, m, d, iters, warmup, dev):
     heads = h // 128
     cfg = ModelConfig(n_layers=d, hidden=h, heads=heads, seq=s, vocab=1024)
     st = Stage(cfg, 1, d, m, dev, layers=[0])  # a middle stage: no embedding / head
-    cal = bench.calibrate(st, torch, native)
+    cal = calibrate(st)
     del st
     torch.cuda.empty_cache()
     costs = measured_pass_costs(cal["t_f"], cal["t_b"], 0.0, (2 * s * h) / 770e9 + 10e-6)
