@@ -111,6 +111,15 @@ def measured_peaks():
         return 6650.0, "fallback", {}
 
 
+def measured_tflops():
+    """Dense bf16 peak for a GEMM timed alone: the burst figure (B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["bf16_tflops"], "measured"
+    except Exception:
+        return 2250.0, "fallback (nominal dense bf16)"
+
+
 def workload_config(config: str, world: int) -> dict:
     """The `config` object both arms print (same workload, same metric)."""
     L, h, heads, s, vocab, pp, m = CONFIGS[config]
@@ -122,6 +131,9 @@ def workload_config(config: str, world: int) -> dict:
         "model": f"GPT shape h={h} heads={heads} s={s} vocab={vocab}, {layers} layers/stage",
         "global_batch": m, "seq_len": s, "parallelism": f"pp{d}" + ("-rank0" if world == 1 else ""),
         "l2": "inputs larger than L2 (the saved set of one microbatch exceeds 126 MB)",
+        "units": ("value = stage-token passes per second summed over the N ranks (each rank runs every "
+                  "token of every microbatch through its stage: N*m*s per step); the pipeline's own "
+                  "tokens/s is value/N (`pipeline_tokens_per_s`)"),
     }
 
 
@@ -189,29 +201,73 @@ def measure_kernels(s, h, heads, dev, torch, native, launches=16, sets=4):
             [(t["x"], 0, 1, E, 0), (t["lse"], E, 1, 4 * heads * s, 0)], t["slab"])),
     }
     out = {}
-    stream = torch.cuda.Stream(dev)
     for name, (entry, nbytes, fn) in cases.items():
-        with torch.cuda.stream(stream):
-            for t in sets_:
-                fn(t)
+        avg = _graph_time_us([lambda t=t, fn=fn: fn(t) for t in sets_], dev, torch, launches)
+        out[name] = {"entry": entry, "bytes_per_launch": nbytes, "avg_us": avg}
+    return out
+
+
+def _graph_time_us(fn_sets, dev, torch, launches=16):
+    """Average device µs per launch: `launches` calls cycling over `fn_sets` captured
+    in one CUDA graph, replayed on its own stream, CUDA events on that stream."""
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for fn in fn_sets:
+            fn()
+    torch.cuda.synchronize(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for i in range(launches):
+            fn_sets[i % len(fn_sets)]()
+    times = []
+    with torch.cuda.stream(stream):  # replay() launches on the current stream
+        graph.replay()
         torch.cuda.synchronize(dev)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            for i in range(launches):
-                fn(sets_[i % sets])
-        times = []
-        with torch.cuda.stream(stream):  # replay() launches on the current stream
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             graph.replay()
-            torch.cuda.synchronize(dev)
-            for _ in range(3):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                graph.replay()
-                e1.record(stream)
-                e1.synchronize()
-                times.append(e0.elapsed_time(e1) * 1e3 / launches)
-        out[name] = {"entry": entry, "bytes_per_launch": nbytes, "avg_us": min(times)}
-        del graph
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e3 / launches)
+    del graph
+    return min(times)
+
+
+GEMM_NAMES = {"ppo_gemm_tn": "gemm_tn", "ppo_gemm_tn_gelu": "gemm_tn_gelu", "ppo_gemm_nn": "gemm_nn",
+              "ppo_gemm_nn_dgelu": "gemm_nn_dgelu", "ppo_gemm_wgrad": "gemm_wgrad"}
+
+
+def measure_gemms(shapes, dev, torch, native, sets=2):
+    """Device time per launch of each tcgen05 GEMM (entry, M, N, K) the step ran."""
+    bf = dict(device=dev, dtype=torch.bfloat16)
+    out = {}
+    for (entry, M, N, K) in sorted(shapes):
+        fns = []
+        for _ in range(sets):
+            if entry == "ppo_gemm_tn":
+                a, b, d = torch.randn(M, K, **bf), torch.randn(N, K, **bf), torch.empty(M, N, **bf)
+                fns.append(lambda a=a, b=b, d=d: native.gemm_tn(a, b, d))
+            elif entry == "ppo_gemm_tn_gelu":
+                a, b = torch.randn(M, K, **bf), torch.randn(N, K, **bf)
+                g, f, z = torch.empty(M, N, **bf), torch.empty(M, N, **bf), torch.zeros(N, device=dev)
+                fns.append(lambda a=a, b=b, g=g, f=f, z=z: native.gemm_tn_gelu(a, b, g, f, z))
+            elif entry == "ppo_gemm_nn":
+                a, b, d = torch.randn(M, K, **bf), torch.randn(K, N, **bf), torch.empty(M, N, **bf)
+                fns.append(lambda a=a, b=b, d=d: native.gemm_nn(a, b, d, 0.0))
+            elif entry == "ppo_gemm_nn_dgelu":
+                a, b, z, d = torch.randn(M, K, **bf), torch.randn(K, N, **bf), torch.randn(M, N, **bf), torch.empty(M, N, **bf)
+                fns.append(lambda a=a, b=b, z=z, d=d: native.gemm_nn_dgelu(a, b, z, d))
+            elif entry == "ppo_gemm_wgrad":
+                dy, x, dw = torch.randn(K, M, **bf), torch.randn(K, N, **bf), torch.zeros(M, N, device=dev)
+                fns.append(lambda dy=dy, x=x, dw=dw: native.gemm_wgrad(dy, x, dw, 1.0))
+            else:
+                continue
+        name = f"{GEMM_NAMES[entry]}_{M}x{N}x{K}"
+        out[name] = {"entry": entry, "shape": (M, N, K), "flops_per_launch": 2 * M * N * K,
+                     "avg_us": _graph_time_us(fns, dev, torch)}
+        del fns
+        torch.cuda.empty_cache()
     return out
 
 
@@ -253,22 +309,37 @@ def run_b200(args, rank, world, local_rank):
     from paper_2503_01328_b200.runtime.model import ModelConfig, Stage
 
     native.require_cuda()
+    # PPO_DIST_BACKEND=gloo: boundary over host copies, so ranks may share a GPU
+    # (the 2-process test on a 1-GPU box); the product path is NCCL, one GPU per rank.
+    backend = os.environ.get("PPO_DIST_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if world > ndev and backend == "nccl":
+        raise SystemExit(f"--gpus {world} needs {world} GPUs for NCCL, found {ndev}")
+    local_rank %= ndev
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     L, h, heads, s, vocab, pp_plan, m = CONFIGS[args.config]
     layers_per_stage = L // pp_plan
     d = pp_plan if world == 1 else world
     n_layers = layers_per_stage * d
     cfg = ModelConfig(n_layers=n_layers, hidden=h, heads=heads, seq=s, vocab=vocab)
-    mode = "emulate" if world == 1 else "nccl"
+    mode = "emulate" if world == 1 else ("nccl" if backend == "nccl" else "gloo")
 
     # ---- calibration: measured T_F, T_B (per stage), T_o (D2H + H2D of one payload)
     cal_stage = Stage(cfg, min(rank, d - 1) if world > 1 else 0, d, m, dev, layers=list(range(layers_per_stage)))
     cal = calibrate(cal_stage)
+    if dist is not None:  # every rank plans with rank 0's measurements (identical programs)
+        box = [cal]
+        dist.broadcast_object_list(box, src=0)
+        cal = box[0]
     del cal_stage
     torch.cuda.empty_cache()
     costs = measured_pass_costs(cal["t_f"] / layers_per_stage, cal["t_b"] / layers_per_stage, 0.0,
@@ -290,11 +361,12 @@ def run_b200(args, rank, world, local_rank):
         if name == "auto" and plan is None:
             results[name] = dict(results["none"], note="k-aware policy keeps everything resident at this k")
             continue
-        if name == "full":
+        if name == "full" and rank == 0:
             sampler = ClockSampler(local_rank)
             sampler.__enter__()
         before = native.kernel_launches()
         native.CALLS.clear()
+        native.SHAPES.clear()
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
                       stream_mode="single" if name in ("none", "none_cublas", "auto", "full_single") else "dual",
@@ -305,10 +377,17 @@ def run_b200(args, rank, world, local_rank):
         captured = sum(sum(r.graph_native_launches.values()) for r in res.runners)
         launches[name] = (native.kernel_launches() - before - captured + replayed) / (args.steps + args.warmup)
         if name == "full":
-            sampler.__exit__()
-            clocks = sampler.summary()
+            if rank == 0:
+                sampler.__exit__()
+                clocks = sampler.summary()
             calls_full = dict(native.CALLS)
+            shapes_full = dict(native.SHAPES)
         results[name] = policy_report(res, sched, plan, m, s, res.slab_bytes, rank)
+        if dist is not None:  # per-GPU peak activation of every rank
+            per_rank = [None] * world
+            dist.all_gather_object(per_rank, results[name]["peak_act_gb"])
+            results[name]["peak_act_gb_per_rank"] = per_rank
+            results[name]["peak_act_gb"] = max(per_rank)
         results[name]["_res"] = res
         for r in res.runners:
             r.close()
@@ -321,32 +400,48 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel of the hot path (HBM-bound recompute)
     hbm_peak, peak_kind, _ = measured_peaks()
+    if rank != 0:  # rank 0 alone measures the kernels and prints the line
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     kstats = measure_kernels(s, h, heads, dev, torch, native)
-    per_step = {k: calls_full.get(v["entry"], 0) / (args.steps + args.warmup) for k, v in kstats.items()}
+    nsteps = args.steps + args.warmup
+    step_us = 1e3 * full["ms_per_step"]
     for k, v in kstats.items():
-        v["launches_per_step"] = per_step[k]
-        v["share_of_step"] = v["avg_us"] * per_step[k] / (1e3 * full["ms_per_step"])
-    kname = max(kstats, key=lambda k: kstats[k]["avg_us"] * per_step[k])
-    pk = kstats[kname]
-    achieved = pk["bytes_per_launch"] / (pk["avg_us"] / 1e6) / 1e9
+        v["launches_per_step"] = calls_full.get(v["entry"], 0) / nsteps
+        v["bound"], v["achieved"] = "hbm", v["bytes_per_launch"] / v["avg_us"] / 1e3  # GB/s
+    gstats = measure_gemms([k for k in shapes_full], dev, torch, native)
+    tc_peak, tc_kind = measured_tflops()
+    for k, v in gstats.items():
+        v["launches_per_step"] = shapes_full[(v["entry"],) + tuple(v["shape"])] / nsteps
+        v["bound"], v["achieved"] = "tensor", v["flops_per_launch"] / v["avg_us"] / 1e6  # TFLOP/s
+    allk = dict(kstats, **gstats)
+    for v in allk.values():
+        v["share_of_step"] = v["avg_us"] * v["launches_per_step"] / step_us
+    # the dominant kernel of OUR code in the step: largest device time per step
+    kname = max(allk, key=lambda k: allk[k]["share_of_step"])
+    pk = allk[kname]
+    peak, unit, pkind = (hbm_peak, "GB/s", peak_kind) if pk["bound"] == "hbm" else (tc_peak, "TFLOP/s", tc_kind)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             traffic = json.load(f).get(kname, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_kind,
-                "bytes_per_launch": pk["bytes_per_launch"], "avg_us": pk["avg_us"],
+    roofline = {"kernel": kname, "bound": pk["bound"], "achieved": pk["achieved"], "peak": peak, "unit": unit,
+                "frac": pk["achieved"] / peak, "traffic": traffic, "peak_source": pkind,
+                "per_launch": pk.get("bytes_per_launch", pk.get("flops_per_launch")), "avg_us": pk["avg_us"],
                 "launches_per_step": pk["launches_per_step"], "share_of_step": pk["share_of_step"],
-                "method": "CUDA-graph replay of 16 launches on rotating inputs (> L2) at the workload shape; "
-                          "CUDA events on the launching stream; traffic: ncu --set full capture committed in "
+                "method": "CUDA-graph replay of 16 launches on rotating inputs at the workload shape; CUDA events "
+                          "on the launching stream; launches per step counted from the ABI calls the step "
+                          "executed (graph replays included); traffic: ncu --set full capture, "
                           "profiles/ncu_traffic.json (per launch)"}
     link_peak = max(cal["d2h_gbs"], cal["h2d_gbs"])
 
     line = {
         "metric": METRIC,
-        "value": full["tokens_per_s"],
+        "value": world * full["tokens_per_s"],
+        "pipeline_tokens_per_s": full["tokens_per_s"],
         "unit": "tokens/s",
         "n_gpus": world,
         "steps": args.steps,
@@ -358,15 +453,16 @@ def run_b200(args, rank, world, local_rank):
         "dtype": "bf16",
         "data": "synthetic tokens, random-init weights (no checkpoint/dataset)",
         "config": workload_config(args.config, world),
-        "e2e": {"value": full["e2e_tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": m * (s + 1) * 8,
+        "e2e": {"value": world * full["e2e_tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": m * (s + 1) * 8,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": launches.get("full"),
         "clocks": clocks,
         "roofline": roofline,
-        "kernels": {k: {"avg_us": round(v["avg_us"], 2), "gbs": round(v["bytes_per_launch"] / v["avg_us"] / 1e3, 1),
-                        "frac": round(v["bytes_per_launch"] / v["avg_us"] / 1e3 / hbm_peak, 3),
+        "kernels": {k: {"bound": v["bound"], "avg_us": round(v["avg_us"], 2), "achieved": round(v["achieved"], 1),
+                        "unit": "GB/s" if v["bound"] == "hbm" else "TFLOP/s",
+                        "frac": round(v["achieved"] / (hbm_peak if v["bound"] == "hbm" else tc_peak), 3),
                         "launches_per_step": v["launches_per_step"], "share_of_step": round(v["share_of_step"], 4)}
-                    for k, v in kstats.items()},
+                    for k, v in sorted(allk.items(), key=lambda kv: -kv[1]["share_of_step"])},
         "host_link": {"bound": "pcie", "d2h_gbs": full["d2h_gbs"], "h2d_gbs": full["h2d_gbs"],
                       "peak_gbs": link_peak, "frac": (full["d2h_gbs"] or 0) / link_peak if link_peak else None,
                       "calibration": {k: cal[k] for k in ("d2h_gbs", "h2d_gbs", "transfer_bytes")}},
@@ -384,12 +480,9 @@ def run_b200(args, rank, world, local_rank):
             "t_duplex_oneway_ms": cal["t_duplex"] * 1e3,
         },
     }
-    if rank == 0:
-        line["cpu_baseline"] = cpu_baseline(args) if not args.no_cpu_baseline else None
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
+    line["cpu_baseline"] = cpu_baseline(args) if not args.no_cpu_baseline else None
+    print(json.dumps(line), flush=True)
+    if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -10,7 +10,9 @@ reference's output files from the *measured* trace:
     <kind>.schedule        emit_schedule (planned, measured costs)
     <kind>.plan            OffloadPlan.emit
     <kind>-trace.csv       SimTrace.to_csv of the measured run (seconds)
-    <kind>-summary.json    SimTrace.summary() + tokens/s, arena GB, k
+    <kind>-summary.json    SimTrace.summary() + tokens/s, arena GB, k, predicted vs
+                           measured makespan (the runner model fed the measured costs)
+    <kind>.svg             timeline of the measured trace (render.render_svg)
 
 Modes: ``emulate`` (rank 0 of the schedule alone on one GPU, loopback boundary),
 ``virtual`` (all ranks on one GPU), and torchrun with WORLD_SIZE > 1 (one rank per
@@ -28,6 +30,7 @@ from fractions import Fraction
 from . import (BUILDERS, PassCosts, build_gis_g, emit_schedule, peak_memory, plan_slots, po_block,
                select_offload_stages, simulate)
 from .policy import choose_offload
+from .render import render_svg
 
 SCHEDULES = ("1f1b", "1f1b-i", "gis", "gis-g", "gis-h", "po")
 
@@ -81,6 +84,7 @@ def cmd_plan(args) -> int:
     sched = _build(args.schedule, args.d, args.v, args.m, args.g, costs)
     plan = _plan(sched, args.d, args.v, costs, Fraction(args.t_o) * costs.total, args.offload)
     trace = simulate(sched, plan)
+    _write(args.out, f"{sched.kind}.svg", render_svg(trace, title=f"{sched.kind} d={args.d} v={args.v} m={args.m}"))
     summary = dict(trace.summary(), schedule=sched.kind, d=args.d, v=args.v, m=args.m,
                    offloaded_stages=list(plan.stages) if plan else [],
                    skip_list=plan.skip_list() if plan else [], late_list=plan.late_list() if plan else [])
@@ -125,18 +129,22 @@ def cmd_run(args) -> int:
                   stream_mode=args.stream_mode, optimizer=args.optimizer)
     trace = res.trace
     it = max(res.iteration_seconds)
+    predicted = simulate(sched, plan, stream_mode=args.stream_mode)
     summary = dict(trace.summary(), schedule=sched.kind, mode=mode, d=args.d, v=args.v, m=args.m,
                    tokens_per_s=args.m * args.seq / it, ms_per_step=it * 1e3,
                    arena_slabs={str(k): v for k, v in res.peak_slabs.items()},
                    arena_gb={str(k): v * res.slab_bytes / 1e9 for k, v in res.peak_slabs.items()},
                    modelled_peak_units=[u for u, _ in peak_memory(simulate(sched, plan))["per_device"]],
                    k_measured=float(t_o / (costs.total * units)), calibration=cal,
+                   predicted_makespan_s=float(predicted.makespan), measured_makespan_s=float(trace.makespan),
+                   model_error_pct=100 * (float(trace.makespan) / float(predicted.makespan) - 1),
                    offloaded_stages=list(plan.stages) if plan else [], losses=res.losses)
     if rank == 0:
         _write(args.out, f"{sched.kind}.schedule", emit_schedule(sched))
         if plan:
             _write(args.out, f"{sched.kind}.plan", plan.emit())
         _write(args.out, f"{sched.kind}-trace.csv", trace.to_csv())
+        _write(args.out, f"{sched.kind}.svg", render_svg(trace, title=f"measured {sched.kind} ({mode}) d={args.d} m={args.m}"))
         _write(args.out, f"{sched.kind}-summary.json", json.dumps(summary, indent=2, default=str))
         print(json.dumps(summary, default=str))
     for r in res.runners:

@@ -103,16 +103,20 @@ class NcclTransport:
     communicator cannot form, also across the interleaved wrap d-1 -> 0.
     """
 
+    _generation = 0  # bumped per transport, in the same sequence on every rank
+
     def __init__(self, rank: int, world: int, device: int, edges):
         import torch.distributed as dist
 
         self.rank = rank
         self.comms = {}
+        NcclTransport._generation += 1
+        gen = NcclTransport._generation
         for ch in sorted(set(edges)):  # identical global order on every rank
             kind, src, dst = ch
             if rank not in (src, dst):
                 continue
-            key = f"ppo_uid/{kind}/{src}/{dst}"
+            key = f"ppo_uid/{gen}/{kind}/{src}/{dst}"
             store = _store()
             if rank == src:
                 uid = native.NcclComm.unique_id()
@@ -140,6 +144,70 @@ class NcclTransport:
         for c in self.comms.values():
             c.close()
         self.comms.clear()
+
+
+class HostTransport:
+    """Boundary over ``torch.distributed`` point-to-point on host copies (gloo).
+
+    A debugging/test transport for multi-process runs where NCCL cannot be used --
+    e.g. several ranks sharing one GPU, which NCCL refuses ("duplicate GPU").  A
+    send waits for the producing stream, copies the ring buffer to the host and
+    posts a non-blocking ``isend``; a receive blocks the issuing host thread until
+    the message is there, then copies it into the ring buffer on the receive
+    stream.  Message order per channel is the program order on both sides (the
+    same FIFO contract as the NCCL channels), so a program that runs over NCCL runs
+    here; its timings include host round trips and mean nothing.
+    """
+
+    TAGS = {"act": 11, "grad": 12}
+
+    def __init__(self, rank: int):
+        self.rank = rank
+        self.pending = []
+
+    def send(self, rank, op, buf, stream) -> bool:
+        import torch.distributed as dist
+
+        stream.synchronize()
+        host = buf.cpu()
+        self.pending.append((dist.isend(host, op.peer, tag=self.TAGS[op.kind[5:].lower()]), host))
+        return True
+
+    def recv(self, rank, op, buf, stream) -> bool:
+        import torch.distributed as dist
+
+        host = torch.empty(buf.shape, dtype=buf.dtype)
+        dist.recv(host, op.peer, tag=self.TAGS[op.kind[5:].lower()])
+        with torch.cuda.stream(stream):
+            buf.copy_(host)
+        return True
+
+    def end_iteration(self):
+        for work, _ in self.pending:
+            work.wait()
+        self.pending.clear()
+
+    def close(self):
+        self.end_iteration()
+
+
+_NCCL_TRANSPORTS = {}
+
+
+def nccl_transport(rank: int, world: int, device: int, edges) -> NcclTransport:
+    """The process's NCCL transport for this set of edges, created once and reused by
+    later ``execute`` calls (communicator set-up is collective and costs seconds)."""
+    key = (rank, world, device, tuple(sorted(set(edges))))
+    t = _NCCL_TRANSPORTS.get(key)
+    if t is None:
+        t = _NCCL_TRANSPORTS[key] = NcclTransport(rank, world, device, edges)
+    return t
+
+
+def close_transports():
+    for t in _NCCL_TRANSPORTS.values():
+        t.close()
+    _NCCL_TRANSPORTS.clear()
 
 
 def _store():
@@ -218,6 +286,7 @@ class RankRunner:
         self.wbufs = {}
         self.graph_native_launches = {}  # libppo_b200 kernels inside each captured pass
         self.replayed_native_launches = 0  # ... executed through graph replays
+        self.graph_calls = {}  # per captured pass: ABI calls (native.CALLS/SHAPES deltas) one replay runs
         self.digests = {}  # (stage, mb) -> [digest at F end, digest at B start]
         self._adam = None
         self.cursor = 0
@@ -379,10 +448,12 @@ class RankRunner:
         if graph is not None:
             graph.replay()
             self.replayed_native_launches += self.graph_native_launches[key]
+            native.credit(self.graph_calls[key])
             return
         body()
         graph = torch.cuda.CUDAGraph()
         before = native.kernel_launches()
+        snap = native.call_counts()
         graph.capture_begin(capture_error_mode="thread_local")
         try:
             body()
@@ -390,6 +461,10 @@ class RankRunner:
             graph.capture_end()
         self.graphs[key] = graph
         self.graph_native_launches[key] = native.kernel_launches() - before
+        # the capture recorded these calls without running them: native.CALLS /
+        # SHAPES count executed calls, so they move to the replays
+        self.graph_calls[key] = native.since(snap)
+        native.credit(self.graph_calls[key], -1)
 
     def _transfer(self, op, stream):
         s, j = op.stage, op.mb
@@ -562,6 +637,25 @@ def measured_trace(sched: Schedule, passes: list[Pass], model: ModelSpec | None 
     )
 
 
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def _reduce_over_ranks(sec, wall, host_issue, loss, dev):
+    """MAX of the times over ranks; the loss from the rank that holds the last stage."""
+    dist = _dist()
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([sec, wall, host_issue], dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    lv = torch.tensor([loss if loss is not None else 0.0, 1.0 if loss is not None else 0.0], dtype=torch.float64,
+                      device=on)
+    dist.all_reduce(lv, op=dist.ReduceOp.SUM)
+    sec, wall, host_issue = (float(x) for x in t.tolist())
+    return sec, wall, host_issue, (float(lv[0]) if float(lv[1]) else None)
+
+
 @dataclass
 class RunResult:
     trace: SimTrace
@@ -584,8 +678,13 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
-    boundary) or "nccl" (this process is ``rank`` of a torchrun job).
+    boundary) or "nccl" (this process is ``rank`` of a torchrun job; "gloo" is the
+    same over host copies, for ranks that share a GPU in tests).
     ``tokens``: [m, s+1] int64 host tensor (pinned for the e2e path).
+
+    In the multi-process modes every iteration starts after a device synchronise
+    and a barrier, and the returned iteration/wall times and losses are the same on
+    every rank: times are the MAX over ranks, the loss is the last stage's.
     """
     native.require_cuda()
     m = microbatches or sched.microbatches
@@ -601,7 +700,12 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     elif mode == "nccl":
         import torch.distributed as dist
 
-        transport = NcclTransport(ranks[0], dist.get_world_size(), dev.index, pipeline_edges(sched))
+        transport = nccl_transport(ranks[0], dist.get_world_size(), dev.index, pipeline_edges(sched))
+    elif mode == "gloo":
+        transport = HostTransport(ranks[0])
+    elif mode != "emulate":
+        raise ValueError(f"unknown mode {mode!r}")
+    dist_mode = mode in ("nccl", "gloo")
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
                           use_graphs=use_graphs, gemm=gemm) for r in ranks]
@@ -612,6 +716,9 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     secs, losses, walls, host_secs = [], [], [], []
     torch.cuda.synchronize(dev)
     for it in range(warmup + iters):
+        if dist_mode:
+            torch.cuda.synchronize(dev)
+            _dist().barrier()
         if it == warmup and probe_kernels:
             for r in runners:
                 for st in r.stages.values():
@@ -633,11 +740,15 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             transport.end_iteration()
         if it >= warmup:
             torch.cuda.synchronize(dev)
+            sec = max(r.iteration_seconds() for r in runners)
+            ls = [v for r, v in zip(runners, values) if r.loss_sum() is not None]
+            loss = ls[0] / m if ls else None
+            if dist_mode:
+                sec, wall, host_issue, loss = _reduce_over_ranks(sec, wall, host_issue, loss, dev)
             walls.append(wall)
             host_secs.append(host_issue)
-            secs.append(max(r.iteration_seconds() for r in runners))
-            ls = [v for r, v in zip(runners, values) if r.loss_sum() is not None]
-            losses.append(ls[0] / m if ls else None)
+            secs.append(sec)
+            losses.append(loss)
     passes = [p for r in runners for p in r.measured_passes()]
     slab_bytes = max(r.slab_bytes for r in runners)
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)

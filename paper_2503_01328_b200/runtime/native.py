@@ -122,11 +122,33 @@ def check(fn: str, rc: int) -> None:
 
 
 CALLS: collections.Counter = collections.Counter()  # ABI entry point -> calls (launch accounting)
+SHAPES: collections.Counter = collections.Counter()  # (GEMM entry point, M, N, K) -> calls
 
 
 def call(fn: str, *args) -> None:
     CALLS[fn] += 1
     check(fn, getattr(load(), fn)(*args))
+
+
+def call_counts():
+    """Snapshot of (CALLS, SHAPES), for crediting CUDA-graph replays (see credit)."""
+    return collections.Counter(CALLS), collections.Counter(SHAPES)
+
+
+def since(snap):
+    """Calls made after ``snap`` (a call_counts() result)."""
+    c, sh = snap
+    return CALLS - c, SHAPES - sh
+
+
+def credit(delta, sign: int = 1):
+    """Add (sign=1) or remove (sign=-1) a block of calls: a graph capture records
+    launches that do not execute; each replay executes them."""
+    c, sh = delta
+    for k, v in c.items():
+        CALLS[k] += sign * v
+    for k, v in sh.items():
+        SHAPES[k] += sign * v
 
 
 def kernel_launches() -> int:
@@ -214,6 +236,7 @@ def gemm_tn(a, b, d, stream=None):
     N = b.shape[0]
     if b.shape[1] != K or tuple(d.shape) != (M, N):
         raise ValueError(f"gemm_tn shapes: a {tuple(a.shape)} b {tuple(b.shape)} d {tuple(d.shape)}")
+    SHAPES[("ppo_gemm_tn", M, N, K)] += 1
     call("ppo_gemm_tn", _ptr(a), _ptr(b), _ptr(d), M, N, K, _stream(stream))
 
 
@@ -224,6 +247,7 @@ def gemm_tn_gelu(a, b, g, f, zero_bias, stream=None):
     N = b.shape[0]
     if b.shape[1] != K or tuple(g.shape) != (M, N) or tuple(f.shape) != (M, N) or zero_bias.numel() != N:
         raise ValueError("gemm_tn_gelu shapes")
+    SHAPES[("ppo_gemm_tn_gelu", M, N, K)] += 1
     call("ppo_gemm_tn_gelu", _ptr(a), _ptr(b), _ptr(g), _ptr(f), _ptr(zero_bias), M, N, K, _stream(stream))
 
 
@@ -234,6 +258,7 @@ def gemm_nn(a, b, d, beta=0.0, stream=None):
     N = b.shape[1]
     if b.shape[0] != K or tuple(d.shape) != (M, N):
         raise ValueError(f"gemm_nn shapes: a {tuple(a.shape)} b {tuple(b.shape)} d {tuple(d.shape)}")
+    SHAPES[("ppo_gemm_nn", M, N, K)] += 1
     call("ppo_gemm_nn", _ptr(a), _ptr(b), _ptr(d), M, N, K, beta, _stream(stream))
 
 
@@ -244,6 +269,7 @@ def gemm_nn_dgelu(a, b, z, d, stream=None):
     N = b.shape[1]
     if b.shape[0] != K or tuple(d.shape) != (M, N) or tuple(z.shape) != (M, N):
         raise ValueError("gemm_nn_dgelu shapes")
+    SHAPES[("ppo_gemm_nn_dgelu", M, N, K)] += 1
     call("ppo_gemm_nn_dgelu", _ptr(a), _ptr(b), _ptr(z), _ptr(d), M, N, K, _stream(stream))
 
 
@@ -254,6 +280,7 @@ def gemm_wgrad(dy, x, dw, beta=1.0, stream=None):
     N = x.shape[1]
     if x.shape[0] != K or tuple(dw.shape) != (M, N) or dw.dtype != _torch().float32 or not dw.is_contiguous():
         raise ValueError(f"gemm_wgrad shapes: dy {tuple(dy.shape)} x {tuple(x.shape)} dw {tuple(dw.shape)}")
+    SHAPES[("ppo_gemm_wgrad", M, N, K)] += 1
     call("ppo_gemm_wgrad", _ptr(dy), _ptr(x), _ptr(dw), M, N, K, beta, _stream(stream))
 
 

@@ -22,6 +22,24 @@ def test_plan_writes_reference_files(tmp_path):
 
     assert po.emit_schedule(po.parse_schedule(text)) == text
     assert (out / "1f1b.plan").read_text().startswith("# plan t_o=")
+    svg = (out / "1f1b.svg").read_text()
+    assert svg.startswith("<svg") and svg.rstrip().endswith("</svg>")
+    assert svg.count("<rect") >= 64 + 8  # 64 compute passes + lane backgrounds (+ transfers)
+
+
+def test_render_svg_is_well_formed():
+    import xml.dom.minidom
+    from fractions import Fraction
+
+    import paper_2503_01328_b200 as po
+    from paper_2503_01328_b200.render import render_svg
+
+    sched, plan = po.build_1f1b_full_offload(4, 8, po.PassCosts.unit(), Fraction(3, 2))
+    trace = po.simulate(sched, plan)
+    doc = xml.dom.minidom.parseString(render_svg(trace, title="c1 <golden>"))
+    rects = doc.getElementsByTagName("rect")
+    n_transfers = sum(1 for p in trace.passes if p.kind.value in ("OFFLOAD", "RELOAD"))
+    assert len(rects) == 8 + len(trace.passes) and n_transfers > 0
 
 
 @pytest.mark.gpu
@@ -37,3 +55,5 @@ def test_run_virtual_pipeline(tmp_path):
     summary = json.loads(res.stdout.strip().splitlines()[-1])
     assert summary["tokens_per_s"] > 0 and summary["schedule"] == "gis-h"
     assert (out / "gis-h-trace.csv").read_text().startswith("device,stage,microbatch,kind")
+    assert (out / "gis-h.svg").read_text().startswith("<svg")
+    assert summary["predicted_makespan_s"] > 0 and summary["measured_makespan_s"] > 0

@@ -9,7 +9,7 @@ def summarize(path, top=25):
     hdr_i = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr, data = rows[hdr_i], rows[hdr_i + 1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in data:
         if len(r) <= vi:
