@@ -27,6 +27,7 @@ duplex plan (``plan_slots_duplex``).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -335,7 +336,7 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- calibration: measured T_F, T_B (per stage), T_o (D2H + H2D of one payload)
     cal_stage = Stage(cfg, min(rank, d - 1) if world > 1 else 0, d, m, dev, layers=list(range(layers_per_stage)))
-    cal = calibrate(cal_stage)
+    cal = calibrate(cal_stage, split=False)
     if dist is not None:  # every rank plans with rank 0's measurements (identical programs)
         box = [cal]
         dist.broadcast_object_list(box, src=0)
@@ -389,8 +390,7 @@ def run_b200(args, rank, world, local_rank):
             results[name]["peak_act_gb_per_rank"] = per_rank
             results[name]["peak_act_gb"] = max(per_rank)
         results[name]["_res"] = res
-        for r in res.runners:
-            r.close()
+        res.close()
     full, none, auto, single = results["full"], results["none"], results["auto"], results["full_single"]
     duplex = results["full_duplex"]
     none_cublas = results["none_cublas"]

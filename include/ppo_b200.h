@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 4
+#define PPO_ABI_VERSION 5
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -152,6 +152,19 @@ int ppo_gelu_bwd(const void* f, const void* dg, void* g, void* df, int64_t n, vo
 /* Column sums of a rows x cols bf16 matrix accumulated into fp32 `acc` (bias grads,
  * tests). */
 int ppo_colsum(const void* x, float* acc, int64_t rows, int64_t cols, void* stream);
+
+/* ------------------------------------------- first-stage embedding (K0) */
+/* The first stage's input and its gradient, around the path: the reference
+ * models the first stage as an ordinary F/B pass (ir.py:97, builders.py:59-75);
+ * in a real GPT it owns the token/position embedding.
+ *   fwd: x[r] = wte[tokens[r]] + wpe[r]              (bf16, rows x hidden)
+ *   bwd: gwte[tokens[r]] += dy[r]; gwpe[r] += dy[r]  (fp32, 16-byte vector atomics)
+ * tokens: device int64[rows], clamped to [0, vocab); read at run time, so the
+ * launches can be captured in a CUDA graph.  hidden % 8 == 0, 16-byte aligned. */
+int ppo_embed_fwd(const int64_t* tokens, const void* wte, const void* wpe, void* x, int64_t rows, int64_t hidden,
+                  int64_t vocab, void* stream);
+int ppo_embed_bwd(const int64_t* tokens, const void* dy, float* gwte, float* gwpe, int64_t rows, int64_t hidden,
+                  int64_t vocab, void* stream);
 
 /* --------------------------------------------- K6: tcgen05 GEMMs (sm_100a) */
 /* D[M,N] = A[M,K] . B[N,K]^T, bf16 row-major in and out, fp32 accumulation in TMEM;

@@ -73,9 +73,10 @@ def residual_dropout(resid, branch, p, seed, offset):
     return bf16_round(resid.astype(np.float32) + dropout(branch, p, seed, offset))
 
 
-def pack(items, total_bytes):
-    """Gather (src_bytes, dst_off, rows, row_bytes, src_pitch) byte ranges into one buffer."""
-    out = np.zeros(total_bytes, dtype=np.uint8)
+def pack(items, total_bytes, base=None):
+    """Gather (src_bytes, dst_off, rows, row_bytes, src_pitch) byte ranges into one buffer
+    (zeros, or a copy of ``base``: bytes outside the items keep their values)."""
+    out = np.zeros(total_bytes, dtype=np.uint8) if base is None else np.array(base, dtype=np.uint8, copy=True)
     for src, off, rows, row_bytes, pitch in items:
         pitch = pitch or row_bytes
         for r in range(rows):

@@ -147,8 +147,7 @@ def cmd_run(args) -> int:
         _write(args.out, f"{sched.kind}.svg", render_svg(trace, title=f"measured {sched.kind} ({mode}) d={args.d} m={args.m}"))
         _write(args.out, f"{sched.kind}-summary.json", json.dumps(summary, indent=2, default=str))
         print(json.dumps(summary, default=str))
-    for r in res.runners:
-        r.close()
+    res.close()
     if world > 1:
         import torch.distributed as dist
 

@@ -130,6 +130,67 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ x, float* __rest
   for (int i = 0; i < 8; ++i) atomicAdd(acc + 8 * col8 + i, s[i]);
 }
 
+// Token + position embedding of the first stage: x[r] = wte[tok[r]] + wpe[r]
+// (bf16 sum rounded once, as torch's embedding + add).  One warp per row, 16-B
+// vectors; the token ids are read from device memory so the launch can sit in a
+// CUDA graph whose token row changes between replays.
+__global__ void __launch_bounds__(256) embed_fwd_kernel(const int64_t* __restrict__ tok,
+                                                        const __nv_bfloat16* __restrict__ wte,
+                                                        const __nv_bfloat16* __restrict__ wpe,
+                                                        __nv_bfloat16* __restrict__ x, int64_t rows, int64_t h,
+                                                        int64_t vocab) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n8 = h >> 3;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    int64_t t = __ldg(tok + r);
+    t = t < 0 ? 0 : (t >= vocab ? vocab - 1 : t);
+    const __nv_bfloat16* a = wte + t * h;
+    const __nv_bfloat16* b = wpe + r * h;
+    for (int64_t c = lane; c < n8; c += 32) {
+      float va[8], vb[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(a) + c), va);
+      unpack8(ld_stream(b + 8 * c), vb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) va[i] += vb[i];
+      st_stream(x + r * h + 8 * c, pack8(va));
+    }
+  }
+}
+
+// Embedding backward: gwte[tok[r]] += dy[r] and gwpe[r] += dy[r] in fp32, straight
+// from the bf16 gradient (no fp32 copy of dy); 16-byte vector atomics
+// (red.global.add.v4.f32) -- repeated tokens in a row add in arbitrary order, as
+// torch's index_add_.
+__global__ void __launch_bounds__(256) embed_bwd_kernel(const int64_t* __restrict__ tok,
+                                                        const __nv_bfloat16* __restrict__ dy,
+                                                        float* __restrict__ gwte, float* __restrict__ gwpe,
+                                                        int64_t rows, int64_t h, int64_t vocab) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n8 = h >> 3;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    int64_t t = __ldg(tok + r);
+    t = t < 0 ? 0 : (t >= vocab ? vocab - 1 : t);
+    for (int64_t c = lane; c < n8; c += 32) {
+      float v[8];
+      unpack8(ld_stream(dy + r * h + 8 * c), v);
+      float4* e = reinterpret_cast<float4*>(gwte + t * h + 8 * c);
+      float4* p = reinterpret_cast<float4*>(gwpe + r * h + 8 * c);
+      atomicAdd(e, make_float4(v[0], v[1], v[2], v[3]));
+      atomicAdd(e + 1, make_float4(v[4], v[5], v[6], v[7]));
+      atomicAdd(p, make_float4(v[0], v[1], v[2], v[3]));
+      atomicAdd(p + 1, make_float4(v[4], v[5], v[6], v[7]));
+    }
+  }
+}
+
+static int row_grid(int64_t rows) {
+  const int64_t cap = (int64_t)sm_count_current() * 8;  // 8 CTAs of 8 warps per SM
+  const int64_t want = (rows + 7) / 8;
+  return (int)(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
 static int elementwise_grid(int64_t n8) {
   const int64_t cap = (int64_t)sm_count_current() * 8;
   int64_t want = (n8 + 511) / 512;
@@ -178,6 +239,31 @@ int ppo_gelu_bwd(const void* f, const void* dg, void* g, void* df, int64_t n, vo
       static_cast<const __nv_bfloat16*>(f), static_cast<const __nv_bfloat16*>(dg), static_cast<__nv_bfloat16*>(g),
       static_cast<__nv_bfloat16*>(df), n >> 3);
   PPO_LAUNCHED("gelu_bwd_kernel");
+  return PPO_OK;
+}
+
+int ppo_embed_fwd(const int64_t* tokens, const void* wte, const void* wpe, void* x, int64_t rows, int64_t hidden,
+                  int64_t vocab, void* stream) {
+  if (!tokens || !wte || !wpe || !x || rows < 0 || hidden <= 0 || (hidden & 7) || vocab <= 0)
+    return set_error(PPO_EINVAL, "ppo_embed_fwd: bad arguments (hidden %% 8 != 0?)");
+  if (!aligned16(wte) || !aligned16(wpe) || !aligned16(x)) return set_error(PPO_EINVAL, "ppo_embed_fwd: unaligned");
+  if (rows == 0) return PPO_OK;
+  embed_fwd_kernel<<<row_grid(rows), 256, 0, as_stream(stream)>>>(
+      tokens, static_cast<const __nv_bfloat16*>(wte), static_cast<const __nv_bfloat16*>(wpe),
+      static_cast<__nv_bfloat16*>(x), rows, hidden, vocab);
+  PPO_LAUNCHED("embed_fwd_kernel");
+  return PPO_OK;
+}
+
+int ppo_embed_bwd(const int64_t* tokens, const void* dy, float* gwte, float* gwpe, int64_t rows, int64_t hidden,
+                  int64_t vocab, void* stream) {
+  if (!tokens || !dy || !gwte || !gwpe || rows < 0 || hidden <= 0 || (hidden & 7) || vocab <= 0)
+    return set_error(PPO_EINVAL, "ppo_embed_bwd: bad arguments (hidden %% 8 != 0?)");
+  if (!aligned16(dy) || !aligned16(gwte) || !aligned16(gwpe)) return set_error(PPO_EINVAL, "ppo_embed_bwd: unaligned");
+  if (rows == 0) return PPO_OK;
+  embed_bwd_kernel<<<row_grid(rows), 256, 0, as_stream(stream)>>>(
+      tokens, static_cast<const __nv_bfloat16*>(dy), gwte, gwpe, rows, hidden, vocab);
+  PPO_LAUNCHED("embed_bwd_kernel");
   return PPO_OK;
 }
 

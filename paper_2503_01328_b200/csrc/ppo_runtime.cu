@@ -85,6 +85,76 @@ __global__ void __launch_bounds__(256) pack_kernel(GatherArgs args, uint8_t* __r
   }
 }
 
+// TMA-staged pack for contiguous items: global -> shared (cp.async.bulk, mbarrier
+// completion) -> global (cp.async.bulk store), kBulkStages chunks of kBulkChunk bytes
+// in flight per CTA.  One thread per CTA issues everything; the copy engine-like TMA
+// unit moves the bytes, so the SM's load/store pipes and registers stay idle.
+constexpr int kBulkChunk = 16384;
+constexpr int kBulkStages = 6;
+struct BulkArgs {
+  const uint8_t* src[kMaxGather];
+  uint64_t dst_off[kMaxGather];
+  uint64_t bytes[kMaxGather];
+  uint64_t first_chunk[kMaxGather + 1];
+  int n;
+};
+
+__global__ void __launch_bounds__(32) pack_bulk_kernel(BulkArgs a, uint8_t* __restrict__ dst) {
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bar[kBulkStages];
+  if (threadIdx.x != 0) return;
+  const uint64_t n_chunks = a.first_chunk[a.n];
+  if (blockIdx.x >= n_chunks) return;
+  const uint64_t mine = (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  for (int i = 0; i < kBulkStages; ++i) mbar_init(&bar[i], 1);
+  mbar_fence_init();
+  auto locate = [&](uint64_t k, const uint8_t*& from, uint8_t*& to, uint32_t& len) {
+    const uint64_t c = blockIdx.x + k * gridDim.x;
+    int i = 0;
+    while (c >= a.first_chunk[i + 1]) ++i;
+    const uint64_t off = (c - a.first_chunk[i]) * kBulkChunk;
+    const uint64_t rest = a.bytes[i] - off;
+    from = a.src[i] + off;
+    to = dst + a.dst_off[i] + off;
+    len = (uint32_t)(rest < (uint64_t)kBulkChunk ? rest : (uint64_t)kBulkChunk);
+  };
+  auto load = [&](uint64_t k) {
+    const uint8_t* from;
+    uint8_t* to;
+    uint32_t len;
+    locate(k, from, to, len);
+    const int sidx = (int)(k % kBulkStages);
+    mbar_expect_tx(&bar[sidx], len);
+    tma_load_1d(stage + sidx * kBulkChunk, from, len, &bar[sidx]);
+  };
+  for (uint64_t k = 0; k < mine && k < (uint64_t)kBulkStages; ++k) load(k);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const int sidx = (int)(k % kBulkStages);
+    mbar_wait(&bar[sidx], (uint32_t)((k / kBulkStages) & 1));
+    const uint8_t* from;
+    uint8_t* to;
+    uint32_t len;
+    locate(k, from, to, len);
+    tma_store_1d(to, stage + sidx * kBulkChunk, len);
+    tma_store_commit();
+    // refill the buffer the previous store read from, once that store is done reading
+    if (k >= 1 && k - 1 + kBulkStages < mine) {
+      tma_store_wait_read<1>();
+      load(k - 1 + kBulkStages);
+    }
+  }
+  tma_store_wait_all();
+}
+
+static bool pack_use_bulk() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = std::getenv("PPO_PACK_MODE");
+    mode = (e && std::strcmp(e, "vector") == 0) ? 0 : 1;
+  }
+  return mode == 1;
+}
+
 }  // namespace ppo
 
 using namespace ppo;
@@ -180,6 +250,36 @@ int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream) {
   }
   args.n = n;
   if (chunks == 0) return PPO_OK;
+  bool contiguous = true;
+  for (int i = 0; i < n; ++i) {
+    const ppo_gather_item& it = items[i];
+    const uint64_t pitch = it.src_pitch ? it.src_pitch : it.row_bytes;
+    const uint64_t dpitch = it.dst_pitch ? it.dst_pitch : it.row_bytes;
+    contiguous &= it.rows <= 1 || (pitch == it.row_bytes && dpitch == it.row_bytes);
+  }
+  if (contiguous && pack_use_bulk() && (chunks << 4) >= (1u << 20)) {
+    BulkArgs b;
+    std::memset(&b, 0, sizeof(b));
+    b.n = n;
+    for (int i = 0; i < n; ++i) {
+      b.src[i] = static_cast<const uint8_t*>(items[i].src);
+      b.dst_off[i] = items[i].dst_off;
+      b.bytes[i] = items[i].row_bytes * items[i].rows;
+      b.first_chunk[i + 1] = b.first_chunk[i] + (b.bytes[i] + kBulkChunk - 1) / kBulkChunk;
+    }
+    static bool attr = false;
+    const int smem = kBulkStages * kBulkChunk;
+    if (!attr) {
+      PPO_TRY_CUDA(cudaFuncSetAttribute(pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    const uint64_t cap = (uint64_t)sm_count_current() * 2;  // two 96 KB stagings per SM
+    const uint64_t nc = b.first_chunk[n];
+    const int blocks = (int)(nc < cap ? nc : cap);
+    pack_bulk_kernel<<<blocks, 32, smem, as_stream(stream)>>>(b, static_cast<uint8_t*>(dst));
+    PPO_LAUNCHED("pack_bulk_kernel");
+    return PPO_OK;
+  }
   const int threads = 256;
   uint64_t want = (chunks + threads * 4 - 1) / (threads * 4);
   const uint64_t cap = (uint64_t)sm_count_current() * 8;  // 8 CTAs of 256 per SM resident

@@ -16,9 +16,9 @@ from . import native
 from .model import SlabView
 
 
-def calibrate(stage, reps: int = 3) -> dict:
-    """T_F, T_B (and split T_B / T_W) of one microbatch of the stage, and the D2H / H2D
-    time of its slab alone and under full-duplex load."""
+def calibrate(stage, reps: int = 3, split: bool = True) -> dict:
+    """T_F, T_B (and, with ``split``, split T_B / T_W) of one microbatch of the stage,
+    and the D2H / H2D time of its slab alone and under full-duplex load."""
     dev = stage.device
     slab_mem = torch.empty(stage.layout.slab_bytes, dtype=torch.uint8, device=dev)
     slab = SlabView(stage.layout, slab_mem)
@@ -43,9 +43,11 @@ def calibrate(stage, reps: int = 3) -> dict:
             tf.append(e[0].elapsed_time(e[1]) / 1e3)
             tb.append(e[1].elapsed_time(e[2]) / 1e3)
     # split backward (GIS / PO schedules): B = activation gradients, W = weight gradients
-    wbuf = stage.new_wbuffer()
-    tbs, tws = [], []
-    for r in range(reps + 1):
+    tbs, tws = [float("nan")], [float("nan")]
+    for r in range(reps + 1 if split else 0):
+        if r == 0:
+            wbuf = stage.new_wbuffer()
+            tbs, tws = [], []
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         stage.set_pass_context(0, 0, tok)
         e[0].record()
@@ -57,8 +59,11 @@ def calibrate(stage, reps: int = 3) -> dict:
         if r:
             tbs.append(e[0].elapsed_time(e[1]) / 1e3)
             tws.append(e[1].elapsed_time(e[2]) / 1e3)
-    del wbuf
+    wbuf = None
     lay = stage.layout
+    from .executor import check_host_memory
+
+    check_host_memory(2 * (lay.host_bytes + 4096))
     pool = native.PinnedPool(lay.host_bytes + 4096)
     bins, acc = [], pool.carve(lay.host_bytes)
     for b in lay.bins:
@@ -126,7 +131,7 @@ def calibrate_costs(cfg, n_stages: int, microbatches: int, device, units: int = 
 
     middle = min(1, n_stages - 1)
     st = Stage(cfg, middle, n_stages, microbatches, device, layers=stage_layers(cfg, n_stages, middle))
-    cal = calibrate(st)
+    cal = calibrate(st, split=split)
     del st
     torch.cuda.empty_cache()
     hop = (2 * cfg.seq * cfg.hidden) / 770e9 + 10e-6

@@ -266,6 +266,7 @@ class RankRunner:
             self.host_slot_base = []
             if program.n_host_slots:
                 slot_bytes = (self.host_bytes + 4095) // 4096 * 4096
+                check_host_memory(program.n_host_slots * slot_bytes)
                 self.pool = native.PinnedPool(program.n_host_slots * slot_bytes)
                 self.host_slot_base = [self.pool.carve(slot_bytes) for _ in range(program.n_host_slots)]
             s_, h = cfg.seq, cfg.hidden
@@ -283,6 +284,12 @@ class RankRunner:
         self.verify_roundtrip = verify_roundtrip
         self.use_graphs = use_graphs
         self.graphs = {}
+        # One memory pool for every pass graph of this rank: passes replay one at a
+        # time on the compute stream and keep nothing in pool memory past their end
+        # (outputs go to the slab arena, rings and workspaces), so their temporaries
+        # (cuDNN attention outputs, dq/dk/dv) can share addresses instead of each graph
+        # pinning a private copy -- at C4 shape that is tens of GB.
+        self.graph_pool = None
         self.wbufs = {}
         self.graph_native_launches = {}  # libppo_b200 kernels inside each captured pass
         self.replayed_native_launches = 0  # ... executed through graph replays
@@ -454,7 +461,9 @@ class RankRunner:
         graph = torch.cuda.CUDAGraph()
         before = native.kernel_launches()
         snap = native.call_counts()
-        graph.capture_begin(capture_error_mode="thread_local")
+        if self.graph_pool is None:
+            self.graph_pool = torch.cuda.graph_pool_handle()
+        graph.capture_begin(pool=self.graph_pool, capture_error_mode="thread_local")
         try:
             body()
         finally:
@@ -560,6 +569,42 @@ class RankRunner:
         if self.pool is not None:
             self.pool.close()
             self.pool = None
+
+
+def host_memory_available() -> int:
+    """Bytes of host memory this process may still pin: MemAvailable, capped by the
+    cgroup (v2 or v1) limit minus current usage when one is set."""
+    avail = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    avail = int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    for lim_p, use_p in (("/sys/fs/cgroup/memory.max", "/sys/fs/cgroup/memory.current"),
+                         ("/sys/fs/cgroup/memory/memory.limit_in_bytes", "/sys/fs/cgroup/memory/memory.usage_in_bytes")):
+        try:
+            with open(lim_p) as f:
+                lim = f.read().strip()
+            with open(use_p) as f:
+                use = int(f.read().strip())
+            if lim != "max" and int(lim) < (1 << 60):
+                room = int(lim) - use
+                avail = room if avail is None else min(avail, room)
+                break
+        except (OSError, ValueError):
+            continue
+    return avail if avail is not None else (1 << 62)
+
+
+def check_host_memory(nbytes: int, fraction: float = 0.8) -> None:
+    """Refuse a pinned pool larger than ``fraction`` of the host memory left: pinning
+    past that takes the box down instead of failing."""
+    avail = host_memory_available()
+    if nbytes > fraction * avail:
+        raise MemoryError(f"pinned host pool of {nbytes / 1e9:.1f} GB exceeds {fraction:.0%} of the "
+                          f"{avail / 1e9:.1f} GB host memory available")
 
 
 def _digest(buf: torch.Tensor) -> torch.Tensor:
@@ -668,6 +713,13 @@ class RunResult:
     host_slots: dict
     wall_seconds: list  # e2e: host clock per step incl. input H2D and result D2H
     host_issue_seconds: list = field(default_factory=list)  # host time to enqueue one iteration
+
+    def close(self):
+        """Release the pinned pools and drop the runners (their device arenas, weights
+        and graphs go with the last reference)."""
+        for r in self.runners:
+            r.close()
+        self.runners.clear()
 
 
 def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelConfig, microbatches: int | None = None,

@@ -269,8 +269,7 @@ class Stage:
         ``tokens``: the microbatch's [s+1] token row (None: use the pass context)."""
         if tokens is not None:
             self.tok.copy_(tokens, non_blocking=True)
-        x0 = slab.get(0, "x")
-        torch.add(torch.nn.functional.embedding(self.tok[:-1], self.w["wte"]), self.w["wpe"], out=x0)
+        native.embed_fwd(self.tok[:-1], self.w["wte"], self.w["wpe"], slab.get(0, "x"))
 
     def forward(self, slab: SlabView, mb: int, iteration: int, out: torch.Tensor | None = None,
                 tokens: torch.Tensor | None = None):
@@ -429,8 +428,7 @@ class Stage:
                                  drop_seed=seed, drop_offset=off_below, eps=eps, offset_base=self.ctx)
             dy_cur = dx_target
         if self.first:
-            self.g["wte"].index_add_(0, self.tok[:-1], dy_cur.float())
-            self.g["wpe"].add_(dy_cur.float())
+            native.embed_bwd(self.tok[:-1], dy_cur, self.g["wte"], self.g["wpe"])
 
     def wgrad_body(self, slab: SlabView, wbuf: dict):
         """W pass of a split backward: weight gradients from the slab (recomputing

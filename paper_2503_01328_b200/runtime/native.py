@@ -73,6 +73,8 @@ SIGNATURES = {
     "ppo_gelu_fwd": [_VP, _VP, _I64, _VP],
     "ppo_gelu_bwd": [_VP, _VP, _VP, _VP, _I64, _VP],
     "ppo_colsum": [_VP, _VP, _I64, _I64, _VP],
+    "ppo_embed_fwd": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
+    "ppo_embed_bwd": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_tn": [_VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_tn_gelu": [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_nn": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
@@ -109,7 +111,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 4:
+        if lib.ppo_abi_version() != 5:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -288,6 +290,26 @@ def _torch():
     import torch
 
     return torch
+
+
+def embed_fwd(tokens, wte, wpe, x, stream=None):
+    """x[r] = wte[tokens[r]] + wpe[r] (first stage input; tokens: int64 [rows] on device)."""
+    _check_bf16(wte, wpe, x)
+    rows, h = x.shape
+    if tokens.dtype != _torch().int64 or tokens.numel() != rows or wte.shape[1] != h or tuple(wpe.shape) != (rows, h):
+        raise ValueError("embed_fwd shapes")
+    call("ppo_embed_fwd", _ptr(tokens), _ptr(wte), _ptr(wpe), _ptr(x), rows, h, wte.shape[0], _stream(stream))
+
+
+def embed_bwd(tokens, dy, gwte, gwpe, stream=None):
+    """gwte[tokens[r]] += dy[r]; gwpe[r] += dy[r] (fp32 accumulators, bf16 dy)."""
+    _check_bf16(dy)
+    rows, h = dy.shape
+    t = _torch()
+    if (tokens.dtype != t.int64 or tokens.numel() != rows or gwte.dtype != t.float32 or gwpe.dtype != t.float32
+            or gwte.shape[1] != h or tuple(gwpe.shape) != (rows, h)):
+        raise ValueError("embed_bwd shapes")
+    call("ppo_embed_bwd", _ptr(tokens), _ptr(dy), _ptr(gwte), _ptr(gwpe), rows, h, gwte.shape[0], _stream(stream))
 
 
 def colsum(x, acc, stream=None):

@@ -1,0 +1,71 @@
+"""The C ABI (include/ppo_b200.h) on a machine without a GPU: the library loads,
+exports every declared entry point, the ctypes binding covers exactly the header,
+the ABI version agrees, and argument errors come back as PPO_E* codes with a
+message -- no compute call is made."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2503_01328_b200 import build_native
+from paper_2503_01328_b200.runtime import native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ppo_b200.h")
+
+
+def declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"^\s*(?:int|const char\*|uint64_t|void\*)\s+(ppo_\w+)\s*\(", text, flags=re.M))
+
+
+def macro(name):
+    m = re.search(rf"#define {name} \(?(-?\d+)\)?", open(HEADER).read())
+    return int(m.group(1))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(native.LIB_PATH):
+        build_native.build()
+    return ctypes.CDLL(native.LIB_PATH)
+
+
+def test_header_declares_the_bound_entry_points():
+    names = declared()
+    assert len(names) >= 25
+    assert names == set(native.SIGNATURES), (names ^ set(native.SIGNATURES))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in sorted(declared()) if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_abi_version_and_binding_load(lib):
+    lib.ppo_abi_version.restype = ctypes.c_int
+    assert lib.ppo_abi_version() == macro("PPO_ABI_VERSION")
+    assert native.load() is not None  # the ctypes binding accepts this library
+
+
+def test_argument_errors_are_codes_not_crashes():
+    lib = native.load()
+    einval = macro("PPO_EINVAL")
+    assert lib.ppo_pack(None, -1, None, None) == einval
+    assert b"ppo_pack" in lib.ppo_last_error()
+    assert lib.ppo_dropout(None, None, 7, ctypes.c_float(0.1), 0, 0, None, None) == einval
+    assert lib.ppo_transfer(7, None, 0, None, None, None) == einval
+    assert lib.ppo_embed_fwd(None, None, None, None, 4, 12, 10, None) == einval
+    assert lib.ppo_pool_create(0, None) == einval
+    assert lib.ppo_pool_destroy(None) == 0
+    assert lib.ppo_pool_bytes(None) == 0
+
+
+def test_product_path_refuses_to_run_without_cuda():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("a GPU is present")
+    with pytest.raises(native.NativeUnavailable):
+        native.require_cuda()

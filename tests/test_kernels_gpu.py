@@ -127,6 +127,26 @@ def test_pack_gather_bit_exact():
     assert np.array_equal(dst.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("sizes", [(16 * 1024 * 1024 + 48, 262144, 16), (1 << 20,), (3 * 16384 + 32, 5 << 20)])
+def test_pack_tma_bulk_bit_exact(sizes):
+    """Contiguous items >= 1 MiB in total take the TMA bulk path (cp.async.bulk
+    global->smem->global, 16 KiB chunks, ragged tails); every byte lands exactly
+    where the numpy restatement puts it, and nothing outside the items is touched."""
+    rng = np.random.default_rng(len(sizes))
+    srcs = [rng.integers(0, 256, n, dtype=np.uint8) for n in sizes]
+    offs, acc = [], 32
+    for n in sizes:
+        offs.append(acc)
+        acc += (n + 255) // 256 * 256 + 64
+    total = acc + 128
+    dst = torch.full((total,), 0xA5, dtype=torch.uint8, device=DEV)
+    items = [(torch.from_numpy(x).to(DEV), o, 1, x.size, 0) for x, o in zip(srcs, offs)]
+    native.pack(items, dst)
+    want = np.full(total, 0xA5, dtype=np.uint8)
+    want = ref.pack([(x, o, 1, x.size, 0) for x, o in zip(srcs, offs)], total, base=want)
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
 def test_offload_reload_round_trip_bit_exact():
     """K2: device slab -> pinned bins -> fresh device slab, every byte identical."""
     from paper_2503_01328_b200.runtime.layout import make_layout
@@ -187,3 +207,28 @@ def test_tcgen05_gemms_match_fp32(M, N, K):
     want = acc + d.float().t() @ a.float()
     native.gemm_wgrad(d, a, acc, 1.0)
     assert rel(acc, want) < 1e-4
+
+
+@pytest.mark.parametrize("rows,h,vocab", [(512, 256, 1024), (4096, 2048, 50304), (8, 8, 3)])
+def test_embedding_fwd_bwd(rows, h, vocab):
+    """First-stage embedding: forward bit-exact vs torch (one bf16 rounding of the
+    sum); backward = fp32 index_add of the bf16 gradient (atomics: order-free up to
+    fp32 rounding), with repeated tokens."""
+    g = torch.Generator(device="cpu").manual_seed(rows + h)
+    tok = torch.randint(0, vocab, (rows,), generator=g)
+    tok[: rows // 4] = tok[0]  # many repeats of one token
+    tok = tok.to(DEV)
+    wte = (torch.randn(vocab, h, generator=g) * 0.02).to(DEV, torch.bfloat16)
+    wpe = (torch.randn(rows, h, generator=g) * 0.02).to(DEV, torch.bfloat16)
+    x = torch.empty(rows, h, device=DEV, dtype=torch.bfloat16)
+    native.embed_fwd(tok, wte, wpe, x)
+    want = torch.nn.functional.embedding(tok, wte) + wpe
+    assert torch.equal(x, want)
+    dy = (torch.randn(rows, h, generator=g)).to(DEV, torch.bfloat16)
+    gwte = torch.randn(vocab, h, device=DEV)
+    gwpe = torch.randn(rows, h, device=DEV)
+    w_te, w_pe = gwte.clone().index_add_(0, tok, dy.float()), gwpe + dy.float()
+    native.embed_bwd(tok, dy, gwte, gwpe)
+    torch.cuda.synchronize()
+    assert torch.equal(gwpe, w_pe)
+    torch.testing.assert_close(gwte, w_te, rtol=1e-5, atol=1e-4 * max(1.0, rows / 64))

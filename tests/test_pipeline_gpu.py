@@ -139,3 +139,63 @@ def test_split_backward_schedules_match_oracle(kind, oracle_result):
     got = _grads(res)
     for k, g in want_grads.items():
         assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
+
+
+def _variant(name):
+    """(schedule, plan, stream_mode) of the plan variants the engine must run exactly."""
+    from paper_2503_01328_b200.offload import plan_slots_duplex
+    from paper_2503_01328_b200.policy import choose_offload
+
+    U = po.PassCosts.unit()
+    if name == "late_reloads_k2":  # k = 2: reloads miss their slots (sim floors them later)
+        sched = po.build_1f1b(4, 1, 8, U)
+        plan = po.plan_slots(sched, (0,), Fraction(6))
+        assert plan.late_list()
+        return sched, plan, "single"
+    if name == "dual_streams":
+        sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+        return sched, plan, "dual"
+    if name == "duplex_plan":
+        sched = po.build_1f1b(4, 1, 8, U)
+        return sched, plan_slots_duplex(sched, (0,), Fraction(3, 2)), "dual"
+    if name == "k_aware_stride":  # every 2nd microbatch offloaded (k = 4 / 3)
+        sched = po.build_1f1b(8, 1, 16, U)
+        choice = choose_offload(sched, (0,), Fraction(4), tolerance=0.05, focus_rank=0)
+        assert choice.plan is not None and choice.stride > 1
+        return sched, choice.plan, "single"
+    if name == "pp1_all_skipped":  # d = 1: zero F->B window, every pair skips (builders.py:252-253)
+        sched, plan = po.build_1f1b_full_offload(1, 4, U, Fraction(3, 2))
+        assert not plan.offloaded_pairs()
+        return sched, plan, "single"
+    if name == "m_not_multiple_of_d":
+        sched, plan = po.build_1f1b_full_offload(4, 6, U, Fraction(3, 2))
+        return sched, plan, "single"
+    if name == "gis_g":
+        sched = po.build_gis_g(4, 2, 8, 3, U)
+        assert sched.kind == "gis-g"
+        plan = po.plan_slots(sched, po.select_offload_stages(po.po_block(4, 2, U), 1), Fraction(2))
+        return sched, plan, "single"
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["late_reloads_k2", "dual_streams", "duplex_plan", "k_aware_stride",
+                                  "pp1_all_skipped", "m_not_multiple_of_d", "gis_g"])
+def test_plan_variants_exact(name, oracle_result):
+    """Every plan shape the planner can emit runs with bit-exact round trips, and the
+    first step's loss is bit-identical to the same schedule without offload (the
+    forward is a pure function of weights, tokens and Philox seeds)."""
+    sched, plan, mode = _variant(name)
+    m = sched.microbatches
+    cfg = CFG if sched.num_stages <= 4 else ModelConfig(n_layers=sched.num_stages, hidden=256, heads=4, seq=512,
+                                                       vocab=1024)
+    tokens = torch.randint(0, cfg.vocab, (m, cfg.seq + 1), generator=torch.Generator().manual_seed(m))
+    kw = dict(model=cfg, mode="virtual", tokens=tokens, optimizer="none", iters=1, warmup=0)
+    on = ex.execute(sched, plan, stream_mode=mode, verify_roundtrip=True, **kw)
+    off = ex.execute(sched, None, **kw)
+    assert ex.roundtrip_mismatches(on.runners) == []
+    assert on.losses[0] == off.losses[0]
+    g_on, g_off = _grads(on), _grads(off)
+    for k in g_off:
+        assert rel(g_on[k], g_off[k]) < 1e-3, k
+    if plan.offloaded_pairs():
+        assert sum(len(p.offloaded) for p in on.programs.values()) == len(plan.offloaded_pairs())

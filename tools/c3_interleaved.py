@@ -7,6 +7,7 @@ n = 1..v) and the k-aware plan, each on one copy stream and on t
 One JSON line per policy to stdout and gpurun_out/c3_interleaved.jsonl.
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -19,8 +20,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2503_01328_b200.runtime.calibrate import calibrate  # noqa: E402
-from paper_2503_01328_b200 import (build_interleaved_1f1b, measured_pass_costs, plan_slots, po_block,  # noqa: E402
-                                   select_offload_stages, simulate, peak_memory)
+from paper_2503_01328_b200 import (BUILDERS, build_interleaved_1f1b, measured_pass_costs, plan_slots,  # noqa: E402
+                                   po_block, select_offload_stages, simulate, peak_memory)
 from paper_2503_01328_b200.policy import choose_offload  # noqa: E402
 from paper_2503_01328_b200.runtime import native  # noqa: E402
 from paper_2503_01328_b200.runtime.executor import execute  # noqa: E402
@@ -37,24 +38,30 @@ def main():
     ap.add_argument("--m", type=int, default=32)
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--schedule", default="1f1b-i", choices=["1f1b-i", "gis-h", "po"],
+                    help="interleaved 1F1B, or the split-backward GIS-H / PO (the paper's PipeOffload schedule)")
+    ap.add_argument("--ns", default=None, help="offloaded local-stage counts to measure, e.g. 1,2 (default 1..v)")
     a = ap.parse_args()
+    split = a.schedule != "1f1b-i"
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     per_chunk = a.layers // (a.d * a.v)
     cfg = ModelConfig(n_layers=a.layers, hidden=a.h, heads=a.h // 128, seq=a.s, vocab=1024)
     st = Stage(cfg, 1, a.d * a.v, a.m, dev, layers=list(range(per_chunk)))
-    cal = calibrate(st)
+    cal = calibrate(st, split=split)
     del st
     torch.cuda.empty_cache()
-    costs = measured_pass_costs(cal["t_f"], cal["t_b"], 0.0, (2 * a.s * a.h) / 770e9 + 10e-6)
+    hop = (2 * a.s * a.h) / 770e9 + 10e-6
+    costs = (measured_pass_costs(cal["t_f"], cal["t_b_split"], cal["t_w_split"], hop) if split
+             else measured_pass_costs(cal["t_f"], cal["t_b"], 0.0, hop))
     t_o = Fraction(round((cal["t_d2h"] + cal["t_h2d"]) * 1e6), 1_000_000)
-    sched = build_interleaved_1f1b(a.d, a.v, a.m, costs)
-    head = {"h": a.h, "s": a.s, "d": a.d, "v": a.v, "m": a.m, "layers_per_chunk": per_chunk,
+    sched = build_interleaved_1f1b(a.d, a.v, a.m, costs) if not split else BUILDERS[a.schedule](a.d, a.v, a.m, costs)
+    head = {"schedule": sched.kind, "h": a.h, "s": a.s, "d": a.d, "v": a.v, "m": a.m, "layers_per_chunk": per_chunk,
             "k_measured": float(t_o / costs.total), "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3,
             "T_o_ms": float(t_o) * 1e3}
     block = po_block(a.d, a.v, sched.costs)
     plans = {"none": None}
-    for n in range(1, a.v + 1):
+    for n in (map(int, a.ns.split(",")) if a.ns else range(1, a.v + 1)):
         plans[f"selective_n{n}"] = plan_slots(sched, select_offload_stages(block, n), t_o)
     choice = choose_offload(sched, select_offload_stages(block, 1), t_o, tolerance=0.05, focus_rank=0)
     if choice.plan is not None:
@@ -76,9 +83,9 @@ def main():
                 if base is None:
                     base = row["tokens_per_s"]
                 row["overhead_pct"] = 100 * (base / row["tokens_per_s"] - 1)
-                for r in res.runners:
-                    r.close()
+                res.close()
                 del res
+                gc.collect()
                 torch.cuda.empty_cache()
                 line = json.dumps(row)
                 print(line, flush=True)

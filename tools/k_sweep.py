@@ -9,6 +9,7 @@ per shape to stdout and gpurun_out/k_sweep.jsonl.
 usage: python tools/k_sweep.py [--hs 2048,4096,8192] [--ss 2048,4096,8192,16384,32768] [--m 16]
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -32,7 +33,7 @@ def run_point(h, s, m, d, iters, warmup, dev):
     heads = h // 128
     cfg = ModelConfig(n_layers=d, hidden=h, heads=heads, seq=s, vocab=1024)
     st = Stage(cfg, 1, d, m, dev, layers=[0])  # a middle stage: no embedding / head
-    cal = calibrate(st)
+    cal = calibrate(st, split=False)
     del st
     torch.cuda.empty_cache()
     costs = measured_pass_costs(cal["t_f"], cal["t_b"], 0.0, (2 * s * h) / 770e9 + 10e-6)
@@ -54,9 +55,9 @@ def run_point(h, s, m, d, iters, warmup, dev):
         out[name] = {"tokens_per_s": m * s / it, "ms_per_step": it * 1e3, "peak_slabs": prog.n_slabs,
                      "peak_act_gb": prog.n_slabs * res.slab_bytes / 1e9, "offloaded": len(prog.offloaded),
                      "late": len(plan.late_list()) if plan is not None else 0}
-        for r in res.runners:
-            r.close()
+        res.close()
         del res
+        gc.collect()
         torch.cuda.empty_cache()
     base = out["none"]["tokens_per_s"]
     for name in ("full", "auto"):

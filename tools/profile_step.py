@@ -26,3 +26,15 @@ sched = build_1f1b(8, 3, 32, costs)
 plan = plan_slots(sched, (0,), Fraction(17750)) if a.policy == "full" else None
 res = execute(sched, plan, model=cfg, mode="emulate", rank=0, iters=a.iters, warmup=a.warmup)
 print("iteration ms", [round(x * 1e3, 2) for x in res.iteration_seconds])
+if a.iters > 1 or a.warmup:
+    import statistics
+
+    tr = res.trace
+    comp = sorted((p for p in tr.passes if p.kind.value in ("F", "B", "W")), key=lambda p: p.start)
+    for kind in ("F", "B"):
+        ds = [float(p.duration) * 1e3 for p in comp if p.kind.value == kind]
+        print(kind, "n", len(ds), "median ms", round(statistics.median(ds), 4), "sum ms", round(sum(ds), 2))
+    gaps = [float(b.start - (a_.start + a_.duration)) * 1e3 for a_, b in zip(comp, comp[1:])]
+    print("gaps between passes: sum ms", round(sum(gaps), 2), "max", round(max(gaps), 3))
+    print("first pass start ms", round(float(comp[0].start) * 1e3, 3), "last end ms",
+          round(float(comp[-1].start + comp[-1].duration) * 1e3, 3))
