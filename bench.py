@@ -109,7 +109,7 @@ def measured_peaks():
             d = json.load(f)
         return d.get("hbm_gbs", 6650.0), "measured", d
     except Exception:
-        return 6650.0, "fallback", {}
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s, earlier measurement on this pool)", {}
 
 
 def measured_tflops():
@@ -118,7 +118,7 @@ def measured_tflops():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f)["bf16_tflops"], "measured"
     except Exception:
-        return 2250.0, "fallback (nominal dense bf16)"
+        return 1590.0, "fallback (B200_PROFILING.md: 1.59 PFLOP/s burst, earlier measurement on this pool)"
 
 
 def workload_config(config: str, world: int) -> dict:
@@ -272,21 +272,47 @@ def measure_gemms(shapes, dev, torch, native, sets=2):
     return out
 
 
+def partial_candidates(sched, t_o, layers, s, h, heads, top=3):
+    """Per-tensor partial-offload plans (``policy.choose_partial_offload``): prefixes of
+    ``layout.offload_candidates`` priced by the runner model at t_o x (share that
+    travels); the ``top`` least-memory plans within 5% modelled overhead, one per
+    tensor set."""
+    from paper_2503_01328_b200.policy import choose_partial_offload
+    from paper_2503_01328_b200.runtime.layout import make_layout, offload_candidates
+
+    order = offload_candidates(layers)
+    cands = []
+    for j in range(1, len(order)):
+        lay = make_layout(layers, s, h, heads, offload=order[:j])
+        label = "+".join(f"{n}{l}" for l, n in order[:j])
+        cands.append((label, tuple(order[:j]), lay.off_bytes, lay.res_bytes))
+    out, seen = [], set()
+    for c in choose_partial_offload(sched, (0,), t_o, cands, rank=0, tolerance=0.05, max_stride=2):
+        if c.label in seen:
+            continue
+        seen.add(c.label)
+        out.append(c)
+        if len(out) == top:
+            break
+    return out
+
+
 def policy_report(res, sched, plan, m, seq, slab_bytes, rank):
     it = statistics.median(res.iteration_seconds)
     wall = statistics.median(res.wall_seconds)
     prog = res.programs[rank]
     d2h = [p for p in res.trace.transfer_passes() if p.kind.value == "OFFLOAD"]
     h2d = [p for p in res.trace.transfer_passes() if p.kind.value == "RELOAD"]
-    gbs = lambda ps: (len(ps) * slab_bytes / float(sum(p.duration for p in ps)) / 1e9) if ps else None  # noqa: E731
+    moved = slab_bytes * res.offload_fraction  # bytes one transfer carries (partial offload: a share of the slab)
+    gbs = lambda ps: (len(ps) * moved / float(sum(p.duration for p in ps)) / 1e9) if ps else None  # noqa: E731
     comp = [p for p in res.trace.compute_passes()]
     busy = float(sum(p.duration for p in comp))
     return {
         "tokens_per_s": m * seq / it,
         "e2e_tokens_per_s": m * seq / wall,
         "ms_per_step": 1000 * it,
-        "peak_act_slabs": prog.n_slabs,
-        "peak_act_gb": prog.n_slabs * slab_bytes / 1e9,
+        "peak_act_slabs": prog.n_slabs if res.offload_fraction >= 1 else None,
+        "peak_act_gb": res.act_bytes[rank] / 1e9,
         "host_slots": prog.n_host_slots,
         "offloaded_pairs": len(prog.offloaded),
         "late_reloads": len(plan.late_list()) if plan is not None else 0,
@@ -352,6 +378,8 @@ def run_b200(args, rank, world, local_rank):
              "full_duplex": plan_slots_duplex(sched, (0,), Fraction(round(cal["t_duplex"] * 1e6), 1_000_000))}
     choice = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
     plans["auto"] = choice.plan
+    # per-tensor partial offload (k-aware): the model's best few candidates are measured
+    partial = partial_candidates(sched, t_o, layers_per_stage, s, h, heads, top=args.partial_top)
 
     tokens = torch.randint(0, vocab, (m, s + 1), generator=torch.Generator().manual_seed(0)).pin_memory()
     results = {}
@@ -391,6 +419,24 @@ def run_b200(args, rank, world, local_rank):
             results[name]["peak_act_gb"] = max(per_rank)
         results[name]["_res"] = res
         res.close()
+    for i, c in enumerate(partial):
+        name = f"partial{i}"
+        res = execute(sched, c.plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
+                      warmup=args.warmup, tokens=tokens, optimizer="sgd", stream_mode=c.stream_mode,
+                      offload_tensors=c.tensors)
+        results[name] = dict(policy_report(res, sched, c.plan, m, s, res.slab_bytes, rank),
+                             tensors=c.label, offload_fraction=round(res.offload_fraction, 4),
+                             stream_mode=c.stream_mode, stride=c.stride, modelled_overhead=round(c.overhead, 4),
+                             modelled_act_gb=c.act_bytes / 1e9)
+        if dist is not None:
+            per_rank = [None] * world
+            dist.all_gather_object(per_rank, results[name]["peak_act_gb"])
+            results[name]["peak_act_gb_per_rank"] = per_rank
+            results[name]["peak_act_gb"] = max(per_rank)
+        res.close()
+        del res
+        gc.collect()
+        torch.cuda.empty_cache()
     full, none, auto, single = results["full"], results["none"], results["auto"], results["full_single"]
     duplex = results["full_duplex"]
     none_cublas = results["none_cublas"]
@@ -478,8 +524,16 @@ def run_b200(args, rank, world, local_rank):
             "overhead_full_single_stream_pct": 100 * (none["tokens_per_s"] / single["tokens_per_s"] - 1),
             "overhead_full_duplex_pct": 100 * (none["tokens_per_s"] / duplex["tokens_per_s"] - 1),
             "t_duplex_oneway_ms": cal["t_duplex"] * 1e3,
+            "partial_candidates": [results[f"partial{i}"] for i in range(len(partial))],
         },
     }
+    # k-aware partial offload: the least-memory measured candidate within 5% of no offload
+    ok = [r for r in line["offload"]["partial_candidates"] if r["tokens_per_s"] >= none["tokens_per_s"] / 1.05]
+    if ok:
+        best = min(ok, key=lambda r: r["peak_act_gb"])
+        line["offload"]["partial"] = best
+        line["offload"]["overhead_partial_pct"] = 100 * (none["tokens_per_s"] / best["tokens_per_s"] - 1)
+        line["offload"]["partial_peak_reduction_pct"] = 100 * (1 - best["peak_act_gb"] / none["peak_act_gb"])
     line["cpu_baseline"] = cpu_baseline(args) if not args.no_cpu_baseline else None
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -505,6 +559,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partial-top", type=int, default=3, help="partial-offload plans to measure (0: none)")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":

@@ -70,3 +70,79 @@ def choose_offload(
         if score(peaks) < score(best.peak_units):
             best = PolicyChoice(plan, q, tr.makespan, base.makespan, peaks, base_peaks, len(plan.offloaded_pairs()))
     return best
+
+
+@dataclass(frozen=True)
+class PartialChoice:
+    """One partial-offload candidate: which tensors travel, the plan, and its modelled cost."""
+
+    label: str
+    tensors: tuple | None  # (local layer, name) that travel; None = the whole saved set
+    off_bytes: int
+    res_bytes: int
+    plan: OffloadPlan | None
+    stream_mode: str
+    stride: int | None
+    overhead: float
+    off_peak: int  # arena slots of offload parts (modelled peak, pairs)
+    res_peak: int  # arena slots of resident parts (= in-flight peak)
+
+    @property
+    def act_bytes(self) -> int:
+        return self.off_peak * self.off_bytes + (self.res_peak * self.res_bytes if self.res_bytes else 0)
+
+
+def choose_partial_offload(
+    sched: Schedule,
+    stages,
+    t_o: Fraction,
+    candidates,
+    rank: int = 0,
+    tolerance: float = 0.05,
+    stream_modes=("single", "dual"),
+    max_stride: int = 4,
+) -> list[PartialChoice]:
+    """Per-tensor partial offload (B200 extension).
+
+    At k > 1 a pair's whole saved set cannot make the round trip inside its F->B
+    window, but a fraction a of it can: its round trip is a * t_o.  Each candidate
+    (label, tensors, off_bytes, res_bytes) names the tensors that travel (the
+    offload part) and the bytes that stay (the resident part).  For every candidate,
+    stream discipline (one copy stream with the reference's ``plan_slots`` grid, or
+    duplex streams with ``plan_slots_duplex``) and microbatch stride q, the reference
+    runner model prices the plan at t_o * a; the resident parts stay from F start to
+    the pair's last use, so rank ``rank`` holds
+
+        off_peak * off_bytes + res_peak * res_bytes
+
+    with off_peak the modelled peak of the offload parts and res_peak the in-flight
+    peak.  Returns every candidate within ``tolerance`` of no offload, least
+    activation bytes first (the no-offload baseline last)."""
+    from .offload import plan_slots_duplex
+
+    base = simulate(sched)
+    res_peak = base.memory.peak(rank) // sched.units_per_stage
+    units = sched.units_per_stage
+    limit = base.makespan * (1 + Fraction(tolerance).limit_denominator(10_000))
+    out = []
+    for label, tensors, off_b, res_b in candidates:
+        slab = off_b + res_b
+        t_a = Fraction(t_o) * Fraction(off_b, slab)
+        t_a = Fraction(max(1, round(t_a * 10**6)), 10**6)  # integer microseconds (costs.measured_pass_costs)
+        for mode in stream_modes:
+            for q in range(1, max_stride + 1):
+                pairs = {(s, j) for s in range(sched.num_stages) for j in range(sched.microbatches) if j % q == 0}
+                if mode == "single":
+                    plan = plan_slots(sched, stages, t_a, pairs=pairs)
+                else:
+                    plan = plan_slots_duplex(sched, stages, t_a / 2, pairs=pairs)
+                if plan.late_list() or not plan.offloaded_pairs():
+                    continue
+                tr = simulate(sched, plan, stream_mode=mode)
+                if tr.makespan > limit:
+                    continue
+                off_peak = tr.memory.peak(rank) // units
+                out.append(PartialChoice(label, tensors, off_b, res_b, plan, mode, q,
+                                         float(tr.makespan / base.makespan - 1), off_peak, res_peak))
+    out.sort(key=lambda c: (c.act_bytes, c.overhead))
+    return out

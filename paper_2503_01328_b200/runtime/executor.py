@@ -244,7 +244,8 @@ class RankRunner:
 
     def __init__(self, program: Program, cfg: ModelConfig, sched: Schedule, microbatches: int, device,
                  transport=None, emulate: bool = False, params=None, seed: int = 1234, optimizer: str = "sgd",
-                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "best"):
+                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "best",
+                 offload_tensors=None):
         torch_ = native.require_cuda()
         self.torch = torch_
         self.prog, self.cfg, self.sched, self.m = program, cfg, sched, microbatches
@@ -256,12 +257,19 @@ class RankRunner:
         with torch.cuda.device(self.device):
             self.stages = {
                 s: Stage(cfg, s, sched.num_stages, microbatches, self.device, params=params,
-                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm)
+                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm, offload=offload_tensors)
                 for s in my_stages
             }
-            self.slab_bytes = max(st.layout.slab_bytes for st in self.stages.values())
-            self.host_bytes = max(st.layout.host_bytes for st in self.stages.values())
-            self.arena = torch.empty(max(1, program.n_slabs) * self.slab_bytes, dtype=torch.uint8, device=self.device)
+            lays = [st.layout for st in self.stages.values()]
+            self.slab_bytes = max(l.slab_bytes for l in lays)  # whole saved set of one pair
+            self.off_bytes = max(l.off_bytes for l in lays)  # the part that travels
+            self.res_bytes = max(l.res_bytes for l in lays)  # the part that never does
+            self.host_bytes = max(l.host_bytes for l in lays)
+            # two fixed arenas: offload parts coloured over their residency (freed at D2H end),
+            # resident parts over F start .. last use (the in-flight peak)
+            self.arena = torch.empty(max(1, program.n_slabs) * self.off_bytes, dtype=torch.uint8, device=self.device)
+            self.res_arena = (torch.empty(max(1, program.n_res_slabs) * self.res_bytes, dtype=torch.uint8,
+                                          device=self.device) if self.res_bytes else None)
             self.pool = None
             self.host_slot_base = []
             if program.n_host_slots:
@@ -310,13 +318,25 @@ class RankRunner:
             self.events[key] = e
         return e
 
-    def slab(self, idx: int, stage: int) -> SlabView:
-        key = (idx, stage)
+    @property
+    def act_bytes(self) -> int:
+        """Device bytes held for activations: both arenas (the measured per-GPU peak)."""
+        return self.prog.n_slabs * self.off_bytes + (self.prog.n_res_slabs * self.res_bytes if self.res_bytes else 0)
+
+    def _rkey(self, op):
+        """Resident slot as part of a pass-graph key (None when there is no resident part)."""
+        return op.res_slab if self.res_bytes else None
+
+    def slab(self, op, stage: int) -> SlabView:
+        idx, ridx = op.slab, (op.res_slab if self.res_bytes else 0)
+        key = (idx, ridx, stage)
         v = self.views.get(key)
         if v is None:
             lay = self.stages[stage].layout
-            base = self.arena[idx * self.slab_bytes: idx * self.slab_bytes + lay.slab_bytes]
-            v = SlabView(lay, base)
+            base = self.arena[idx * self.off_bytes: idx * self.off_bytes + lay.off_bytes]
+            res = (self.res_arena[ridx * self.res_bytes: ridx * self.res_bytes + lay.res_bytes]
+                   if self.res_bytes else base[lay.off_bytes:])
+            v = SlabView(lay, base, res)
             self.views[key] = v
         return v
 
@@ -384,7 +404,7 @@ class RankRunner:
         st = self.stages[s]
         self.ev(("F_start", s, j)).record(stream)
         with torch.cuda.stream(stream):
-            slab = self.slab(op.slab, s)
+            slab = self.slab(op, s)
             st.set_pass_context(j, self.iteration, self.tokens[j])
             if st.first:
                 st.embed(slab)
@@ -396,7 +416,7 @@ class RankRunner:
             out = None
             if not st.last:
                 out = self.rings["send_act"][op.send_ring] if op.send_ring is not None else self.scratch_out
-            key = ("F", s, op.slab, out.data_ptr() if out is not None else 0)
+            key = ("F", s, op.slab, self._rkey(op), out.data_ptr() if out is not None else 0)
             self._run_body(key, lambda: st.forward_body(slab, out), stream)
             if self.verify_roundtrip and (s, j) in self.prog.offloaded:
                 self.digests[(s, j)] = [_digest(slab.base), None]
@@ -407,7 +427,7 @@ class RankRunner:
         st = self.stages[s]
         self.ev(("B_start", s, j)).record(stream)
         with torch.cuda.stream(stream):
-            slab = self.slab(op.slab, s)
+            slab = self.slab(op, s)
             if self.verify_roundtrip and (s, j) in self.prog.offloaded:
                 self.digests[(s, j)][1] = _digest(slab.base)
             st.set_pass_context(j, self.iteration, self.tokens[j] if st.first else None)
@@ -418,7 +438,7 @@ class RankRunner:
             if not st.first:
                 dx_out = self.rings["send_grad"][op.send_ring] if op.send_ring is not None else self.scratch_out
             wbuf = self.wbuf(op.wbuf, s) if op.wbuf is not None else None
-            key = ("B", s, op.slab, dy.data_ptr() if dy is not None else 0, dx_out.data_ptr() if dx_out is not None else 0,
+            key = ("B", s, op.slab, self._rkey(op), dy.data_ptr() if dy is not None else 0, dx_out.data_ptr() if dx_out is not None else 0,
                    op.wbuf)
             self._run_body(key, lambda: st.backward_body(slab, dy, dx_out, wbuf), stream)
         self.ev(("B_end", s, j)).record(stream)
@@ -428,9 +448,9 @@ class RankRunner:
         st = self.stages[s]
         self.ev(("W_start", s, j)).record(stream)
         with torch.cuda.stream(stream):
-            slab = self.slab(op.slab, s)
+            slab = self.slab(op, s)
             wbuf = self.wbuf(op.wbuf, s)
-            self._run_body(("W", s, op.slab, op.wbuf), lambda: st.wgrad_body(slab, wbuf), stream)
+            self._run_body(("W", s, op.slab, self._rkey(op), op.wbuf), lambda: st.wgrad_body(slab, wbuf), stream)
         self.ev(("W_end", s, j)).record(stream)
 
     def wbuf(self, idx: int, stage: int) -> dict:
@@ -478,7 +498,7 @@ class RankRunner:
     def _transfer(self, op, stream):
         s, j = op.stage, op.mb
         lay = self.stages[s].layout
-        slab_ptr = self.arena.data_ptr() + op.slab * self.slab_bytes
+        slab_ptr = self.arena.data_ptr() + op.slab * self.off_bytes
         segs = lay.segments(slab_ptr, self.host_bins(op.host_slot, s))
         tag = "D2H" if op.kind == "OFFLOAD" else "H2D"
         self.ev((tag + "_start", s, j)).record(stream)
@@ -713,6 +733,8 @@ class RunResult:
     host_slots: dict
     wall_seconds: list  # e2e: host clock per step incl. input H2D and result D2H
     host_issue_seconds: list = field(default_factory=list)  # host time to enqueue one iteration
+    act_bytes: dict = field(default_factory=dict)  # rank -> activation arena bytes (both parts)
+    offload_fraction: float = 1.0  # share of a pair's saved set that travels when it is offloaded
 
     def close(self):
         """Release the pinned pools and drop the runners (their device arenas, weights
@@ -726,13 +748,15 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
-            use_graphs: bool = True, gemm: str = "best") -> RunResult:
+            use_graphs: bool = True, gemm: str = "best", offload_tensors=None) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
     boundary) or "nccl" (this process is ``rank`` of a torchrun job; "gloo" is the
     same over host copies, for ranks that share a GPU in tests).
     ``tokens``: [m, s+1] int64 host tensor (pinned for the e2e path).
+    ``offload_tensors``: None (an offloaded pair moves its whole saved set) or the
+    (local layer, name) tensors that move (partial offload, ``layout.make_layout``).
 
     In the multi-process modes every iteration starts after a device synchronise
     and a barrier, and the returned iteration/wall times and losses are the same on
@@ -760,7 +784,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     dist_mode = mode in ("nccl", "gloo")
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
-                          use_graphs=use_graphs, gemm=gemm) for r in ranks]
+                          use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors) for r in ranks]
     if tokens is None:
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
@@ -806,4 +830,5 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
     return RunResult(trace, secs, losses, programs, runners, slab_bytes,
                      {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners},
-                     walls, host_secs)
+                     walls, host_secs, {r.rank: r.act_bytes for r in runners},
+                     max(r.off_bytes for r in runners) / max(1, slab_bytes))

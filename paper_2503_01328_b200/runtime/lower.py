@@ -55,6 +55,7 @@ class Op:
     waits: list = field(default_factory=list)
     records: list = field(default_factory=list)
     slab: int | None = None
+    res_slab: int | None = None  # resident-part slot (partial offload; = in-flight colouring)
     host_slot: int | None = None
     ring: int | None = None
     peer: int | None = None  # remote rank of a boundary op
@@ -74,6 +75,7 @@ class Program:
     ops: list  # host issue order
     n_slabs: int
     n_host_slots: int
+    n_res_slabs: int
     n_wbufs: int
     offloaded: set
     witness_makespan: Fraction
@@ -172,6 +174,10 @@ def lower(
             if pair in offloaded:
                 intervals.append((h2d[pair].start, done, ("R",) + pair))
     slab_of, n_slabs = _colour(intervals)
+    # resident part of every slab (partial offload keeps it on the device from F start
+    # to the pair's last use, offloaded or not): colours = the in-flight peak
+    res_of, n_res = _colour([(p.start, timed[(last_use, p.stage, p.microbatch)].end, ("P", p.stage, p.microbatch))
+                             for p in my_passes if p.kind == F])
     wbuf_of, n_wbufs = _colour([(timed[(B,) + pr].start, timed[(W,) + pr].end, ("G",) + pr)
                                 for pr in ((p.stage, p.microbatch) for p in my_passes if p.kind == B)]) if split else ({}, 0)
     host_of, n_host = _colour([(d2h[pr].start, h2d[pr].end, ("H",) + pr) for pr in sorted(offloaded)])
@@ -208,6 +214,9 @@ def lower(
             rel = release_event(prev)
             if rel:
                 op.waits.append(rel)
+            op.res_slab, prev_res = res_of[("P",) + pair]
+            if prev_res is not None and (f"{last_use}_end",) + prev_res[1:] != rel:
+                op.waits.append((f"{last_use}_end",) + prev_res[1:])
             if s > 0:
                 src = placement[s - 1]
                 if src == rank and not emulate_neighbors:
@@ -247,6 +256,7 @@ def lower(
             op = Op("W", s, j, "compute", p.start)
             op.records = [("W_start", s, j), ("W_end", s, j)]
             op.slab = slab_of[(("R",) if pair in offloaded else ("F",)) + pair][0]
+            op.res_slab = res_of[("P",) + pair][0]
             op.wbuf = wbuf_of[("G",) + pair][0]
             compute_ops.append(op)
             continue
@@ -258,6 +268,7 @@ def lower(
                 op.slab = slab_of[("R",) + pair][0]
             else:
                 op.slab = slab_of[("F",) + pair][0]
+            op.res_slab = res_of[("P",) + pair][0]
             if split:
                 op.wbuf = wbuf_of[("G",) + pair][0]
             if s < last_stage:
@@ -332,7 +343,8 @@ def lower(
     assert got == want, "lowering changed the per-device op order"
     peak = trace.memory.peak(rank)
     return Program(
-        rank=rank, devices=sched.devices, ops=ordered, n_slabs=n_slabs, n_host_slots=n_host, n_wbufs=n_wbufs,
+        rank=rank, devices=sched.devices, ops=ordered, n_slabs=n_slabs, n_host_slots=n_host, n_res_slabs=n_res,
+        n_wbufs=n_wbufs,
         offloaded=offloaded, witness_makespan=trace.makespan, witness_peak_units=peak,
         compute_order=want, copy_order=copy_order, recv_orders=recv_orders, send_orders=send_orders,
     )

@@ -94,32 +94,45 @@ def _wgrad(acc: torch.Tensor, a_t: torch.Tensor, b: torch.Tensor) -> None:
 
 
 class SlabView:
-    """Typed tensor views of one slab (device memory owned by the arena)."""
+    """Typed tensor views of one slab (device memory owned by the arena).
 
-    def __init__(self, layout: SlabLayout, base: torch.Tensor):
+    ``base`` holds the offload part (the bytes that travel, layout.off_bytes); the
+    resident part lives at ``res_base`` -- a separate arena slot under partial
+    offload, or simply the rest of ``base`` when the slab is one contiguous buffer."""
+
+    def __init__(self, layout: SlabLayout, base: torch.Tensor, res_base: torch.Tensor | None = None):
         self.layout = layout
-        self.base = base  # uint8 tensor of layout.slab_bytes
+        if res_base is None:  # one contiguous buffer of layout.slab_bytes
+            res_base = base[layout.off_bytes: layout.slab_bytes]
+            base = base[: layout.off_bytes]
+        self.base = base  # uint8 tensor of layout.off_bytes
+        self.res_base = res_base  # uint8 tensor of layout.res_bytes
         self._cache = {}
+
+    def locate(self, layer: int, name: str) -> tuple[torch.Tensor, int]:
+        """(part base tensor, byte offset inside it) of one saved tensor."""
+        slot = self.layout.find(layer, name)
+        if self.layout.travels(slot):
+            return self.base, slot.dev_offset
+        return self.res_base, slot.dev_offset - self.layout.off_bytes
 
     def get(self, layer: int, name: str) -> torch.Tensor:
         key = (layer, name)
         t = self._cache.get(key)
         if t is None:
             slot = self.layout.find(layer, name)
-            raw = self.base[slot.dev_offset: slot.dev_offset + slot.nbytes]
+            part, off = self.locate(layer, name)
+            raw = part[off: off + slot.nbytes]
             t = raw.view(torch.bfloat16 if slot.dtype == "bf16" else torch.float32).view(slot.shape)
             self._cache[key] = t
         return t
-
-    def offset(self, layer: int, name: str) -> int:
-        return self.layout.find(layer, name).dev_offset
 
 
 class Stage:
     """Parameters, gradients, workspace and the F/B passes of one pipeline stage."""
 
     def __init__(self, cfg: ModelConfig, stage: int, num_stages: int, microbatches: int, device, params=None,
-                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "best"):
+                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "best", offload=None):
         native.require_cuda()
         if gemm not in ("best", "tcgen05", "cublas"):
             raise ValueError(f"gemm backend {gemm!r}")
@@ -131,7 +144,10 @@ class Stage:
         self.first, self.last = stage == 0, stage == num_stages - 1
         self.layers = layers if layers is not None else stage_layers(cfg, num_stages, stage)
         self.device = torch.device(device)
-        self.layout = make_layout(len(self.layers), cfg.seq, cfg.hidden, cfg.heads, head_grad=self.last)
+        # offload: None = the whole saved set travels; else the (local layer, name)
+        # tensors that do (partial offload, layout.make_layout)
+        self.layout = make_layout(len(self.layers), cfg.seq, cfg.hidden, cfg.heads, head_grad=self.last,
+                                  offload=offload)
         names = set()
         for l in self.layers:
             names |= {f"l{l}.{k}" for k in ("ln1_g", "ln1_b", "w_qkv", "w_proj", "ln2_g", "ln2_b", "w_fc1", "w_fc2")}
@@ -323,8 +339,13 @@ class Stage:
         s, h, H = self.cfg.seq, self.cfg.hidden, self.cfg.heads
         if not o_tmp.transpose(1, 2).is_contiguous() or not lse.is_contiguous():
             raise RuntimeError(f"unexpected cuDNN attention layout: o {o_tmp.stride()} lse {lse.stride()}")
-        items = [(o_tmp, slab.offset(i, "o"), 1, 2 * s * h, 0), (lse, slab.offset(i, "lse"), 1, 4 * H * s, 0)]
-        self._k("pack", 2 * (2 * s * h + 4 * H * s), native.pack, items, slab.base)
+        (o_base, o_off), (l_base, l_off) = slab.locate(i, "o"), slab.locate(i, "lse")
+        items = [(o_tmp, o_off, 1, 2 * s * h, 0), (lse, l_off, 1, 4 * H * s, 0)]
+        if o_base is l_base:
+            self._k("pack", 2 * (2 * s * h + 4 * H * s), native.pack, items, o_base)
+        else:  # partial offload: o and lse in different parts (lse travels with o; defensive)
+            self._k("pack", 4 * s * h, native.pack, items[:1], o_base)
+            self._k("pack", 8 * H * s, native.pack, items[1:], l_base)
 
     def _head(self, slab: SlabView, targets: torch.Tensor):
         """Loss head of the last stage, forward and backward fused into F.

@@ -232,3 +232,23 @@ def test_embedding_fwd_bwd(rows, h, vocab):
     torch.cuda.synchronize()
     assert torch.equal(gwpe, w_pe)
     torch.testing.assert_close(gwte, w_te, rtol=1e-5, atol=1e-4 * max(1.0, rows / 64))
+
+
+@pytest.mark.parametrize("nbytes", [16, 4096 * 2048 * 2 + 6])
+def test_nccl_p2p_self_loop(nbytes):
+    """K8 on hardware with one GPU: a 1-rank NCCL communicator sends to and receives
+    from itself in one grouped ppo_p2p call (the same ncclGroupStart/ncclSend/ncclRecv
+    path the pipeline's 2-rank edge communicators use); bytes arrive bit-exact."""
+    comm = native.NcclComm(native.NcclComm.unique_id(), 1, 0, 0)
+    try:
+        src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=DEV)
+        dst = torch.zeros_like(src)
+        stream = torch.cuda.Stream(DEV)
+        stream.wait_stream(torch.cuda.current_stream(DEV))
+        comm.p2p([(True, 0, src.data_ptr(), nbytes), (False, 0, dst.data_ptr(), nbytes)], stream.cuda_stream)
+        stream.synchronize()
+        assert torch.equal(src, dst)
+        with pytest.raises(native.PpoError):
+            comm.p2p([(True, 1, src.data_ptr(), nbytes)], stream.cuda_stream)  # peer out of range
+    finally:
+        comm.close()

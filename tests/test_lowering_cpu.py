@@ -37,6 +37,7 @@ class CpuWalker:
     def __init__(self, sched, prog, channel):
         self.sched, self.prog, self.channel = sched, prog, channel
         self.slabs = [None] * max(1, prog.n_slabs)
+        self.res = [None] * max(1, prog.n_res_slabs)  # resident parts (partial offload)
         self.host = [None] * max(1, prog.n_host_slots)
         self.rings = {k: [None] * 2 for k in ("recv_act", "send_act", "recv_grad", "send_grad")}
         self.cursor = 0
@@ -58,6 +59,8 @@ class CpuWalker:
             assert self.slabs[op.slab] is None or self.slabs[op.slab][0] not in self.live, "slab still live"
             self.slabs[op.slab] = (pair, x)
             self.live.add(pair)
+            assert self.res[op.res_slab] is None, f"resident slot of F{pair} still held by {self.res[op.res_slab]}"
+            self.res[op.res_slab] = pair
             y = x + 1.0
             if op.stage < last and op.send_ring is not None:
                 self.rings["send_act"][op.send_ring] = y
@@ -74,6 +77,7 @@ class CpuWalker:
         elif op.kind == "B":
             tag, x = self.slabs[op.slab]
             assert tag == pair, f"B{pair} found slab holding {tag}"
+            assert self.res[op.res_slab] == pair, f"B{pair} found resident slot holding {self.res[op.res_slab]}"
             g = x + 1.0 if op.stage == last else self.rings["recv_grad"][op.ring]
             gx = 2.0 * g
             self.grad_out[pair] = gx
@@ -83,14 +87,17 @@ class CpuWalker:
             else:
                 self.live.discard(pair)
                 self.slabs[op.slab] = None
+                self.res[op.res_slab] = None
             if op.stage > 0 and op.send_ring is not None:
                 self.rings["send_grad"][op.send_ring] = gx
         elif op.kind == "W":
             assert self.slabs[op.slab][0] == pair, f"W{pair} found slab holding {self.slabs[op.slab][0]}"
             assert self.wbufs.get(op.wbuf) == pair, f"W{pair} found gradient buffer of {self.wbufs.get(op.wbuf)}"
+            assert self.res[op.res_slab] == pair, f"W{pair} found resident slot holding {self.res[op.res_slab]}"
             self.wbufs[op.wbuf] = None
             self.live.discard(pair)
             self.slabs[op.slab] = None
+            self.res[op.res_slab] = None
         elif op.kind in ("SEND_ACT", "SEND_GRAD"):
             ring = "send_act" if op.kind == "SEND_ACT" else "send_grad"
             self.channel.send(op, self.rings[ring][op.ring])
@@ -179,6 +186,8 @@ def test_arena_matches_reference_peaks_c1():
     progs = [lower(sched, plan, r) for r in range(4)]
     assert [p.n_slabs for p in progs] == [2, 2, 2, 1]  # peaks [2,2,2,1]
     assert [lower(sched, None, r).n_slabs for r in range(4)] == [4, 3, 2, 1]
+    # resident parts (partial offload) are held F start .. B end: the no-offload peak
+    assert [p.n_res_slabs for p in progs] == [4, 3, 2, 1]
 
 
 def test_send_recv_orders_match_across_ranks():

@@ -199,3 +199,28 @@ def test_plan_variants_exact(name, oracle_result):
         assert rel(g_on[k], g_off[k]) < 1e-3, k
     if plan.offloaded_pairs():
         assert sum(len(p.offloaded) for p in on.programs.values()) == len(plan.offloaded_pairs())
+
+
+@pytest.mark.parametrize("tensors", [((0, "f"),), ((0, "f"), (0, "qkv"), (0, "o"))])
+def test_c1_partial_offload_matches_oracle(oracle_result, tensors):
+    """Per-tensor partial offload (layout.make_layout(offload=...)): only the named
+    tensors travel (bit-exact round trip of the offload part), the resident part
+    stays in its own arena; the run matches the oracle like full offload does."""
+    tokens, want_loss, want_grads = oracle_result
+    U = po.PassCosts.unit()
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    res = ex.execute(sched, plan, model=CFG, mode="virtual", tokens=tokens, optimizer="none", verify_roundtrip=True,
+                     offload_tensors=tensors)
+    assert ex.roundtrip_mismatches(res.runners) == []
+    assert sum(len(p.offloaded) for p in res.programs.values()) == 24
+    assert 0 < res.offload_fraction < 1
+    for r in res.runners:
+        lay = next(iter(r.stages.values())).layout
+        assert r.act_bytes == r.prog.n_slabs * r.off_bytes + r.prog.n_res_slabs * r.res_bytes
+        assert r.prog.n_res_slabs == [4, 3, 2, 1][r.rank]  # in-flight peak (no-offload arena)
+        assert lay.host_bytes < lay.slab_bytes
+    loss = res.losses[-1]
+    assert abs(loss - want_loss) < 0.02 * abs(want_loss), (loss, want_loss)
+    got = _grads(res)
+    for k, g in want_grads.items():
+        assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
