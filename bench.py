@@ -362,7 +362,7 @@ def run_b200(args, rank, world, local_rank):
 
     # ---- calibration: measured T_F, T_B (per stage), T_o (D2H + H2D of one payload)
     cal_stage = Stage(cfg, min(rank, d - 1) if world > 1 else 0, d, m, dev, layers=list(range(layers_per_stage)))
-    cal = calibrate(cal_stage, split=False)
+    cal = calibrate(cal_stage, split=True)
     if dist is not None:  # every rank plans with rank 0's measurements (identical programs)
         box = [cal]
         dist.broadcast_object_list(box, src=0)
@@ -380,6 +380,22 @@ def run_b200(args, rank, world, local_rank):
     plans["auto"] = choice.plan
     # per-tensor partial offload (k-aware): the model's best few candidates are measured
     partial = partial_candidates(sched, t_o, layers_per_stage, s, h, heads, top=args.partial_top)
+    # the paper's split-backward schedules at v = layers per stage (1-layer chunks): GIS-H
+    # and PO, without offload and with the reference's selective plan n=1
+    # (select_offload_stages(po_block(d, v), 1), cli.py:159-160) on duplex copy streams
+    sched_variants = {}
+    if args.schedules and layers_per_stage > 1 and world == 1:
+        from paper_2503_01328_b200 import build_gis_h, build_po, po_block, select_offload_stages
+
+        v = layers_per_stage
+        c1 = measured_pass_costs(cal["t_f"] / v, cal["t_b_split"] / v, cal["t_w_split"] / v,
+                                 (2 * s * h) / 770e9 + 10e-6)
+        w1 = Fraction(round(cal["t_duplex"] / v * 1e6), 1_000_000)
+        for kind, builder in (("gis-h", build_gis_h), ("po", build_po)):
+            sv = builder(d, v, m, c1)
+            st = select_offload_stages(po_block(d, v, c1), 1)
+            sched_variants[f"{kind}_v{v}_none"] = (sv, None, "single")
+            sched_variants[f"{kind}_v{v}_n1_duplex"] = (sv, plan_slots_duplex(sv, st, w1), "dual")
 
     tokens = torch.randint(0, vocab, (m, s + 1), generator=torch.Generator().manual_seed(0)).pin_memory()
     results = {}
@@ -399,7 +415,7 @@ def run_b200(args, rank, world, local_rank):
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
                       stream_mode="single" if name in ("none", "none_cublas", "auto", "full_single") else "dual",
-                      gemm="cublas" if name == "none_cublas" else "best")
+                      gemm="cublas" if name == "none_cublas" else "best", iteration_graph=args.iteration_graph)
         # real launches = eager launches + kernels executed by graph replays
         # (launch calls made while capturing a graph record nodes, they do not run)
         replayed = sum(r.replayed_native_launches for r in res.runners)
@@ -423,11 +439,25 @@ def run_b200(args, rank, world, local_rank):
         name = f"partial{i}"
         res = execute(sched, c.plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd", stream_mode=c.stream_mode,
-                      offload_tensors=c.tensors)
+                      offload_tensors=c.tensors, iteration_graph=args.iteration_graph)
         results[name] = dict(policy_report(res, sched, c.plan, m, s, res.slab_bytes, rank),
                              tensors=c.label, offload_fraction=round(res.offload_fraction, 4),
                              stream_mode=c.stream_mode, stride=c.stride, modelled_overhead=round(c.overhead, 4),
                              modelled_act_gb=c.act_bytes / 1e9)
+        if dist is not None:
+            per_rank = [None] * world
+            dist.all_gather_object(per_rank, results[name]["peak_act_gb"])
+            results[name]["peak_act_gb_per_rank"] = per_rank
+            results[name]["peak_act_gb"] = max(per_rank)
+        res.close()
+        del res
+        gc.collect()
+        torch.cuda.empty_cache()
+    for name, (sv, pv, sm) in sched_variants.items():
+        res = execute(sv, pv, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps, warmup=args.warmup,
+                      tokens=tokens, optimizer="sgd", stream_mode=sm, iteration_graph=args.iteration_graph)
+        results[name] = dict(policy_report(res, sv, pv, m, s, res.slab_bytes, rank), schedule=sv.kind,
+                             v=sv.local_stages, stream_mode=sm)
         if dist is not None:
             per_rank = [None] * world
             dist.all_gather_object(per_rank, results[name]["peak_act_gb"])
@@ -525,6 +555,7 @@ def run_b200(args, rank, world, local_rank):
             "overhead_full_duplex_pct": 100 * (none["tokens_per_s"] / duplex["tokens_per_s"] - 1),
             "t_duplex_oneway_ms": cal["t_duplex"] * 1e3,
             "partial_candidates": [results[f"partial{i}"] for i in range(len(partial))],
+            "schedules": {k: results[k] for k in sched_variants},
         },
     }
     # k-aware partial offload: the least-memory measured candidate within 5% of no offload
@@ -534,6 +565,16 @@ def run_b200(args, rank, world, local_rank):
         line["offload"]["partial"] = best
         line["offload"]["overhead_partial_pct"] = 100 * (none["tokens_per_s"] / best["tokens_per_s"] - 1)
         line["offload"]["partial_peak_reduction_pct"] = 100 * (1 - best["peak_act_gb"] / none["peak_act_gb"])
+    # every measured (schedule, plan) within 5% of 1F1B without offload: the least memory
+    cands = {"1f1b_" + k: line["offload"][k] for k in ("no_offload", "full", "full_duplex_plan", "partial")
+             if k in line["offload"]}
+    cands.update(line["offload"]["schedules"])
+    ok = {k: r for k, r in cands.items() if r["tokens_per_s"] >= none["tokens_per_s"] / 1.05}
+    kbest = min(ok, key=lambda k: ok[k]["peak_act_gb"])
+    line["offload"]["least_memory_within_5pct"] = {
+        "policy": kbest, "tokens_per_s": ok[kbest]["tokens_per_s"], "peak_act_gb": ok[kbest]["peak_act_gb"],
+        "overhead_pct": 100 * (none["tokens_per_s"] / ok[kbest]["tokens_per_s"] - 1),
+        "peak_reduction_pct": 100 * (1 - ok[kbest]["peak_act_gb"] / none["peak_act_gb"])}
     line["cpu_baseline"] = cpu_baseline(args) if not args.no_cpu_baseline else None
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -559,6 +600,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-iteration-graph", dest="iteration_graph", action="store_false",
+                    help="issue passes per step from the host (per-pass CUDA graphs) instead of one graph per step")
+    ap.add_argument("--no-schedules", dest="schedules", action="store_false",
+                    help="skip the GIS-H / PO split-backward schedule variants")
     ap.add_argument("--partial-top", type=int, default=3, help="partial-offload plans to measure (0: none)")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 5
+#define PPO_ABI_VERSION 6
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -84,6 +84,13 @@ typedef struct {
  * anchor lowered from the slot start (sim.py:177-181). */
 int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_stream,
                  void* wait_event, void* done_event);
+
+/* Stream-ordered timestamp: one thread writes the GPU global timer (ns) to *slot
+ * (device memory) when the stream reaches it.  Times the passes inside a captured
+ * whole-iteration CUDA graph without event records, whose host-visible semaphore
+ * writes queue behind saturated PCIe offload traffic (profiles/r1_issue_paths.json).
+ * Replaces the reference runner's clock bookkeeping of pass start/end (sim.py:334-353). */
+int ppo_timestamp(uint64_t* slot, void* stream);
 
 /* ------------------------------------------------------------ K1: pack / gather */
 /* Gather `n` 2-D byte ranges into one destination: item i copies `rows[i]` rows of

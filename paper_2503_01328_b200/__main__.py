@@ -29,6 +29,7 @@ from fractions import Fraction
 
 from . import (BUILDERS, PassCosts, build_gis_g, emit_schedule, peak_memory, plan_slots, po_block,
                select_offload_stages, simulate)
+from .offload import plan_slots_duplex
 from .policy import choose_offload
 from .render import render_svg
 
@@ -67,14 +68,20 @@ def _write(out: str, name: str, text: str) -> None:
     os.replace(tmp, os.path.join(out, name))
 
 
-def _plan(sched, d, v, costs, t_o, offload):
+def _plan(sched, d, v, costs, t_o, offload, planner="slots", t_duplex=None):
+    """planner: "slots" = the reference's one-stream slot grid (offload.py:209-220);
+    "duplex" = independent D2H / H2D grids (``plan_slots_duplex``) of one-way width
+    ``t_duplex`` (measured with both directions in flight; default t_o / 2)."""
     n = _offload_count(offload, v)
     if not n:
         return None
     block = po_block(d, v, costs)
     if n == "auto":
         return choose_offload(sched, select_offload_stages(block, 1), t_o).plan
-    return plan_slots(sched, select_offload_stages(block, n), t_o)
+    stages = select_offload_stages(block, n)
+    if planner == "duplex":
+        return plan_slots_duplex(sched, stages, t_duplex if t_duplex is not None else t_o / 2)
+    return plan_slots(sched, stages, t_o)
 
 
 def cmd_plan(args) -> int:
@@ -124,16 +131,17 @@ def cmd_run(args) -> int:
     split = args.schedule in ("gis", "gis-g", "gis-h", "po")
     costs, t_o, cal = calibrate_costs(cfg, n_stages, args.m, dev, units=units, split=split)
     sched = _build(args.schedule, args.d, args.v, args.m, args.g, costs)
-    plan = _plan(sched, args.d, args.v, costs, t_o, args.offload)
+    t_dup = Fraction(round(cal["t_duplex"] * 1e6), 1_000_000) if cal.get("t_duplex") else None
+    plan = _plan(sched, args.d, args.v, costs, t_o, args.offload, args.planner, t_dup)
     res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.iters, warmup=args.warmup,
-                  stream_mode=args.stream_mode, optimizer=args.optimizer)
+                  stream_mode=args.stream_mode, optimizer=args.optimizer, iteration_graph=args.iteration_graph)
     trace = res.trace
     it = max(res.iteration_seconds)
     predicted = simulate(sched, plan, stream_mode=args.stream_mode)
     summary = dict(trace.summary(), schedule=sched.kind, mode=mode, d=args.d, v=args.v, m=args.m,
                    tokens_per_s=args.m * args.seq / it, ms_per_step=it * 1e3,
                    arena_slabs={str(k): v for k, v in res.peak_slabs.items()},
-                   arena_gb={str(k): v * res.slab_bytes / 1e9 for k, v in res.peak_slabs.items()},
+                   arena_gb={str(k): v / 1e9 for k, v in res.act_bytes.items()},
                    modelled_peak_units=[u for u, _ in peak_memory(simulate(sched, plan))["per_device"]],
                    k_measured=float(t_o / (costs.total * units)), calibration=cal,
                    predicted_makespan_s=float(predicted.makespan), measured_makespan_s=float(trace.makespan),
@@ -179,6 +187,10 @@ def make_parser() -> argparse.ArgumentParser:
     run.add_argument("--vocab", type=int, default=1024)
     run.add_argument("--mode", choices=("emulate", "virtual"), default="virtual")
     run.add_argument("--stream-mode", choices=("single", "dual"), default="single")
+    run.add_argument("--iteration-graph", action="store_true",
+                     help="capture each iteration as one CUDA graph (emulate / virtual modes)")
+    run.add_argument("--planner", choices=("slots", "duplex"), default="slots",
+                     help="slots: reference plan_slots; duplex: plan_slots_duplex (run with --stream-mode dual)")
     run.add_argument("--optimizer", choices=("none", "sgd", "adamw"), default="sgd")
     run.add_argument("--iters", type=int, default=2)
     run.add_argument("--warmup", type=int, default=1)

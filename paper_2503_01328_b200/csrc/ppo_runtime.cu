@@ -159,6 +159,14 @@ static bool pack_use_bulk() {
 
 using namespace ppo;
 
+namespace {
+__global__ void timestamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+}  // namespace
+
 extern "C" {
 
 int ppo_abi_version(void) { return PPO_ABI_VERSION; }
@@ -227,6 +235,13 @@ int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_s
     PPO_TRY_CUDA(cudaMemcpyAsync(dst, src, segs[i].bytes, kind, s));
   }
   if (done_event) PPO_TRY_CUDA(cudaEventRecord(as_event(done_event), s));
+  return PPO_OK;
+}
+
+int ppo_timestamp(uint64_t* slot, void* stream) {
+  if (!slot) return set_error(PPO_EINVAL, "ppo_timestamp: null slot");
+  timestamp_kernel<<<1, 1, 0, as_stream(stream)>>>(reinterpret_cast<unsigned long long*>(slot));
+  PPO_LAUNCHED("timestamp_kernel");
   return PPO_OK;
 }
 

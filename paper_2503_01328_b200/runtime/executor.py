@@ -308,6 +308,15 @@ class RankRunner:
         self.iteration = 0
         self.tokens = None
         self.t0 = None
+        # whole-iteration CUDA graph (execute(iteration_graph=True)): while capturing,
+        # pass bodies run inline (no per-pass graphs) and pass boundaries are timed by
+        # stream-ordered global-timer writes (native.timestamp) into ``ts_buf`` instead of
+        # event records, whose host-visible semaphore writes stall behind saturated PCIe
+        self.capturing = False
+        self.graph_timed = False  # measured_passes reads ts_buf
+        self.pass_timing = True
+        self.ts_index = {}
+        self.ts_buf = None
 
     # -------------------------------------------------------------- plumbing
     def ev(self, key):
@@ -317,6 +326,19 @@ class RankRunner:
             e = torch.cuda.Event(enable_timing=timed)
             self.events[key] = e
         return e
+
+    def rec(self, key, stream):
+        """Record event ``key`` on ``stream`` (sync), plus its timing twin in graph mode."""
+        self.ev(key).record(stream)
+        if self.capturing and self.pass_timing and key[0] in TIMED:
+            self.timestamp(key, stream)
+
+    def timestamp(self, key, stream):
+        """Global-timer write for ``key`` into this runner's timestamp buffer."""
+        if self.ts_buf is None:
+            self.ts_buf = torch.zeros(2 * len(self.prog.ops) + 8, dtype=torch.int64, device=self.device)
+        i = self.ts_index.setdefault(key, len(self.ts_index))
+        native.timestamp(self.ts_buf.data_ptr() + 8 * i, stream)
 
     @property
     def act_bytes(self) -> int:
@@ -349,11 +371,22 @@ class RankRunner:
         return tuple(out)
 
     # ------------------------------------------------------------ iteration
-    def begin_iteration(self, tokens_dev: torch.Tensor | None):
-        """tokens_dev: [m, s+1] int64 already on this device (first/last stages use it)."""
+    def pre_iteration(self, stream):
+        """Per-iteration device state a captured iteration graph reads (on ``stream``,
+        outside any capture): the iteration part of the Philox offsets."""
+        with torch.cuda.stream(stream):
+            for st in self.stages.values():
+                st.set_iteration(self.iteration)
+
+    def begin_iteration(self, tokens_dev: torch.Tensor | None, timed: bool = True):
+        """tokens_dev: [m, s+1] int64 already on this device (first/last stages use it).
+        ``timed=False``: the iteration start event is recorded by the caller (around a
+        whole-iteration graph replay)."""
         self.cursor = 0
         self.tokens = tokens_dev
         comp = self.streams["compute"]
+        if timed:
+            self.pre_iteration(torch.cuda.current_stream(self.device))
         comp.wait_stream(torch.cuda.current_stream(self.device))
         for name, st in self.streams.items():
             if name != "compute":
@@ -361,8 +394,9 @@ class RankRunner:
         for st in self.stages.values():
             with torch.cuda.stream(comp):
                 st.zero_grad()
-        self.t0 = torch.cuda.Event(enable_timing=True)
-        self.t0.record(comp)
+        if timed:
+            self.t0 = torch.cuda.Event(enable_timing=True)
+            self.t0.record(comp)
 
     def done(self) -> bool:
         return self.cursor >= len(self.prog.ops)
@@ -377,7 +411,7 @@ class RankRunner:
             buf = self.rings["recv_act" if op.kind == "RECV_ACT" else "recv_grad"][op.ring]
             if not self.transport.recv(self.rank, op, buf, stream):
                 return False
-            self.ev(op.records[0]).record(stream)
+            self.rec(op.records[0], stream)
             self.cursor += 1
             return True
         for key in op.waits:
@@ -393,7 +427,7 @@ class RankRunner:
         elif op.kind in ("SEND_ACT", "SEND_GRAD"):
             buf = self.rings["send_act" if op.kind == "SEND_ACT" else "send_grad"][op.ring]
             self.transport.send(self.rank, op, buf, stream)
-            self.ev(op.records[0]).record(stream)
+            self.rec(op.records[0], stream)
         else:  # pragma: no cover
             raise ValueError(op.kind)
         self.cursor += 1
@@ -402,17 +436,17 @@ class RankRunner:
     def _forward(self, op, stream):
         s, j = op.stage, op.mb
         st = self.stages[s]
-        self.ev(("F_start", s, j)).record(stream)
+        self.rec(("F_start", s, j), stream)
         with torch.cuda.stream(stream):
             slab = self.slab(op, s)
-            st.set_pass_context(j, self.iteration, self.tokens[j])
+            st.set_pass_context(j, None, self.tokens[j])
             if st.first:
                 st.embed(slab)
             elif op.ring is not None:
                 slab.get(0, "x").copy_(self.rings["recv_act"][op.ring])
             else:  # emulated upstream stage
                 slab.get(0, "x").copy_(self.synthetic_x)
-            self.ev(("F_in", s, j)).record(stream)
+            self.rec(("F_in", s, j), stream)
             out = None
             if not st.last:
                 out = self.rings["send_act"][op.send_ring] if op.send_ring is not None else self.scratch_out
@@ -420,17 +454,17 @@ class RankRunner:
             self._run_body(key, lambda: st.forward_body(slab, out), stream)
             if self.verify_roundtrip and (s, j) in self.prog.offloaded:
                 self.digests[(s, j)] = [_digest(slab.base), None]
-        self.ev(("F_end", s, j)).record(stream)
+        self.rec(("F_end", s, j), stream)
 
     def _backward(self, op, stream):
         s, j = op.stage, op.mb
         st = self.stages[s]
-        self.ev(("B_start", s, j)).record(stream)
+        self.rec(("B_start", s, j), stream)
         with torch.cuda.stream(stream):
             slab = self.slab(op, s)
             if self.verify_roundtrip and (s, j) in self.prog.offloaded:
                 self.digests[(s, j)][1] = _digest(slab.base)
-            st.set_pass_context(j, self.iteration, self.tokens[j] if st.first else None)
+            st.set_pass_context(j, None, self.tokens[j] if st.first else None)
             dy = None
             if not st.last:
                 dy = self.rings["recv_grad"][op.ring] if op.ring is not None else self.synthetic_dy
@@ -441,17 +475,17 @@ class RankRunner:
             key = ("B", s, op.slab, self._rkey(op), dy.data_ptr() if dy is not None else 0, dx_out.data_ptr() if dx_out is not None else 0,
                    op.wbuf)
             self._run_body(key, lambda: st.backward_body(slab, dy, dx_out, wbuf), stream)
-        self.ev(("B_end", s, j)).record(stream)
+        self.rec(("B_end", s, j), stream)
 
     def _wgrad(self, op, stream):
         s, j = op.stage, op.mb
         st = self.stages[s]
-        self.ev(("W_start", s, j)).record(stream)
+        self.rec(("W_start", s, j), stream)
         with torch.cuda.stream(stream):
             slab = self.slab(op, s)
             wbuf = self.wbuf(op.wbuf, s)
             self._run_body(("W", s, op.slab, self._rkey(op), op.wbuf), lambda: st.wgrad_body(slab, wbuf), stream)
-        self.ev(("W_end", s, j)).record(stream)
+        self.rec(("W_end", s, j), stream)
 
     def wbuf(self, idx: int, stage: int) -> dict:
         """Split-backward gradient buffers of colour ``idx`` (shared by the rank's stages
@@ -468,7 +502,7 @@ class RankRunner:
         boundary buffer) key is eager and is then captured, later runs replay it.
         Capture uses the low-level begin/end API (no device synchronisation), so it is
         safe mid-iteration and across NCCL ranks."""
-        if not self.use_graphs:
+        if not self.use_graphs or self.capturing:
             body()
             return
         graph = self.graphs.get(key)
@@ -501,19 +535,20 @@ class RankRunner:
         slab_ptr = self.arena.data_ptr() + op.slab * self.off_bytes
         segs = lay.segments(slab_ptr, self.host_bins(op.host_slot, s))
         tag = "D2H" if op.kind == "OFFLOAD" else "H2D"
-        self.ev((tag + "_start", s, j)).record(stream)
+        self.rec((tag + "_start", s, j), stream)
         native.transfer(native.PPO_D2H if op.kind == "OFFLOAD" else native.PPO_H2D, segs, stream.cuda_stream)
-        self.ev((tag, s, j)).record(stream)
+        self.rec((tag, s, j), stream)
 
-    def end_iteration(self):
+    def end_iteration(self, timed: bool = True):
         comp = self.streams["compute"]
         for name, st in self.streams.items():
             if name != "compute":
                 comp.wait_stream(st)
         with torch.cuda.stream(comp):
             self._optimizer_step()
-        self.t_end = torch.cuda.Event(enable_timing=True)
-        self.t_end.record(comp)
+        if timed:
+            self.t_end = torch.cuda.Event(enable_timing=True)
+            self.t_end.record(comp)
         torch.cuda.current_stream(self.device).wait_stream(comp)
         self.iteration += 1
 
@@ -567,18 +602,25 @@ class RankRunner:
     # -------------------------------------------------------- measured trace
     def measured_passes(self) -> list[Pass]:
         """CUDA-event times (seconds from iteration start) of this rank's passes."""
-        t0 = self.t0
-        sec = lambda ev: Fraction(t0.elapsed_time(ev)) / 1000  # noqa: E731
+        if self.graph_timed:
+            ts = self.ts_buf.cpu().tolist()
+            base = ts[self.ts_index[("iter_start",)]]
+            evs = {k: ts[i] for k, i in self.ts_index.items()}
+            sec = lambda t: Fraction(t - base, 10**9)  # noqa: E731
+        else:
+            t0 = self.t0
+            sec = lambda ev: Fraction(t0.elapsed_time(ev)) / 1000  # noqa: E731
+            evs = self.events
         out = []
         for (kind, s, j) in self.prog.compute_order:
-            a, b = self.events[(f"{kind}_start", s, j)], self.events[(f"{kind}_end", s, j)]  # F, B or W
+            a, b = evs[(f"{kind}_start", s, j)], evs[(f"{kind}_end", s, j)]  # F, B or W
             st = sec(a)
             out.append(Pass(PassKind(kind), self.rank, s, j, st, sec(b) - st))
         for op in self.prog.ops:
             if op.kind in ("OFFLOAD", "RELOAD"):
                 tag = "D2H" if op.kind == "OFFLOAD" else "H2D"
-                st = sec(self.events[(tag + "_start", op.stage, op.mb)])
-                en = sec(self.events[(tag, op.stage, op.mb)])
+                st = sec(evs[(tag + "_start", op.stage, op.mb)])
+                en = sec(evs[(tag, op.stage, op.mb)])
                 out.append(Pass(PassKind(op.kind), self.rank, op.stage, op.mb, st, en - st))
         return out
 
@@ -660,6 +702,65 @@ def drive(runners: list[RankRunner]):
         if not progressed:
             stuck = [(r.rank, r.prog.ops[r.cursor].key) for r in runners if not r.done()]
             raise DeadlockError(f"virtual pipeline cannot make progress: {stuck}")
+
+
+def _capture_iteration(runners, tokens_dev, origin, dev, transport):
+    """Capture one whole iteration of every runner into a single CUDA graph on
+    ``origin``: each runner's streams fork from origin (begin_iteration) and join back
+    (end_iteration), so the lowered program's event waits become graph edges.
+    Returns (graph, native launches one replay runs, ABI call deltas)."""
+    graph = torch.cuda.CUDAGraph()
+    pool = torch.cuda.graph_pool_handle()
+    origin.wait_stream(torch.cuda.current_stream(dev))
+    before = native.kernel_launches()
+    snap = native.call_counts()
+    for r in runners:
+        if r.pass_timing and r.ts_buf is None:  # allocated outside the capture
+            r.ts_buf = torch.zeros(2 * len(r.prog.ops) + 8, dtype=torch.int64, device=r.device)
+    with torch.cuda.stream(origin):
+        for r in runners:
+            r.capturing = True
+        graph.capture_begin(pool=pool, capture_error_mode="thread_local")
+        try:
+            for r in runners:
+                if r.pass_timing:
+                    r.timestamp(("iter_start",), origin)
+                r.begin_iteration(tokens_dev, timed=False)
+            drive(runners)
+            for r in runners:
+                r.end_iteration(timed=False)
+        finally:
+            graph.capture_end()
+            for r in runners:
+                r.capturing = False
+                r.graph_timed = r.pass_timing
+    for r in runners:
+        r.iteration -= 1  # the capture ran nothing
+    if transport is not None:
+        transport.end_iteration()
+    launched = native.kernel_launches() - before
+    calls = native.since(snap)
+    native.credit(calls, -1)  # recorded, not executed: each replay credits them back
+    runners[0].graph_native_launches["iteration"] = launched
+    return graph, launched, calls
+
+
+def _replay_iteration(runners, captured, origin, dev):
+    graph, launched, calls = captured
+    origin.wait_stream(torch.cuda.current_stream(dev))
+    for r in runners:
+        r.pre_iteration(origin)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(origin):
+        t0.record(origin)
+        graph.replay()
+        t1.record(origin)
+    torch.cuda.current_stream(dev).wait_stream(origin)
+    for r in runners:
+        r.t0, r.t_end = t0, t1
+        r.iteration += 1
+    runners[0].replayed_native_launches += launched
+    native.credit(calls)
 
 
 def measured_trace(sched: Schedule, passes: list[Pass], model: ModelSpec | None = None,
@@ -748,7 +849,8 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
-            use_graphs: bool = True, gemm: str = "best", offload_tensors=None) -> RunResult:
+            use_graphs: bool = True, gemm: str = "best", offload_tensors=None,
+            iteration_graph: bool = False, pass_timing: bool = True) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
@@ -757,6 +859,12 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     ``tokens``: [m, s+1] int64 host tensor (pinned for the e2e path).
     ``offload_tensors``: None (an offloaded pair moves its whole saved set) or the
     (local layer, name) tensors that move (partial offload, ``layout.make_layout``).
+    ``iteration_graph``: after one eager iteration, capture a whole iteration -- every
+    stream, event edge, pass, D2H/H2D and the optimizer step -- into ONE CUDA graph and
+    replay it (modes "emulate" / "virtual"): no host issue and no per-launch command
+    fetch over the host link the copy engines are saturating.
+    ``pass_timing=False`` (graph mode): no per-pass timestamps inside the graph, only
+    the iteration's start/end -- the returned trace then has no passes.
 
     In the multi-process modes every iteration starts after a device synchronise
     and a barrier, and the returned iteration/wall times and losses are the same on
@@ -790,6 +898,14 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
     tokens_dev = torch.empty(tokens.shape, dtype=torch.int64, device=dev)
     secs, losses, walls, host_secs = [], [], [], []
+    whole = (iteration_graph and mode in ("emulate", "virtual") and not probe_kernels
+             and optimizer in ("none", "sgd") and warmup + iters > 1)
+    origin = torch.cuda.Stream(dev) if whole else None
+    graph = None
+    if whole:
+        for r in runners:
+            r.use_graphs = False  # iteration 0 runs eagerly; then the whole iteration is one graph
+            r.pass_timing = pass_timing
     torch.cuda.synchronize(dev)
     for it in range(warmup + iters):
         if dist_mode:
@@ -801,13 +917,20 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
                     st.probe = {}
         wall0 = time.perf_counter()
         tokens_dev.copy_(tokens, non_blocking=True)  # H2D of the step's inputs (pinned host)
-        for r in runners:
-            r.begin_iteration(tokens_dev)
-        host0 = time.perf_counter()
-        drive(runners)
-        host_issue = time.perf_counter() - host0
-        for r in runners:
-            r.end_iteration()
+        if whole and it >= 1:
+            if graph is None:
+                graph = _capture_iteration(runners, tokens_dev, origin, dev, transport)
+            host0 = time.perf_counter()
+            _replay_iteration(runners, graph, origin, dev)
+            host_issue = time.perf_counter() - host0
+        else:
+            for r in runners:
+                r.begin_iteration(tokens_dev)
+            host0 = time.perf_counter()
+            drive(runners)
+            host_issue = time.perf_counter() - host0
+            for r in runners:
+                r.end_iteration()
         result = [r.result_scalar() for r in runners]
         values = [float(x) for x in result]  # D2H read of the step's result (syncs)
         wall = time.perf_counter() - wall0
@@ -825,7 +948,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             host_secs.append(host_issue)
             secs.append(sec)
             losses.append(loss)
-    passes = [p for r in runners for p in r.measured_passes()]
+    passes = [p for r in runners for p in r.measured_passes()] if (pass_timing or not whole) else []
     slab_bytes = max(r.slab_bytes for r in runners)
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
     return RunResult(trace, secs, losses, programs, runners, slab_bytes,

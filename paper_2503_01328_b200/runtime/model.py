@@ -176,6 +176,9 @@ class Stage:
         # Per-pass context in device memory, so a captured pass (CUDA graph) serves every
         # microbatch: ctx[0] = Philox offset base of (iteration, mb); tok = token row.
         self.ctx = torch.zeros(1, device=self.device, dtype=torch.int64)
+        # (iteration) part of ctx, device-resident so a captured whole-iteration graph
+        # replays with the current iteration's Philox offsets (set_iteration, outside it)
+        self.iter_base = torch.zeros(1, device=self.device, dtype=torch.int64)
         self.tok = torch.zeros(cfg.seq + 1, device=self.device, dtype=torch.int64)
         self._attn_meta = None
         self.probe = None  # kernel name -> [bytes_per_launch, [(start_event, end_event), ...]]
@@ -268,9 +271,17 @@ class Stage:
         base = l_global * self.m * 2
         return base, base + 1
 
-    def set_pass_context(self, mb: int, iteration: int, tokens: torch.Tensor | None = None):
-        """Stream-ordered update of the per-pass device context (eager, never captured)."""
-        self.ctx.fill_(iteration * self.cfg.n_layers * self.m * 2 + mb * 2)
+    def set_iteration(self, iteration: int):
+        """Stream-ordered: the iteration part of every pass context (never captured)."""
+        self.iter_base.fill_(iteration * self.cfg.n_layers * self.m * 2)
+
+    def set_pass_context(self, mb: int, iteration: int | None = None, tokens: torch.Tensor | None = None):
+        """Stream-ordered update of the per-pass device context: ctx = iter_base + 2 mb.
+        Graph-safe (mb is static per pass; the iteration comes from ``iter_base``);
+        passing ``iteration`` also sets ``iter_base`` (eager single-pass use)."""
+        if iteration is not None:
+            self.set_iteration(iteration)
+        torch.add(self.iter_base, mb * 2, out=self.ctx)
         if tokens is not None:
             self.tok.copy_(tokens, non_blocking=True)
 

@@ -58,6 +58,7 @@ _FP = ctypes.POINTER(ctypes.c_float)
 SIGNATURES = {
     "ppo_abi_version": [],
     "ppo_last_error": [],
+    "ppo_timestamp": [_VP, _VP],
     "ppo_kernel_launches": [],
     "ppo_device_info": [_I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
     "ppo_pool_create": [_U64, ctypes.POINTER(_VP)],
@@ -111,7 +112,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 5:
+        if lib.ppo_abi_version() != 6:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -333,6 +334,11 @@ def transfer(direction, segments, copy_stream, wait_event=None, done_event=None)
     for i, (d, h, n) in enumerate(segments):
         arr[i] = Segment(d, h, n)
     call("ppo_transfer", direction, arr, len(segments), copy_stream, wait_event, done_event)
+
+
+def timestamp(slot_ptr: int, stream) -> None:
+    """Stream-ordered GPU global-timer write (ns, uint64) to device address slot_ptr."""
+    call("ppo_timestamp", slot_ptr, stream.cuda_stream)
 
 
 class PinnedPool:

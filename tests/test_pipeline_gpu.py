@@ -224,3 +224,30 @@ def test_c1_partial_offload_matches_oracle(oracle_result, tensors):
     got = _grads(res)
     for k, g in want_grads.items():
         assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
+
+
+@pytest.mark.parametrize("mode,stream_mode", [("virtual", "single"), ("emulate", "dual")])
+def test_whole_iteration_graph(oracle_result, mode, stream_mode):
+    """execute(iteration_graph=True): one CUDA graph per iteration (every stream, event
+    edge, pass, D2H/H2D and the SGD step) replays with the same results as the per-pass
+    issue path: bit-exact round trips, same losses over 3 SGD steps (to the LN-bwd
+    atomics' nondeterminism), every pass timed from inside the graph."""
+    tokens, _, _ = oracle_result
+    U = po.PassCosts.unit()
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    kw = dict(model=CFG, mode=mode, rank=0, tokens=tokens, optimizer="sgd", lr=1e-2, iters=3, warmup=1,
+              stream_mode=stream_mode, verify_roundtrip=True)
+    ref = ex.execute(sched, plan, **kw)
+    got = ex.execute(sched, plan, iteration_graph=True, **kw)
+    assert "iteration" in got.runners[0].graph_native_launches
+    assert ex.roundtrip_mismatches(got.runners) == []
+    if mode == "virtual":
+        for a, b in zip(got.losses, ref.losses):
+            assert abs(a - b) < 1e-3 * abs(b), (got.losses, ref.losses)
+        assert got.losses[-1] < got.losses[0]  # SGD steps inside the graph take effect
+    n_passes = sum(len(p.compute_order) for p in got.programs.values())
+    assert len(got.trace.compute_passes()) == n_passes
+    assert all(p.duration > 0 for p in got.trace.passes)
+    assert 0 < got.iteration_seconds[-1] < 10
+    got.close()
+    ref.close()
