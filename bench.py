@@ -415,7 +415,7 @@ def run_b200(args, rank, world, local_rank):
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
                       stream_mode="single" if name in ("none", "none_cublas", "auto", "full_single") else "dual",
-                      gemm="cublas" if name == "none_cublas" else "best", iteration_graph=args.iteration_graph)
+                      gemm="cublas" if name == "none_cublas" else "auto", iteration_graph=args.iteration_graph)
         # real launches = eager launches + kernels executed by graph replays
         # (launch calls made while capturing a graph record nodes, they do not run)
         replayed = sum(r.replayed_native_launches for r in res.runners)
@@ -532,6 +532,7 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": world * full["e2e_tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": m * (s + 1) * 8,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": launches.get("full"),
+        "gemm_backend": gemm_decisions(),
         "clocks": clocks,
         "roofline": roofline,
         "kernels": {k: {"bound": v["bound"], "avg_us": round(v["avg_us"], 2), "achieved": round(v["achieved"], 1),
@@ -580,6 +581,14 @@ def run_b200(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def gemm_decisions():
+    """Per layer-GEMM shape: libppo_b200 tcgen05 vs cuBLAS device time as measured by
+    the gemm="auto" tuner (runtime/gemm_tune.py), and the backend it picked."""
+    from paper_2503_01328_b200.runtime import gemm_tune
+
+    return gemm_tune.decisions()
 
 
 def cpu_baseline(args):

@@ -244,7 +244,7 @@ class RankRunner:
 
     def __init__(self, program: Program, cfg: ModelConfig, sched: Schedule, microbatches: int, device,
                  transport=None, emulate: bool = False, params=None, seed: int = 1234, optimizer: str = "sgd",
-                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "best",
+                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "auto",
                  offload_tensors=None):
         torch_ = native.require_cuda()
         self.torch = torch_
@@ -849,7 +849,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
-            use_graphs: bool = True, gemm: str = "best", offload_tensors=None,
+            use_graphs: bool = True, gemm: str = "auto", offload_tensors=None,
             iteration_graph: bool = False, pass_timing: bool = True) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 

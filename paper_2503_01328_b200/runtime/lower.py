@@ -93,23 +93,28 @@ def _colour(intervals):
     """Greedy interval colouring. intervals: list of (start, end, key).
 
     Frees sort before allocations at equal times (half-open residency, as in
-    ir.py:649).  Returns (assignment key -> (colour, previous occupant key or
-    None), n_colours).
+    ir.py:649).  A new interval takes the colour that has been free the longest
+    (LRU), so the release event it waits on is as old as possible: on the GPU the
+    compute stream can run ahead of the witness timeline (an emulated rank has no
+    pipeline bubbles) and a just-freed slab would stall it.  Greedy colouring uses
+    max-overlap colours whatever free colour it picks.  Returns (assignment key ->
+    (colour, previous occupant key or None), n_colours).
     """
     events = []
     for start, end, key in intervals:
         events.append((start, 1, key))
         events.append((end, 0, key))
     events.sort(key=lambda e: (e[0], e[1]))
-    free: list = []  # heap of colour ids
+    free: list = []  # heap of (release order, colour)
     last_holder: dict = {}
     held: dict = {}
     assignment = {}
     n = 0
+    order = 0
     for _t, is_alloc, key in events:
         if is_alloc:
             if free:
-                c = heapq.heappop(free)
+                _, c = heapq.heappop(free)
             else:
                 c = n
                 n += 1
@@ -118,7 +123,8 @@ def _colour(intervals):
         else:
             c = held.pop(key)
             last_holder[c] = key
-            heapq.heappush(free, c)
+            heapq.heappush(free, (order, c))
+            order += 1
     return assignment, n
 
 

@@ -9,9 +9,10 @@ LayerNorm, GeLU and both dropout masks (K3-K5, ``libppo_b200.so``) and never
 needs anything that was not saved -- the recompute scheme of PAPER.md:439 that
 turns the reference's 34bsh coefficient into 20bsh (costs.py:1-7,18-20).
 
-Dense GEMMs run on libppo_b200's tcgen05 kernels (``gemm="best"``, the default, uses
-them for every shape where they match or beat cuBLAS -- see profiles/r1_gemm_tuning.txt):
-fc1 fuses the GeLU into its epilogue (writes f into the slab and g for fc2), the
+Dense GEMMs run on libppo_b200's tcgen05 kernels or cuBLAS, per shape whichever the
+device measured faster (``gemm="auto"``, the default, runtime/gemm_tune.py);
+``gemm="best"`` is the static round-1 rule (ours except narrow-N / deep-K shapes,
+profiles/r1_gemm_tuning.txt).  fc1 fuses the GeLU into its epilogue (writes f into the slab and g for fc2), the
 fc2 activation-gradient GEMM fuses the GeLU backward (df = (dm @ Wfc2) * gelu'(f)),
 weight gradients accumulate in fp32 inside the GEMM epilogue.  ``gemm="cublas"``
 keeps the library GEMMs as the comparison baseline.  Causal attention runs on
@@ -27,6 +28,7 @@ from dataclasses import dataclass
 import torch
 
 from . import native
+from . import gemm_tune
 from .layout import SlabLayout, make_layout
 
 
@@ -132,9 +134,9 @@ class Stage:
     """Parameters, gradients, workspace and the F/B passes of one pipeline stage."""
 
     def __init__(self, cfg: ModelConfig, stage: int, num_stages: int, microbatches: int, device, params=None,
-                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "best", offload=None):
+                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "auto", offload=None):
         native.require_cuda()
-        if gemm not in ("best", "tcgen05", "cublas"):
+        if gemm not in ("auto", "best", "tcgen05", "cublas"):
             raise ValueError(f"gemm backend {gemm!r}")
         # "tcgen05": every GEMM on libppo_b200's kernels (fused GeLU epilogues); "cublas": the
         # library baseline; "best": ours except narrow-N / deep-K shapes (N <= 2048, K >= 3N)
@@ -202,20 +204,45 @@ class Stage:
 
     # ------------------------------------------------------------------ GEMMs
     def _ours(self, n: int, k: int) -> bool:
+        """Static rule of gemm="best": ours except narrow-N / deep-K (N <= 2048, K >= 3N)."""
         if self.gemm == "best":
             return not (n <= 2048 and k >= 3 * n)
-        return self.gemm == "tcgen05"
+        return self.gemm in ("tcgen05", "auto")
+
+    def _tuned(self, kind: str, shape: tuple, make) -> bool:
+        """gemm="auto": the measured faster backend for (kind, shape) (runtime/gemm_tune.py)."""
+        if self.gemm != "auto":
+            return self.gemm != "cublas" and (kind not in ("tn", "nn", "nn_acc") or self._ours(shape[1], shape[2]))
+        return gemm_tune.prefer_ours(kind, shape, self.device, make, fallback=True)
+
+    def _rand(self, *shape, dtype=torch.bfloat16):
+        return torch.randn(*shape, device=self.device, dtype=torch.float32).to(dtype) * 0.1
 
     def mm_fwd(self, a, w, out):
         """out = a @ w^T (nn.Linear forward; w is [out, in])."""
-        if self._ours(w.shape[0], w.shape[1]):
+        M, (N, K) = a.shape[0], w.shape
+
+        def make():
+            a_, w_, o_ = self._rand(M, K), self._rand(N, K), torch.empty(M, N, device=self.device, dtype=torch.bfloat16)
+            return (lambda: native.gemm_tn(a_, w_, o_)), (lambda: torch.mm(a_, w_.t(), out=o_))
+
+        if self._tuned("tn", (M, N, K), make):
             native.gemm_tn(a, w, out)
         else:
             torch.mm(a, w.t(), out=out)
 
     def mm_fc1_gelu(self, a, w, f_out, g_out):
         """f = a @ w^T (saved GeLU input) and g = gelu(f) (fc2 operand)."""
-        if self.gemm != "cublas":
+        M, (N, K) = a.shape[0], w.shape
+
+        def make():
+            a_, w_ = self._rand(M, K), self._rand(N, K)
+            f_, g_ = (torch.empty(M, N, device=self.device, dtype=torch.bfloat16) for _ in range(2))
+            zb = self.zero_bias[:N]
+            return ((lambda: native.gemm_tn_gelu(a_, w_, g_, f_, zb)),
+                    (lambda: (torch.mm(a_, w_.t(), out=f_), native.gelu_fwd(f_, g_))))
+
+        if self._tuned("tn_gelu", (M, N, K), make):
             native.gemm_tn_gelu(a, w, g_out, f_out, self.zero_bias[: w.shape[0]])
         else:
             torch.mm(a, w.t(), out=f_out)
@@ -223,7 +250,15 @@ class Stage:
 
     def mm_dgrad(self, dy, w, out, accumulate: bool = False):
         """out (+)= dy @ w (activation gradient of nn.Linear)."""
-        if self._ours(w.shape[1], w.shape[0]):
+        M, (K, N) = dy.shape[0], w.shape
+
+        def make():
+            d_, w_, o_ = self._rand(M, K), self._rand(K, N), torch.zeros(M, N, device=self.device, dtype=torch.bfloat16)
+            beta = 1.0 if accumulate else 0.0
+            return ((lambda: native.gemm_nn(d_, w_, o_, beta)),
+                    (lambda: torch.addmm(o_, d_, w_, out=o_) if accumulate else torch.mm(d_, w_, out=o_)))
+
+        if self._tuned("nn_acc" if accumulate else "nn", (M, N, K), make):
             native.gemm_nn(dy, w, out, 1.0 if accumulate else 0.0)
         elif accumulate:
             torch.addmm(out, dy, w, out=out)
@@ -236,8 +271,16 @@ class Stage:
         When g is needed (unsplit backward) the plain dgrad GEMM + one gelu_bwd pass
         (reads f and dg once, writes df and g) is cheaper; when it is not (split
         backward: the W pass recomputes g) the GeLU backward rides in the GEMM
-        epilogue (``gemm_nn_dgelu``)."""
-        if g_out is None and self.gemm != "cublas":
+        epilogue (``gemm_nn_dgelu``) unless the tuner measured GEMM + gelu_bwd faster."""
+        M, (K, N) = dm.shape[0], w.shape
+
+        def make():
+            d_, w_, f_ = self._rand(M, K), self._rand(K, N), self._rand(M, N)
+            o_ = torch.empty(M, N, device=self.device, dtype=torch.bfloat16)
+            return ((lambda: native.gemm_nn_dgelu(d_, w_, f_, o_)),
+                    (lambda: (self.mm_dgrad(d_, w_, o_), native.gelu_bwd(f_, o_, None, o_))))
+
+        if g_out is None and self.gemm != "cublas" and self._tuned("nn_dgelu", (M, N, K), make):
             native.gemm_nn_dgelu(dm, w, f, df_out)
             return
         self.mm_dgrad(dm, w, df_out)
@@ -245,7 +288,14 @@ class Stage:
 
     def wgrad(self, acc, dy, x):
         """acc (fp32, [out, in]) += dy^T @ x with dy [tokens, out], x [tokens, in]."""
-        if self.gemm != "cublas":
+        T, (O, I) = dy.shape[0], acc.shape
+
+        def make():
+            d_, x_ = self._rand(T, O), self._rand(T, I)
+            a_ = torch.zeros(O, I, device=self.device, dtype=torch.float32)
+            return (lambda: native.gemm_wgrad(d_, x_, a_, 1.0)), (lambda: _wgrad(a_, d_.t(), x_))
+
+        if self._tuned("wgrad", (O, I, T), make):
             native.gemm_wgrad(dy, x, acc, 1.0)
         else:
             _wgrad(acc, dy.t(), x)
