@@ -193,6 +193,17 @@ int ppo_gemm_nn_dgelu(const void* A, const void* B, const void* Z, void* D, int6
 int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t N, int64_t K, float beta,
                    void* stream);
 
+/* Tile-scheduler rasterisation swizzle (1, 2, 4, 8, 16; 0 = default 1) used by GEMM entry
+ * point `op` (PPO_GEMM_OP_*) for problems of exactly M x N x K: consecutive persistent
+ * CTAs walk bands of `swizzle` tiles so they share A rows / B columns in L2.  Set by
+ * the host's per-shape tuner before capture; read at launch. */
+#define PPO_GEMM_OP_TN 0
+#define PPO_GEMM_OP_TN_GELU 1
+#define PPO_GEMM_OP_NN 2
+#define PPO_GEMM_OP_NN_DGELU 3
+#define PPO_GEMM_OP_WGRAD 4
+int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
+
 /* ----------------------------------------------- K8: stage-boundary send/recv */
 /* NCCL communicator of the pipeline (one rank per GPU).  The 128-byte unique id is
  * produced by rank 0 with ppo_comm_unique_id and broadcast by the host runtime

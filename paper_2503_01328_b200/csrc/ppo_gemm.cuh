@@ -6,6 +6,7 @@
 #include "ppo_common.cuh"
 
 #include <cute/tensor.hpp>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -91,9 +92,32 @@ inline void* workspace(void* stream, size_t bytes, int* rc) {
   return b.first;
 }
 
+// CTA rasterisation swizzle of the persistent tile scheduler: tiles are visited in
+// bands of `swizzle` tiles so consecutive CTAs share A rows / B columns in L2 (126 MB).
+// Per (entry point, M, N, K) as set by ppo_gemm_set_swizzle (the host tuner measures
+// 1/2/4/8 per shape: large h=5120 shapes gain up to 20%, C2 shapes want 1);
+// PPO_GEMM_SWIZZLE overrides everything for A/B runs.
+using ShapeKey = std::tuple<int, int64_t, int64_t, int64_t>;
+inline std::mutex& swizzle_mu() {
+  static std::mutex mu;
+  return mu;
+}
+inline std::map<ShapeKey, int>& swizzle_table() {
+  static std::map<ShapeKey, int> table;
+  return table;
+}
+inline int swizzle_for(int op, int64_t M, int64_t N, int64_t K) {
+  if (const char* e = std::getenv("PPO_GEMM_SWIZZLE")) return std::atoi(e);
+  std::lock_guard<std::mutex> lock(swizzle_mu());
+  auto it = swizzle_table().find(ShapeKey{op, M, N, K});
+  return it == swizzle_table().end() ? 1 : it->second;
+}
+
 template <class G>
-int launch(typename G::Args& args, void* stream, const char* who) {
+int launch(int op, typename G::Args& args, void* stream, const char* who) {
   typename G::Gemm gemm;
+  args.scheduler.max_swizzle_size = swizzle_for(op, cute::get<0>(args.problem_shape), cute::get<1>(args.problem_shape),
+                                                cute::get<2>(args.problem_shape));
   cutlass::Status st = gemm.can_implement(args);
   if (st != cutlass::Status::kSuccess)
     return set_error(PPO_ESHAPE, "%s: cannot implement (%s)", who, cutlassGetStatusString(st));

@@ -25,7 +25,7 @@ int nn_plain(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_
                         hw_info()};
   args.epilogue.thread.alpha = 1.f;
   args.epilogue.thread.beta = beta;
-  return launch<G>(args, stream, "ppo_gemm_nn");
+  return launch<G>(PPO_GEMM_OP_NN, args, stream, "ppo_gemm_nn");
 }
 }  // namespace
 
@@ -52,7 +52,7 @@ int ppo_gemm_nn_dgelu(const void* A, const void* B, const void* Z, void* D, int6
   fusion.beta = 0.f;
   fusion.aux_ptr = static_cast<const bf16*>(Z);
   fusion.dAux = sd;
-  return launch<G>(args, stream, "ppo_gemm_nn_dgelu");
+  return launch<G>(PPO_GEMM_OP_NN_DGELU, args, stream, "ppo_gemm_nn_dgelu");
 }
 
 }  // extern "C"

@@ -26,7 +26,7 @@ int tn_plain(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_
                         hw_info()};
   args.epilogue.thread.alpha = 1.f;
   args.epilogue.thread.beta = 0.f;
-  return launch<G>(args, stream, "ppo_gemm_tn");
+  return launch<G>(PPO_GEMM_OP_TN, args, stream, "ppo_gemm_tn");
 }
 }  // namespace
 
@@ -54,7 +54,7 @@ int ppo_gemm_tn_gelu(const void* A, const void* B, void* G_out, void* F_out, con
   fusion.bias_ptr = zero_bias;
   fusion.aux_ptr = static_cast<bf16*>(F_out);
   fusion.dAux = sd;
-  return launch<G>(args, stream, "ppo_gemm_tn_gelu");
+  return launch<G>(PPO_GEMM_OP_TN_GELU, args, stream, "ppo_gemm_tn_gelu");
 }
 
 }  // extern "C"

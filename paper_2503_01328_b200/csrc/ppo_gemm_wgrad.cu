@@ -26,7 +26,15 @@ int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t 
                         hw_info()};
   args.epilogue.thread.alpha = 1.f;
   args.epilogue.thread.beta = beta;
-  return launch<G>(args, stream, "ppo_gemm_wgrad");
+  return launch<G>(PPO_GEMM_OP_WGRAD, args, stream, "ppo_gemm_wgrad");
 }
 
 }  // extern "C"
+
+extern "C" int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle) {
+  if (op < PPO_GEMM_OP_TN || op > PPO_GEMM_OP_WGRAD || swizzle < 0 || swizzle > 16 || (swizzle & (swizzle - 1)))
+    return set_error(PPO_EINVAL, "ppo_gemm_set_swizzle: op=%d swizzle=%d", op, swizzle);
+  std::lock_guard<std::mutex> lock(ppo::gemm::swizzle_mu());
+  ppo::gemm::swizzle_table()[ppo::gemm::ShapeKey{op, M, N, K}] = swizzle ? swizzle : 1;
+  return PPO_OK;
+}

@@ -59,6 +59,7 @@ SIGNATURES = {
     "ppo_abi_version": [],
     "ppo_last_error": [],
     "ppo_timestamp": [_VP, _VP],
+    "ppo_gemm_set_swizzle": [_I32, _I64, _I64, _I64, _I32],
     "ppo_kernel_launches": [],
     "ppo_device_info": [_I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
     "ppo_pool_create": [_U64, ctypes.POINTER(_VP)],
@@ -334,6 +335,14 @@ def transfer(direction, segments, copy_stream, wait_event=None, done_event=None)
     for i, (d, h, n) in enumerate(segments):
         arr[i] = Segment(d, h, n)
     call("ppo_transfer", direction, arr, len(segments), copy_stream, wait_event, done_event)
+
+
+GEMM_OPS = {"tn": 0, "tn_gelu": 1, "nn": 2, "nn_acc": 2, "nn_dgelu": 3, "wgrad": 4}
+
+
+def gemm_set_swizzle(kind: str, M: int, N: int, K: int, swizzle: int) -> None:
+    """Tile-scheduler swizzle for libppo_b200 GEMM ``kind`` at M x N x K (tuner hook)."""
+    call("ppo_gemm_set_swizzle", GEMM_OPS[kind], M, N, K, swizzle)
 
 
 def timestamp(slot_ptr: int, stream) -> None:

@@ -78,3 +78,16 @@ def test_partial_planner_c2_shape():
     assert best.res_peak == 8  # rank 0 of PP=8 1F1B holds 8 microbatches
     tr = simulate(sched, best.plan, stream_mode=best.stream_mode)
     assert tr.memory.peak(0) == best.off_peak
+
+
+def test_bench_partial_candidates_distinct():
+    """bench.py measures at most `top` partial plans, one per tensor set, least memory first."""
+    import bench
+
+    costs = po.measured_pass_costs(1.28e-3, 2.78e-3)
+    sched = po.build_1f1b(8, 3, 32, costs)
+    out = bench.partial_candidates(sched, Fraction(18227, 10**6), 3, 4096, 2048, 16, top=3)
+    assert 1 <= len(out) <= 3
+    assert len({c.label for c in out}) == len(out)
+    assert [c.act_bytes for c in out] == sorted(c.act_bytes for c in out)
+    assert all(c.overhead <= 0.05 and not c.plan.late_list() for c in out)

@@ -23,7 +23,8 @@ import torch  # noqa: E402
 
 from paper_2503_01328_b200.runtime.calibrate import calibrate  # noqa: E402
 from paper_2503_01328_b200 import build_1f1b, measured_pass_costs, plan_slots  # noqa: E402
-from paper_2503_01328_b200.policy import choose_offload  # noqa: E402
+from paper_2503_01328_b200.policy import choose_offload, choose_partial_offload  # noqa: E402
+from paper_2503_01328_b200.runtime.layout import make_layout, offload_candidates  # noqa: E402
 from paper_2503_01328_b200.runtime import native  # noqa: E402
 from paper_2503_01328_b200.runtime.executor import execute  # noqa: E402
 from paper_2503_01328_b200.runtime.model import ModelConfig, Stage  # noqa: E402
@@ -43,24 +44,34 @@ def run_point(h, s, m, d, iters, warmup, dev):
     out = {"h": h, "s": s, "m": m, "k_measured": k, "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3,
            "T_o_ms": float(t_o) * 1e3, "d2h_gbs": cal["d2h_gbs"], "h2d_gbs": cal["h2d_gbs"]}
     choice = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
-    plans = {"none": None, "full": plan_slots(sched, (0,), t_o), "auto": choice.plan}
-    for name, plan in plans.items():
+    order = offload_candidates(1)
+    cands = []
+    for j in range(1, len(order)):
+        lay = make_layout(1, s, h, heads, offload=order[:j])
+        cands.append(("+".join(f"{n}{l}" for l, n in order[:j]), tuple(order[:j]), lay.off_bytes, lay.res_bytes))
+    part = choose_partial_offload(sched, (0,), t_o, cands, rank=0, tolerance=0.05, max_stride=2)
+    plans = {"none": (None, "single", None), "full": (plan_slots(sched, (0,), t_o), "single", None),
+             "auto": (choice.plan, "single", None)}
+    if part:
+        plans["partial"] = (part[0].plan, part[0].stream_mode, part[0].tensors)
+        out["partial_tensors"] = part[0].label
+    for name, (plan, sm, tensors) in plans.items():
         if plan is None and name != "none":
             out[name] = dict(out["none"], note="nothing offloadable within tolerance")
             continue
         res = execute(sched, plan, model=cfg, mode="emulate", rank=0, device=dev, iters=iters, warmup=warmup,
-                      optimizer="sgd")
+                      optimizer="sgd", stream_mode=sm, offload_tensors=tensors, iteration_graph=True)
         it = statistics.median(res.iteration_seconds)
         prog = res.programs[0]
         out[name] = {"tokens_per_s": m * s / it, "ms_per_step": it * 1e3, "peak_slabs": prog.n_slabs,
-                     "peak_act_gb": prog.n_slabs * res.slab_bytes / 1e9, "offloaded": len(prog.offloaded),
+                     "peak_act_gb": res.act_bytes[0] / 1e9, "offloaded": len(prog.offloaded),
                      "late": len(plan.late_list()) if plan is not None else 0}
         res.close()
         del res
         gc.collect()
         torch.cuda.empty_cache()
     base = out["none"]["tokens_per_s"]
-    for name in ("full", "auto"):
+    for name in [n for n in ("full", "auto", "partial") if n in out]:
         out[name]["overhead_pct"] = 100 * (base / out[name]["tokens_per_s"] - 1)
     out["auto_stride"] = choice.stride
     return out
