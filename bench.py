@@ -236,11 +236,13 @@ def _graph_time_us(fn_sets, dev, torch, launches=16):
 
 
 GEMM_NAMES = {"ppo_gemm_tn": "gemm_tn", "ppo_gemm_tn_gelu": "gemm_tn_gelu", "ppo_gemm_nn": "gemm_nn",
-              "ppo_gemm_nn_dgelu": "gemm_nn_dgelu", "ppo_gemm_wgrad": "gemm_wgrad"}
+              "ppo_gemm_nn_dgelu": "gemm_nn_dgelu", "ppo_gemm_wgrad": "gemm_wgrad", "ppo_attn_fwd": "attn_fwd"}
 
 
 def measure_gemms(shapes, dev, torch, native, sets=2):
-    """Device time per launch of each tcgen05 GEMM (entry, M, N, K) the step ran."""
+    """Device time per launch of each tcgen05 GEMM (entry, M, N, K) and attention forward
+    (entry, s, heads, head_dim) the step ran.  Attention FLOPs are causal-effective:
+    QK^T and PV over the lower triangle, 2 * 2 * s^2/2 * head_dim per head = 2 s^2 h."""
     bf = dict(device=dev, dtype=torch.bfloat16)
     out = {}
     for (entry, M, N, K) in sorted(shapes):
@@ -262,10 +264,15 @@ def measure_gemms(shapes, dev, torch, native, sets=2):
             elif entry == "ppo_gemm_wgrad":
                 dy, x, dw = torch.randn(K, M, **bf), torch.randn(K, N, **bf), torch.zeros(M, N, device=dev)
                 fns.append(lambda dy=dy, x=x, dw=dw: native.gemm_wgrad(dy, x, dw, 1.0))
-            else:
-                continue
+            elif entry == "ppo_attn_fwd":  # (s, heads, head_dim)
+                qkv, o = torch.randn(M, 3 * N * K, **bf), torch.empty(M, N * K, **bf)
+                lse = torch.empty(N, M, device=dev)
+                fns.append(lambda qkv=qkv, o=o, lse=lse, H=N: native.attn_fwd(qkv, o, lse, H))
+        if not fns:
+            continue
         name = f"{GEMM_NAMES[entry]}_{M}x{N}x{K}"
-        out[name] = {"entry": entry, "shape": (M, N, K), "flops_per_launch": 2 * M * N * K,
+        flops = 2 * M * M * N * K if entry == "ppo_attn_fwd" else 2 * M * N * K
+        out[name] = {"entry": entry, "shape": (M, N, K), "flops_per_launch": flops,
                      "avg_us": _graph_time_us(fns, dev, torch)}
         del fns
         torch.cuda.empty_cache()
@@ -402,8 +409,8 @@ def run_b200(args, rank, world, local_rank):
     launches = {}
     clocks = None
     backend = "auto"  # GEMM backend of every policy after the two no-offload runs: the faster one end to end
-    for name in ("none", "none_cublas", "auto", "full", "full_single", "full_duplex"):
-        plan = plans["full" if name == "full_single" else ("none" if name == "none_cublas" else name)]
+    for name in ("none", "none_cublas", "none_tcgen05_attn", "auto", "full", "full_single", "full_duplex"):
+        plan = plans["full" if name == "full_single" else ("none" if name.startswith("none") else name)]
         if name == "auto" and results["none_cublas"]["tokens_per_s"] > results["none"]["tokens_per_s"]:
             backend = "cublas"
         if name == "auto" and plan is None:
@@ -418,8 +425,10 @@ def run_b200(args, rank, world, local_rank):
         native.SHAPES.clear()
         res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps,
                       warmup=args.warmup, tokens=tokens, optimizer="sgd",
-                      stream_mode="single" if name in ("none", "none_cublas", "auto", "full_single") else "dual",
+                      stream_mode="single" if name in ("none", "none_cublas", "none_tcgen05_attn", "auto",
+                                                       "full_single") else "dual",
                       gemm="cublas" if name == "none_cublas" else (backend if name != "none" else "auto"),
+                      attn="tcgen05" if name == "none_tcgen05_attn" else "auto",
                       iteration_graph=args.iteration_graph)
         # real launches = eager launches + kernels executed by graph replays
         # (launch calls made while capturing a graph record nodes, they do not run)
@@ -543,6 +552,8 @@ def run_b200(args, rank, world, local_rank):
         "gemm_backend": {"policies": "tcgen05/cuBLAS per shape (gemm=auto)" if backend == "auto"
                          else "cuBLAS (faster end to end than gemm=auto in this run)",
                          "per_shape": gemm_decisions()},
+        "attn_backend": {"policies": "attention forward: tcgen05 (ours) or cuDNN + K1 pack, measured per shape "
+                                     "(attn=auto); backward: cuDNN", "per_shape": attn_decisions()},
         "clocks": clocks,
         "roofline": roofline,
         "kernels": {k: {"bound": v["bound"], "avg_us": round(v["avg_us"], 2), "achieved": round(v["achieved"], 1),
@@ -558,6 +569,7 @@ def run_b200(args, rank, world, local_rank):
             "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3, "T_o_ms": float(t_o) * 1e3,
             "slab_bytes": slab_bytes,
             "no_offload": none, "no_offload_auto_gemms": results["none"], "no_offload_cublas_gemms": none_cublas,
+            "no_offload_tcgen05_attention_fwd": results["none_tcgen05_attn"],
             "full": full, "auto": auto,
             "full_single_stream": single, "full_duplex_plan": duplex,
             "auto_stride": choice.stride, "auto_modelled_overhead": choice.overhead,
@@ -592,6 +604,12 @@ def run_b200(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def attn_decisions():
+    from paper_2503_01328_b200.runtime import gemm_tune
+
+    return gemm_tune.attn_decisions()
 
 
 def gemm_decisions():

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 6
+#define PPO_ABI_VERSION 7
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -203,6 +203,18 @@ int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t 
 #define PPO_GEMM_OP_NN_DGELU 3
 #define PPO_GEMM_OP_WGRAD 4
 int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
+
+/* ------------------------------------------------ K7: causal attention forward */
+/* Replaces the attention core priced by the reference's FLOP model (costs.py:144-161,
+ * 12bs^2h per layer of the 12bsh(6h+s)).  One microbatch (b = 1), causal, MHA,
+ * head_dim 128, seq a multiple of 256: from qkv[s, 3, heads, head_dim] (bf16, the QKV
+ * GEMM's output) writes o[s, heads*head_dim] (bf16) and lse[heads, s] (fp32, natural
+ * log of the row softmax denominators of scale*QK^T -- the statistics the backward
+ * consumes).  o and lse may be views into the activation slab: the producer writes the
+ * saved set directly (costs.py:99-105), no pack.  tcgen05 + TMEM + TMA, persistent
+ * causal tile scheduler; the first call per seq must not be inside a stream capture. */
+int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t heads, int64_t head_dim, float scale,
+                 void* stream);
 
 /* ----------------------------------------------- K8: stage-boundary send/recv */
 /* NCCL communicator of the pipeline (one rank per GPU).  The 128-byte unique id is

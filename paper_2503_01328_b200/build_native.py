@@ -21,7 +21,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libppo_b200.so")
-SOURCES = ["ppo_runtime.cu", "ppo_kernels.cu", "ppo_layernorm.cu", "ppo_comm.cu", "ppo_gemm_fwd.cu", "ppo_gemm_bwd.cu", "ppo_gemm_wgrad.cu"]
+SOURCES = ["ppo_runtime.cu", "ppo_kernels.cu", "ppo_layernorm.cu", "ppo_comm.cu", "ppo_gemm_fwd.cu", "ppo_gemm_bwd.cu", "ppo_gemm_wgrad.cu",
+           "ppo_attention.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -67,18 +68,31 @@ def cutlass_include() -> str | None:
     return None
 
 
+def fmha_include() -> str | None:
+    """Blackwell FMHA collectives (CUTLASS example 77) vendored in flashinfer's header tree."""
+    cand = os.environ.get("FMHA_INCLUDE") or _site_dir("flashinfer", os.path.join("data", "include"))
+    if cand and os.path.exists(os.path.join(cand, "flashinfer", "attention", "blackwell", "device", "fmha.hpp")):
+        return cand
+    return None
+
+
 def _flags(src: str) -> list[str]:
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{os.path.join(ROOT, 'include')}"]
     flags += ["-Xptxas", "-v"] if os.environ.get("PPO_PTXAS_VERBOSE") else []
     nd = nccl_dir()
     if nd:
         flags += ["-DPPO_WITH_NCCL", f"-I{os.path.join(nd, 'include')}"]
-    if src.startswith("ppo_gemm"):
+    if src.startswith("ppo_gemm") or src == "ppo_attention.cu":
         inc = cutlass_include()
         if not inc:
             raise RuntimeError("CUTLASS headers not found (set CUTLASS_INCLUDE)")
         util = os.path.join(os.path.dirname(inc), "tools", "util", "include")
         flags += [f"-I{inc}", f"-I{util}", "--expt-relaxed-constexpr", "-DNDEBUG"]
+    if src == "ppo_attention.cu":
+        fi = fmha_include()
+        if not fi:
+            raise RuntimeError("Blackwell FMHA headers not found (set FMHA_INCLUDE)")
+        flags += [f"-I{os.path.join(fi, 'flashinfer', 'attention', 'blackwell')}", f"-I{fi}"]
     return flags
 
 

@@ -244,7 +244,7 @@ class RankRunner:
 
     def __init__(self, program: Program, cfg: ModelConfig, sched: Schedule, microbatches: int, device,
                  transport=None, emulate: bool = False, params=None, seed: int = 1234, optimizer: str = "sgd",
-                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "auto",
+                 lr: float = 1e-4, verify_roundtrip: bool = False, use_graphs: bool = True, gemm: str = "auto", attn: str = "auto",
                  offload_tensors=None):
         torch_ = native.require_cuda()
         self.torch = torch_
@@ -257,7 +257,7 @@ class RankRunner:
         with torch.cuda.device(self.device):
             self.stages = {
                 s: Stage(cfg, s, sched.num_stages, microbatches, self.device, params=params,
-                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm, offload=offload_tensors)
+                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm, offload=offload_tensors, attn=attn)
                 for s in my_stages
             }
             lays = [st.layout for st in self.stages.values()]
@@ -849,7 +849,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             mode: str = "virtual", rank: int | None = None, device=None, iters: int = 1, warmup: int = 0,
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
-            use_graphs: bool = True, gemm: str = "auto", offload_tensors=None,
+            use_graphs: bool = True, gemm: str = "auto", offload_tensors=None, attn: str = "auto",
             iteration_graph: bool = False, pass_timing: bool = True) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
@@ -892,7 +892,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     dist_mode = mode in ("nccl", "gloo")
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
-                          use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors) for r in ranks]
+                          use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors, attn=attn) for r in ranks]
     if tokens is None:
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)

@@ -97,3 +97,36 @@ def decisions() -> dict:
         out[f"{key[1]} {'x'.join(str(x) for x in key[2:])}"] = {
             "ours_us": to, "ours_swizzle": sw, "cublas_us": tc, "choice": "tcgen05" if to <= tc else "cublas"}
     return out
+
+
+_ATTN_CHOICE: dict = {}
+ATTN_LOG: list = []  # (key, ours_us, cudnn_us)
+
+
+def prefer_ours_attn(shape: tuple, device, make) -> bool:
+    """``attn="auto"``: True if libppo_b200's attention forward (writing o and lse into
+    the slab) beats cuDNN's fused forward plus the K1 pack its separate outputs need,
+    for shape = (seq, heads, head_dim).  Timed head to head like the GEMMs (alternating,
+    >= ~10 ms per sample, medians); cached per process.  Must be called outside a
+    stream capture (Stage construction)."""
+    key = (torch.device(device).index,) + tuple(shape)
+    hit = _ATTN_CHOICE.get(key)
+    if hit is not None:
+        return hit
+    run_ours, run_cudnn = make()
+    est = max(_time_us(run_ours, reps=1, warm=1), _time_us(run_cudnn, reps=1, warm=1))
+    n = int(min(50, max(3, 10_000 / max(est, 1.0))))
+    t_o, t_c = [], []
+    for _ in range(4):
+        t_o.append(_time_batch_us(run_ours, n))
+        t_c.append(_time_batch_us(run_cudnn, n))
+    t_ours, t_cudnn = statistics.median(t_o), statistics.median(t_c)
+    _ATTN_CHOICE[key] = t_ours <= t_cudnn
+    ATTN_LOG.append((key, round(t_ours, 2), round(t_cudnn, 2)))
+    return _ATTN_CHOICE[key]
+
+
+def attn_decisions() -> dict:
+    """{"attn_fwd s x heads x head_dim": {"ours_us", "cudnn_pack_us", "choice"}}."""
+    return {f"attn_fwd {'x'.join(str(x) for x in key[1:])}": {
+        "ours_us": to, "cudnn_pack_us": tc, "choice": "tcgen05" if to <= tc else "cudnn"} for key, to, tc in ATTN_LOG}

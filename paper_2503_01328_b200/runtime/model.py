@@ -3,8 +3,8 @@
 Forward writes the 20bsh saved set of every layer straight into the
 (stage, microbatch) slab (``layout.SlabLayout``): the QKV and fc1 GEMMs write
 their outputs into slab views, the fused residual+dropout+LayerNorm kernel
-writes h1 and the next layer's x, and only the attention output / LSE need a
-K1 pack into the slab.  Backward reads the (possibly reloaded) slab, recomputes
+writes h1 and the next layer's x, and the tcgen05 attention kernel writes the
+attention output and its softmax statistics (the cuDNN baseline needs a K1 pack).  Backward reads the (possibly reloaded) slab, recomputes
 LayerNorm, GeLU and both dropout masks (K3-K5, ``libppo_b200.so``) and never
 needs anything that was not saved -- the recompute scheme of PAPER.md:439 that
 turns the reference's 34bsh coefficient into 20bsh (costs.py:1-7,18-20).
@@ -15,8 +15,10 @@ device measured faster (``gemm="auto"``, the default, runtime/gemm_tune.py);
 profiles/r1_gemm_tuning.txt).  fc1 fuses the GeLU into its epilogue (writes f into the slab and g for fc2), the
 fc2 activation-gradient GEMM fuses the GeLU backward (df = (dm @ Wfc2) * gelu'(f)),
 weight gradients accumulate in fp32 inside the GEMM epilogue.  ``gemm="cublas"``
-keeps the library GEMMs as the comparison baseline.  Causal attention runs on
-cuDNN's fused kernel; the embedding and loss head (first/last stage only) use
+keeps the library GEMMs as the comparison baseline.  Causal attention forward runs
+on libppo_b200's tcgen05 kernel or cuDNN's fused kernel, per shape whichever the
+device measured faster with cuDNN's output pack included (``attn="auto"``), its
+backward on cuDNN's fused kernel; the embedding and loss head (first/last stage only) use
 torch ops.
 """
 
@@ -134,10 +136,23 @@ class Stage:
     """Parameters, gradients, workspace and the F/B passes of one pipeline stage."""
 
     def __init__(self, cfg: ModelConfig, stage: int, num_stages: int, microbatches: int, device, params=None,
-                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "auto", offload=None):
+                 layers: list[int] | None = None, seed: int = 1234, gemm: str = "auto", offload=None,
+                 attn: str = "auto"):
         native.require_cuda()
         if gemm not in ("auto", "best", "tcgen05", "cublas"):
             raise ValueError(f"gemm backend {gemm!r}")
+        if attn not in ("auto", "tcgen05", "cudnn"):
+            raise ValueError(f"attention backend {attn!r}")
+        # attention forward: "tcgen05" = libppo_b200's kernel writing o and lse straight into
+        # the slab (head_dim 64/128, seq % 256 == 0); "cudnn" = cuDNN's fused kernel + K1 pack
+        # (the library baseline); "auto" = whichever measured faster at this shape
+        # (gemm_tune.prefer_ours_attn, decided in _attn_init).  The backward is cuDNN's fused
+        # kernel in every case, fed the saved o and lse.
+        self.attn_supported = cfg.head_dim in (64, 128) and cfg.seq % 256 == 0
+        if attn == "tcgen05" and not self.attn_supported:
+            raise ValueError(f"tcgen05 attention needs head_dim 64/128 and seq % 256 == 0 (got {cfg.head_dim}, {cfg.seq})")
+        self.attn_mode = attn
+        self.attn_ours = attn == "tcgen05"
         # "tcgen05": every GEMM on libppo_b200's kernels (fused GeLU epilogues); "cublas": the
         # library baseline; "best": ours except narrow-N / deep-K shapes (N <= 2048, K >= 3N)
         # where cuBLAS nvjet measured ~7% faster (profiles/r1_gemm_tuning.txt).
@@ -183,7 +198,37 @@ class Stage:
         self.iter_base = torch.zeros(1, device=self.device, dtype=torch.int64)
         self.tok = torch.zeros(cfg.seq + 1, device=self.device, dtype=torch.int64)
         self._attn_meta = None
+        self._attn_init()
         self.probe = None  # kernel name -> [bytes_per_launch, [(start_event, end_event), ...]]
+
+    def _attn_init(self):
+        """One eager attention call on scratch buffers before any capture: records the
+        cuDNN backward's metadata and statistics shape, and (tcgen05 path) lets the
+        library create its per-seq device constants outside a stream capture."""
+        cfg, ws = self.cfg, self.ws
+        s, h = cfg.seq, cfg.hidden
+        qkv = ws["big"].view(-1)[: s * 3 * h].view(s, 3 * h).zero_()
+        q, k, v = self._qkv_views(qkv)
+        res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+        self._attn_meta = tuple(res[2:8])
+        self._o_strides = res[0].stride()
+        self._lse_shape = tuple(res[1].shape)
+        if self.attn_mode != "cudnn" and self.attn_supported:
+            lse = torch.empty(cfg.heads * s, device=self.device, dtype=torch.float32)
+            native.attn_fwd(qkv, ws["a"], lse, cfg.heads)  # creates the library's per-seq constants
+            if self.attn_mode == "auto":
+                qkv.normal_()
+                dst = torch.empty(2 * s * h + 4 * cfg.heads * s, device=self.device, dtype=torch.uint8)
+
+                def make():
+                    def cudnn():
+                        r = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+                        native.pack([(r[0], 0, 1, 2 * s * h, 0), (r[1], 2 * s * h, 1, 4 * cfg.heads * s, 0)], dst)
+                    return (lambda: native.attn_fwd(qkv, ws["a"], lse, cfg.heads)), cudnn
+
+                self.attn_ours = gemm_tune.prefer_ours_attn((s, cfg.heads, cfg.head_dim), self.device, make)
+                del dst
+        del res
 
     def _k(self, name: str, nbytes: int, fn, *args, **kw):
         """Launch one native kernel; with probing on, bracket it with CUDA events."""
@@ -370,15 +415,13 @@ class Stage:
             off_a, off_m = self._offsets(l)
             x, qkv, h1, f = slab.get(i, "x"), slab.get(i, "qkv"), slab.get(i, "h1"), slab.get(i, "f")
             self.mm_fwd(ws["ln"], self.p(l, "w_qkv"), qkv)
-            q, k, v = self._qkv_views(qkv)
-            res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
-            o_tmp, lse = res[0], res[1]
-            if self._attn_meta is None:
-                self._attn_meta = tuple(res[2:8])
-                self._o_strides = o_tmp.stride()
-                self._lse_shape = tuple(lse.shape)
-            self._pack_attention(slab, i, o_tmp, lse)
             o = slab.get(i, "o")
+            if self.attn_ours:  # K7 writes o and lse straight into the slab
+                native.attn_fwd(qkv, o, slab.get(i, "lse"), cfg.heads)
+            else:
+                q, k, v = self._qkv_views(qkv)
+                res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+                self._pack_attention(slab, i, res[0], res[1])
             self.mm_fwd(o, self.p(l, "w_proj"), ws["a"])
             self._k("residual_dropout_ln_fwd", 8 * s * h, native.residual_dropout_ln_fwd, x, ws["a"], h1, self.p(l, "ln2_g"),
                     self.p(l, "ln2_b"), ws["ln"], p, seed, off_a, eps, offset_base=self.ctx)

@@ -82,6 +82,7 @@ SIGNATURES = {
     "ppo_gemm_nn": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_gemm_nn_dgelu": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_wgrad": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
+    "ppo_attn_fwd": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
     "ppo_comm_init": [ctypes.POINTER(ctypes.c_uint8), _I32, _I32, _I32, ctypes.POINTER(_VP)],
     "ppo_comm_destroy": [_VP],
@@ -113,7 +114,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 6:
+        if lib.ppo_abi_version() != 7:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -253,6 +254,22 @@ def gemm_tn_gelu(a, b, g, f, zero_bias, stream=None):
         raise ValueError("gemm_tn_gelu shapes")
     SHAPES[("ppo_gemm_tn_gelu", M, N, K)] += 1
     call("ppo_gemm_tn_gelu", _ptr(a), _ptr(b), _ptr(g), _ptr(f), _ptr(zero_bias), M, N, K, _stream(stream))
+
+
+def attn_fwd(qkv, o, lse, heads, scale=None, stream=None):
+    """Causal attention forward on tcgen05 (K7): qkv[s, 3h] bf16 -> o[s, h] bf16 and
+    lse[heads, s] fp32 (natural log), both writable views into the activation slab."""
+    _check_bf16(qkv, o)
+    s, h3 = qkv.shape
+    h = h3 // 3
+    D = h // heads
+    if h3 != 3 * h or tuple(o.shape) != (s, h) or lse.dtype != _torch().float32 or not lse.is_cuda or lse.numel() != heads * s:
+        raise ValueError(f"attn_fwd shapes: qkv {tuple(qkv.shape)} o {tuple(o.shape)} lse {tuple(lse.shape)}")
+    if not (qkv.is_contiguous() and o.is_contiguous() and lse.is_contiguous()):
+        raise ValueError("attn_fwd: qkv, o and lse must be contiguous")
+    scale = D ** -0.5 if scale is None else scale
+    SHAPES[("ppo_attn_fwd", s, heads, D)] += 1
+    call("ppo_attn_fwd", _ptr(qkv), _ptr(o), _ptr(lse), s, heads, D, scale, _stream(stream))
 
 
 def gemm_nn(a, b, d, beta=0.0, stream=None):

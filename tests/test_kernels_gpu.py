@@ -286,3 +286,67 @@ def test_gemm_swizzle_bit_identical_and_tuner():
     dec = gemm_tune.decisions()
     assert "tn 512x768x256" in dec and dec["tn 512x768x256"]["choice"] in ("tcgen05", "cublas")
     assert dec["tn 512x768x256"]["ours_swizzle"] in gemm_tune.SWIZZLES
+
+
+def _attn_ref(qkv: torch.Tensor, heads: int):
+    """fp32 causal attention on the device: o [s, h] and natural-log lse [heads, s]."""
+    s, h3 = qkv.shape
+    h = h3 // 3
+    D = h // heads
+    q, k, v = qkv.float().view(s, 3, heads, D).permute(1, 2, 0, 3)  # [heads, s, D] each
+    scores = (q @ k.transpose(1, 2)) * D ** -0.5
+    mask = torch.ones(s, s, device=qkv.device, dtype=torch.bool).triu(1)
+    scores = scores.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(scores, dim=-1)  # [heads, s]
+    o = torch.softmax(scores, dim=-1) @ v  # [heads, s, D]
+    return o.transpose(0, 1).reshape(s, h), lse
+
+
+@pytest.mark.parametrize("s,heads,D", [(256, 4, 64), (512, 4, 64), (1024, 8, 128), (2048, 2, 128)])
+def test_attn_fwd_matches_fp32(s, heads, D):
+    """K7 (tcgen05 causal attention forward) against fp32 attention on the same bf16
+    inputs: o within bf16 rounding of P (rel. L2 <= 1e-2, max abs <= 2e-2 at unit-scale
+    inputs), lse within 2e-3 absolute (fp32 statistics, exp2-based softmax)."""
+    g = torch.Generator(device=DEV).manual_seed(s + heads + D)
+    qkv = torch.randn(s, 3 * heads * D, device=DEV, generator=g).bfloat16()
+    o = torch.full((s, heads * D), float("nan"), device=DEV, dtype=torch.bfloat16)
+    lse = torch.full((heads, s), float("nan"), device=DEV, dtype=torch.float32)
+    native.attn_fwd(qkv, o, lse, heads)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = _attn_ref(qkv, heads)
+    assert torch.isfinite(o.float()).all() and torch.isfinite(lse).all()
+    rel = ((o.float() - o_ref).norm() / o_ref.norm()).item()
+    assert rel <= 1e-2, rel
+    assert (o.float() - o_ref).abs().max().item() <= 2e-2
+    assert (lse - lse_ref).abs().max().item() <= 2e-3
+
+
+def test_attn_fwd_matches_cudnn_at_c2_shape():
+    """At the C2 attention shape (s=4096, 16 heads of 128) our o and lse match cuDNN's
+    fused forward -- the statistics feed cuDNN's backward, so they must be the same
+    quantity (natural-log logsumexp, [heads, s])."""
+    s, heads, D = 4096, 16, 128
+    g = torch.Generator(device=DEV).manual_seed(7)
+    qkv = torch.randn(s, 3 * heads * D, device=DEV, generator=g).bfloat16()
+    o = torch.empty(s, heads * D, device=DEV, dtype=torch.bfloat16)
+    lse = torch.empty(heads, s, device=DEV, dtype=torch.float32)
+    native.attn_fwd(qkv, o, lse, heads)
+    q, k, v = [t.transpose(1, 2) for t in qkv.view(1, s, 3, heads, D).unbind(2)]
+    res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+    torch.cuda.synchronize()
+    o_cud = res[0].transpose(1, 2).reshape(s, heads * D).float()
+    lse_cud = res[1].reshape(heads, s)
+    assert (lse - lse_cud).abs().max().item() <= 2e-3
+    rel = ((o.float() - o_cud).norm() / o_cud.norm()).item()
+    assert rel <= 1e-2, rel
+
+
+def test_attn_fwd_rejects_bad_shapes():
+    qkv = torch.zeros(300, 3 * 256, device=DEV, dtype=torch.bfloat16)  # seq not a multiple of 256
+    with pytest.raises(native.PpoError):
+        native.attn_fwd(qkv, torch.empty(300, 256, device=DEV, dtype=torch.bfloat16),
+                        torch.empty(4 * 300, device=DEV), 4)
+    qkv = torch.zeros(256, 3 * 96 * 2, device=DEV, dtype=torch.bfloat16)  # head_dim 96
+    with pytest.raises(native.PpoError):
+        native.attn_fwd(qkv, torch.empty(256, 192, device=DEV, dtype=torch.bfloat16),
+                        torch.empty(2 * 256, device=DEV), 2)

@@ -18,7 +18,8 @@ def rel_err(a, b):
     return float((a - b).norm() / (b.norm() + 1e-12))
 
 
-def test_single_stage_loss_and_grads_match_oracle():
+@pytest.mark.parametrize("attn", ["tcgen05", "cudnn"])
+def test_single_stage_loss_and_grads_match_oracle(attn):
     cfg = rt.ModelConfig(n_layers=2, hidden=256, heads=4, seq=512, vocab=1024)
     ocfg = oracle_gpt.GPTConfig(n_layers=2, hidden=256, heads=4, seq=512, vocab=1024)
     m = 2
@@ -28,7 +29,8 @@ def test_single_stage_loss_and_grads_match_oracle():
     assert all(torch.equal(params[k], ref_params[k]) for k in params)
     want_loss, _, want_grads = oracle_gpt.forward_backward(ocfg, params, tokens)
 
-    st = rt.Stage(cfg, 0, 1, m, DEV)
+    st = rt.Stage(cfg, 0, 1, m, DEV, attn=attn)
+    assert st.attn_ours == (attn == "tcgen05")
     slab_mem = torch.empty(st.layout.slab_bytes, dtype=torch.uint8, device=DEV)
     slab = rt.SlabView(st.layout, slab_mem)
     st.zero_grad()
