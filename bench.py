@@ -403,6 +403,9 @@ def run_b200(args, rank, world, local_rank):
             st = select_offload_stages(po_block(d, v, c1), 1)
             sched_variants[f"{kind}_v{v}_none"] = (sv, None, "single")
             sched_variants[f"{kind}_v{v}_n1_duplex"] = (sv, plan_slots_duplex(sv, st, w1), "dual")
+            # one offload-arena slab beyond the modelled peak: memory for slack against
+            # D2H running slower than modelled (runtime/lower.py _colour)
+            sched_variants[f"{kind}_v{v}_n1_duplex_spare1"] = (sv, plan_slots_duplex(sv, st, w1), "dual", 1)
 
     tokens = torch.randint(0, vocab, (m, s + 1), generator=torch.Generator().manual_seed(0)).pin_memory()
     results = {}
@@ -467,12 +470,13 @@ def run_b200(args, rank, world, local_rank):
         del res
         gc.collect()
         torch.cuda.empty_cache()
-    for name, (sv, pv, sm) in sched_variants.items():
+    for name, (sv, pv, sm, *spare) in sched_variants.items():
+        spare = spare[0] if spare else 0
         res = execute(sv, pv, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps, warmup=args.warmup,
                       tokens=tokens, optimizer="sgd", stream_mode=sm, iteration_graph=args.iteration_graph,
-                      gemm=backend)
+                      gemm=backend, spare_slabs=spare)
         results[name] = dict(policy_report(res, sv, pv, m, s, res.slab_bytes, rank), schedule=sv.kind,
-                             v=sv.local_stages, stream_mode=sm)
+                             v=sv.local_stages, stream_mode=sm, spare_slabs=spare)
         if dist is not None:
             per_rank = [None] * world
             dist.all_gather_object(per_rank, results[name]["peak_act_gb"])

@@ -87,7 +87,9 @@ def _flags(src: str) -> list[str]:
         if not inc:
             raise RuntimeError("CUTLASS headers not found (set CUTLASS_INCLUDE)")
         util = os.path.join(os.path.dirname(inc), "tools", "util", "include")
-        flags += [f"-I{inc}", f"-I{util}", "--expt-relaxed-constexpr", "-DNDEBUG"]
+        # CUTLASS_ENABLE_GDC_FOR_SM100: the kernels' griddepcontrol.wait / launch_dependents
+        # are compiled in, so they may be launched with programmatic dependent launch
+        flags += [f"-I{inc}", f"-I{util}", "--expt-relaxed-constexpr", "-DNDEBUG", "-DCUTLASS_ENABLE_GDC_FOR_SM100=1"]
     if src == "ppo_attention.cu":
         fi = fmha_include()
         if not fi:

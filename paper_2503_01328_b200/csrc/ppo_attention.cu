@@ -176,7 +176,8 @@ int run(const bf16* q, bf16* o, float* lse, int s, int H, int* offs, float scale
   if (cs != cutlass::Status::kSuccess) return set_error(PPO_ESHAPE, "ppo_attn_fwd: cannot implement");
   cs = op.initialize(args, nullptr, st);
   if (cs != cutlass::Status::kSuccess) return set_error(PPO_EINVAL, "ppo_attn_fwd: initialize failed");
-  cs = op.run(st);
+  auto params = op.params();  // launched without PDL unless PPO_PDL bit 1 (profiles/r1_pdl_ab.jsonl)
+  cs = Fmha<D>::Operation::run(params, st, pdl_gemm_enabled());
   count_launch();
   if (cs != cutlass::Status::kSuccess) return cuda_error(cudaGetLastError(), "ppo_attn_fwd: launch");
   return PPO_OK;
@@ -185,6 +186,7 @@ int run(const bf16* q, bf16* o, float* lse, int s, int H, int* offs, float scale
 // The statistics come out of the correction warpgroup as log2(rowsum) + log2(e)*scale*rowmax;
 // the backward pass consumes natural-log logsumexp.  One thread per element, in place.
 __global__ void __launch_bounds__(256) lse_log2_to_ln_kernel(float* __restrict__ lse, int n) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) lse[i] *= 0.69314718055994530942f;
 }
@@ -215,7 +217,7 @@ int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t head
                : run<128>(static_cast<const bf16*>(qkv), static_cast<bf16*>(o), lse, s, H, offs, scale, st);
   if (rc) return rc;
   int n = H * s;
-  lse_log2_to_ln_kernel<<<(n + 255) / 256, 256, 0, st>>>(lse, n);
+  launch_pdl(lse_log2_to_ln_kernel, (n + 255) / 256, 256, 0, st, lse, n);
   PPO_LAUNCHED("lse_log2_to_ln_kernel");
   return PPO_OK;
 }

@@ -127,7 +127,7 @@ int launch(int op, typename G::Args& args, void* stream, const char* who) {
   st = gemm.initialize(args, ws, as_stream(stream));
   if (st != cutlass::Status::kSuccess)
     return set_error(PPO_EINVAL, "%s: initialize (%s)", who, cutlassGetStatusString(st));
-  st = gemm.run(as_stream(stream));
+  st = gemm.run(as_stream(stream), nullptr, pdl_gemm_enabled());  // PDL: GDC waits are compiled in (build_native)
   count_launch();
   if (st != cutlass::Status::kSuccess) return set_error(PPO_EINVAL, "%s: run (%s)", who, cutlassGetStatusString(st));
   return PPO_OK;

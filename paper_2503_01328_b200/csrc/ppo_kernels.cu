@@ -12,6 +12,7 @@ __global__ void __launch_bounds__(256) dropout_kernel(const __nv_bfloat16* __res
                                                       __nv_bfloat16* __restrict__ y, int64_t n8,
                                                       uint32_t threshold, float scale, uint64_t seed,
                                                       uint64_t offset_add, const uint64_t* __restrict__ offset_base) {
+  pdl_wait();
   const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < n8; c0 += 2 * stride) {
@@ -56,6 +57,7 @@ constexpr int kVec = 2;
 
 __global__ void __launch_bounds__(256) gelu_fwd_kernel(const __nv_bfloat16* __restrict__ f,
                                                        __nv_bfloat16* __restrict__ g, int64_t n8) {
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < n8; c0 += kVec * stride) {
     uint4 raw[kVec];
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(256) gelu_bwd_kernel(const __nv_bfloat16* __re
                                                        const __nv_bfloat16* dg_in,
                                                        __nv_bfloat16* __restrict__ g_out,
                                                        __nv_bfloat16* df_out, int64_t n8) {
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < n8; c0 += kVec * stride) {
     uint4 rf[kVec], rd[kVec];
@@ -115,6 +118,7 @@ __global__ void __launch_bounds__(256) gelu_bwd_kernel(const __nv_bfloat16* __re
 
 __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ acc, int64_t rows,
                               int64_t cols, int64_t rows_per_block) {
+  pdl_wait();
   const int64_t col8 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (8 * col8 >= cols) return;
   const int64_t r0 = blockIdx.y * rows_per_block;
@@ -139,6 +143,7 @@ __global__ void __launch_bounds__(256) embed_fwd_kernel(const int64_t* __restric
                                                         const __nv_bfloat16* __restrict__ wpe,
                                                         __nv_bfloat16* __restrict__ x, int64_t rows, int64_t h,
                                                         int64_t vocab) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t n8 = h >> 3;
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__(256) embed_bwd_kernel(const int64_t* __restric
                                                         const __nv_bfloat16* __restrict__ dy,
                                                         float* __restrict__ gwte, float* __restrict__ gwpe,
                                                         int64_t rows, int64_t h, int64_t vocab) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t n8 = h >> 3;
@@ -216,7 +222,7 @@ int ppo_dropout(const void* x, void* y, int64_t n, float p, uint64_t seed, uint6
   if (!(p >= 0.f && p < 1.f)) return set_error(PPO_EINVAL, "ppo_dropout: p=%f", p);
   if (n == 0) return PPO_OK;
   const int64_t n8 = n >> 3;
-  dropout_kernel<<<elementwise_grid(n8), 256, 0, as_stream(stream)>>>(
+  launch_pdl(dropout_kernel, elementwise_grid(n8), 256, 0, as_stream(stream), 
       static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), n8, dropout_threshold(p),
       1.f / (1.f - p), seed, offset, offset_base);
   PPO_LAUNCHED("dropout_kernel");
@@ -226,7 +232,7 @@ int ppo_dropout(const void* x, void* y, int64_t n, float p, uint64_t seed, uint6
 int ppo_gelu_fwd(const void* f, void* g, int64_t n, void* stream) {
   if (!f || !g || n < 0 || (n & 7)) return set_error(PPO_EINVAL, "ppo_gelu_fwd: bad arguments");
   if (n == 0) return PPO_OK;
-  gelu_fwd_kernel<<<elementwise_grid(n >> 3), 256, 0, as_stream(stream)>>>(
+  launch_pdl(gelu_fwd_kernel, elementwise_grid(n >> 3), 256, 0, as_stream(stream),
       static_cast<const __nv_bfloat16*>(f), static_cast<__nv_bfloat16*>(g), n >> 3);
   PPO_LAUNCHED("gelu_fwd_kernel");
   return PPO_OK;
@@ -235,7 +241,7 @@ int ppo_gelu_fwd(const void* f, void* g, int64_t n, void* stream) {
 int ppo_gelu_bwd(const void* f, const void* dg, void* g, void* df, int64_t n, void* stream) {
   if (!f || !dg || !df || n < 0 || (n & 7)) return set_error(PPO_EINVAL, "ppo_gelu_bwd: bad arguments");
   if (n == 0) return PPO_OK;
-  gelu_bwd_kernel<<<elementwise_grid(n >> 3), 256, 0, as_stream(stream)>>>(
+  launch_pdl(gelu_bwd_kernel, elementwise_grid(n >> 3), 256, 0, as_stream(stream),
       static_cast<const __nv_bfloat16*>(f), static_cast<const __nv_bfloat16*>(dg), static_cast<__nv_bfloat16*>(g),
       static_cast<__nv_bfloat16*>(df), n >> 3);
   PPO_LAUNCHED("gelu_bwd_kernel");
@@ -248,7 +254,7 @@ int ppo_embed_fwd(const int64_t* tokens, const void* wte, const void* wpe, void*
     return set_error(PPO_EINVAL, "ppo_embed_fwd: bad arguments (hidden %% 8 != 0?)");
   if (!aligned16(wte) || !aligned16(wpe) || !aligned16(x)) return set_error(PPO_EINVAL, "ppo_embed_fwd: unaligned");
   if (rows == 0) return PPO_OK;
-  embed_fwd_kernel<<<row_grid(rows), 256, 0, as_stream(stream)>>>(
+  launch_pdl(embed_fwd_kernel, row_grid(rows), 256, 0, as_stream(stream), 
       tokens, static_cast<const __nv_bfloat16*>(wte), static_cast<const __nv_bfloat16*>(wpe),
       static_cast<__nv_bfloat16*>(x), rows, hidden, vocab);
   PPO_LAUNCHED("embed_fwd_kernel");
@@ -261,7 +267,7 @@ int ppo_embed_bwd(const int64_t* tokens, const void* dy, float* gwte, float* gwp
     return set_error(PPO_EINVAL, "ppo_embed_bwd: bad arguments (hidden %% 8 != 0?)");
   if (!aligned16(dy) || !aligned16(gwte) || !aligned16(gwpe)) return set_error(PPO_EINVAL, "ppo_embed_bwd: unaligned");
   if (rows == 0) return PPO_OK;
-  embed_bwd_kernel<<<row_grid(rows), 256, 0, as_stream(stream)>>>(
+  launch_pdl(embed_bwd_kernel, row_grid(rows), 256, 0, as_stream(stream), 
       tokens, static_cast<const __nv_bfloat16*>(dy), gwte, gwpe, rows, hidden, vocab);
   PPO_LAUNCHED("embed_bwd_kernel");
   return PPO_OK;
@@ -274,7 +280,7 @@ int ppo_colsum(const void* x, float* acc, int64_t rows, int64_t cols, void* stre
   const int64_t gx = (cols / 8 + threads - 1) / threads;
   const int64_t rpb = 64;
   const int64_t gy = (rows + rpb - 1) / rpb;
-  colsum_kernel<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, as_stream(stream)>>>(
+  launch_pdl(colsum_kernel, dim3((unsigned)gx, (unsigned)gy), threads, 0, as_stream(stream), 
       static_cast<const __nv_bfloat16*>(x), acc, rows, cols, rpb);
   PPO_LAUNCHED("colsum_kernel");
   return PPO_OK;

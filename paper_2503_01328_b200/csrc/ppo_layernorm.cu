@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_fwd_kernel(
     const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
     int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add,
     const uint64_t* __restrict__ offset_base, int use_dropout) {
+  pdl_wait();
   extern __shared__ __align__(16) float sm[];
   const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
   float* scratch = sm;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ resid_grad, __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
     float* __restrict__ dbeta, int64_t rows, int hidden, float eps, __nv_bfloat16* __restrict__ drop_out,
     uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add, const uint64_t* __restrict__ offset_base) {
+  pdl_wait();
   extern __shared__ __align__(16) float sm[];
   const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
   float* s_acc = sm;                 // [2h]: dgamma partials, then dbeta partials
@@ -361,7 +363,7 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
   const int vpl = vpl_choice(hidden, 4);
 #define PPO_LN_FWD_W(W, V)                                                                                    \
   if ((rc = row_launch(ln_fwd_kernel<false, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
-  ln_fwd_kernel<false, W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                 \
+  launch_pdl(ln_fwd_kernel<false, W, V>, l.grid, l.block, l.smem, as_stream(stream),                                  \
       nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta, static_cast<__nv_bfloat16*>(y), rows, \
       (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0);
 #define PPO_LN_FWD_V(V)                                               \
@@ -397,7 +399,7 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   const int vpl = vpl_choice(hidden, 4);
 #define PPO_RES_W(W, V)                                                                                      \
   if ((rc = row_launch(ln_fwd_kernel<true, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
-  ln_fwd_kernel<true, W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                 \
+  launch_pdl(ln_fwd_kernel<true, W, V>, l.grid, l.block, l.smem, as_stream(stream),                                  \
       static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),                   \
       static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps, \
       dropout_threshold(p), 1.f / (1.f - p), seed, offset, offset_base, p > 0.f ? 1 : 0);
@@ -435,7 +437,7 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
   const int vpl = vpl_choice(hidden, 2);
 #define PPO_LN_BWD_W(W, V)                                                                                     \
   if ((rc = row_launch(ln_bwd_kernel<W, V>, rows, hidden, V, 2, &l))) return rc;                              \
-  ln_bwd_kernel<W, V><<<l.grid, l.block, l.smem, as_stream(stream)>>>(                                         \
+  launch_pdl(ln_bwd_kernel<W, V>, l.grid, l.block, l.smem, as_stream(stream),                                          \
       static_cast<const __nv_bfloat16*>(x), gamma, static_cast<const __nv_bfloat16*>(dy),                     \
       static_cast<const __nv_bfloat16*>(resid_grad), static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows,    \
       (int)hidden, eps, static_cast<__nv_bfloat16*>(drop_out), dropout_threshold(p), p > 0.f ? 1.f / (1.f - p) : 1.f, \

@@ -31,6 +31,14 @@ int cuda_error(cudaError_t err, const char* what) {
   return set_error((int)err, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
 }
 
+int pdl_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("PPO_PDL");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode;
+}
+
 int sm_count_current() {
   static thread_local int cached_dev = -1, cached_sms = 148;
   int dev = 0;
@@ -54,6 +62,7 @@ struct GatherArgs {
 // Persistent gather: every thread walks each item's 16-byte chunks with a grid
 // stride, four independent 16 B loads in flight before the stores.
 __global__ void __launch_bounds__(256) pack_kernel(GatherArgs args, uint8_t* __restrict__ dst) {
+  pdl_wait();
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   for (int i = 0; i < args.n; ++i) {
@@ -100,6 +109,7 @@ struct BulkArgs {
 };
 
 __global__ void __launch_bounds__(32) pack_bulk_kernel(BulkArgs a, uint8_t* __restrict__ dst) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t stage[];
   __shared__ __align__(8) uint64_t bar[kBulkStages];
   if (threadIdx.x != 0) return;
@@ -161,6 +171,7 @@ using namespace ppo;
 
 namespace {
 __global__ void timestamp_kernel(unsigned long long* out) {
+  pdl_wait();
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *out = t;
@@ -240,7 +251,7 @@ int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_s
 
 int ppo_timestamp(uint64_t* slot, void* stream) {
   if (!slot) return set_error(PPO_EINVAL, "ppo_timestamp: null slot");
-  timestamp_kernel<<<1, 1, 0, as_stream(stream)>>>(reinterpret_cast<unsigned long long*>(slot));
+  launch_pdl(timestamp_kernel, 1, 1, 0, as_stream(stream), reinterpret_cast<unsigned long long*>(slot));
   PPO_LAUNCHED("timestamp_kernel");
   return PPO_OK;
 }
@@ -291,7 +302,7 @@ int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream) {
     const uint64_t cap = (uint64_t)sm_count_current() * 2;  // two 96 KB stagings per SM
     const uint64_t nc = b.first_chunk[n];
     const int blocks = (int)(nc < cap ? nc : cap);
-    pack_bulk_kernel<<<blocks, 32, smem, as_stream(stream)>>>(b, static_cast<uint8_t*>(dst));
+    launch_pdl(pack_bulk_kernel, blocks, 32, smem, as_stream(stream), b, static_cast<uint8_t*>(dst));
     PPO_LAUNCHED("pack_bulk_kernel");
     return PPO_OK;
   }
@@ -299,7 +310,7 @@ int ppo_pack(const ppo_gather_item* items, int n, void* dst, void* stream) {
   uint64_t want = (chunks + threads * 4 - 1) / (threads * 4);
   const uint64_t cap = (uint64_t)sm_count_current() * 8;  // 8 CTAs of 256 per SM resident
   const int blocks = (int)(want < cap ? (want ? want : 1) : cap);
-  pack_kernel<<<blocks, threads, 0, as_stream(stream)>>>(args, static_cast<uint8_t*>(dst));
+  launch_pdl(pack_kernel, blocks, threads, 0, as_stream(stream), args, static_cast<uint8_t*>(dst));
   PPO_LAUNCHED("pack_kernel");
   return PPO_OK;
 }

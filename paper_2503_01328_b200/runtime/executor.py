@@ -850,7 +850,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
             use_graphs: bool = True, gemm: str = "auto", offload_tensors=None, attn: str = "auto",
-            iteration_graph: bool = False, pass_timing: bool = True) -> RunResult:
+            iteration_graph: bool = False, pass_timing: bool = True, spare_slabs: int = 0) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
@@ -865,6 +865,9 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     fetch over the host link the copy engines are saturating.
     ``pass_timing=False`` (graph mode): no per-pass timestamps inside the graph, only
     the iteration's start/end -- the returned trace then has no passes.
+    ``spare_slabs``: offload-arena slabs beyond the modelled peak (``lower``): device
+    memory traded for slack when transfers run slower than the plan modelled.
+    ``attn``: attention forward backend of every stage ("auto" | "tcgen05" | "cudnn").
 
     In the multi-process modes every iteration starts after a device synchronise
     and a barrier, and the returned iteration/wall times and losses are the same on
@@ -877,7 +880,8 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         ranks = list(range(sched.devices))
     else:
         ranks = [rank if rank is not None else 0]
-    programs = {r: lower(sched, plan, r, stream_mode=stream_mode, emulate_neighbors=(mode == "emulate")) for r in ranks}
+    programs = {r: lower(sched, plan, r, stream_mode=stream_mode, emulate_neighbors=(mode == "emulate"),
+                      spare_slabs=spare_slabs) for r in ranks}
     transport = None
     if mode == "virtual":
         transport = LocalTransport()

@@ -89,7 +89,7 @@ class Program:
         return [op for op in self.ops if op.stream == stream]
 
 
-def _colour(intervals):
+def _colour(intervals, spare: int = 0):
     """Greedy interval colouring. intervals: list of (start, end, key).
 
     Frees sort before allocations at equal times (half-open residency, as in
@@ -97,25 +97,38 @@ def _colour(intervals):
     (LRU), so the release event it waits on is as old as possible: on the GPU the
     compute stream can run ahead of the witness timeline (an emulated rank has no
     pipeline bubbles) and a just-freed slab would stall it.  Greedy colouring uses
-    max-overlap colours whatever free colour it picks.  Returns (assignment key ->
-    (colour, previous occupant key or None), n_colours).
+    max-overlap colours whatever free colour it picks.  ``spare`` extra colours widen
+    the LRU choice (every acquirer then waits on a release at least one holder older):
+    memory traded for slack against transfers that run slower than modelled.  Returns
+    (assignment key -> (colour, previous occupant key or None), n_colours).
     """
+    if spare:
+        _, n0 = _colour(intervals)
+        return _colour_fixed(intervals, n0 + spare), n0 + spare
+    return _colour_fixed(intervals, None)
+
+
+def _colour_fixed(intervals, n_fixed):
+    """LRU greedy colouring; with ``n_fixed`` all colours exist up front (free, in
+    index order), else they are created on demand.  Returns (assignment, n) or, with
+    n_fixed, the assignment alone."""
     events = []
     for start, end, key in intervals:
         events.append((start, 1, key))
         events.append((end, 0, key))
     events.sort(key=lambda e: (e[0], e[1]))
-    free: list = []  # heap of (release order, colour)
+    free: list = [(i - n_fixed, i) for i in range(n_fixed)] if n_fixed else []  # heap of (release order, colour)
     last_holder: dict = {}
     held: dict = {}
     assignment = {}
-    n = 0
+    n = n_fixed or 0
     order = 0
     for _t, is_alloc, key in events:
         if is_alloc:
             if free:
                 _, c = heapq.heappop(free)
             else:
+                assert n_fixed is None, "fixed colouring ran out of colours"
                 c = n
                 n += 1
             assignment[key] = (c, last_holder.get(c))
@@ -125,7 +138,7 @@ def _colour(intervals):
             last_holder[c] = key
             heapq.heappush(free, (order, c))
             order += 1
-    return assignment, n
+    return assignment if n_fixed else (assignment, n)
 
 
 def _anchor_for(t: Fraction, passes):
@@ -147,10 +160,12 @@ def lower(
     rank: int,
     stream_mode: str = "single",
     emulate_neighbors: bool = False,
+    spare_slabs: int = 0,
 ) -> Program:
     """Per-rank program.  ``emulate_neighbors`` drops cross-rank ops (the rank runs
     alone with a loopback stage boundary, e.g. the single-GPU bench of one rank
-    of a PP=d schedule)."""
+    of a PP=d schedule).  ``spare_slabs`` adds that many slabs to the offload arena
+    beyond the modelled peak (see ``_colour``)."""
     trace = simulate(sched, plan, stream_mode=stream_mode)
     timed = {(p.kind, p.stage, p.microbatch): p for p in trace.passes}
     my_passes = [timed[(p.kind, p.stage, p.microbatch)] for p in sched.device_passes[rank]]
@@ -179,7 +194,7 @@ def lower(
             intervals.append((p.start, end, ("F",) + pair))
             if pair in offloaded:
                 intervals.append((h2d[pair].start, done, ("R",) + pair))
-    slab_of, n_slabs = _colour(intervals)
+    slab_of, n_slabs = _colour(intervals, spare=spare_slabs if offloaded else 0)
     # resident part of every slab (partial offload keeps it on the device from F start
     # to the pair's last use, offloaded or not): colours = the in-flight peak
     res_of, n_res = _colour([(p.start, timed[(last_use, p.stage, p.microbatch)].end, ("P", p.stage, p.microbatch))

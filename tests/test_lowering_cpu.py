@@ -132,9 +132,10 @@ class LocalChannels:
         return Bound()
 
 
-def run_all_ranks(sched, plan, stream_mode="single"):
+def run_all_ranks(sched, plan, stream_mode="single", spare_slabs=0):
     chans = LocalChannels()
-    walkers = [CpuWalker(sched, lower(sched, plan, r, stream_mode=stream_mode), chans.bind(r)) for r in range(sched.devices)]
+    walkers = [CpuWalker(sched, lower(sched, plan, r, stream_mode=stream_mode, spare_slabs=spare_slabs), chans.bind(r))
+               for r in range(sched.devices)]
     while not all(w.done() for w in walkers):
         progressed = False
         for w in walkers:
@@ -179,6 +180,21 @@ def test_lowered_programs_execute_correctly(name, make, stream_mode):
         assert w.prog.compute_order == [(str(p.kind), p.stage, p.microbatch) for p in sched.device_passes[r]]
         # the arena holds exactly the runner model's peak (slabs are per pair; units = v per pair)
         assert w.prog.n_slabs * sched.units_per_stage == w.prog.witness_peak_units or plan is None
+
+
+@pytest.mark.parametrize("name,make", [c for c in CASES if "no offload" not in c[0]], ids=lambda c: c if isinstance(c, str) else "")
+def test_spare_slab_programs_execute_correctly(name, make):
+    """One offload-arena slab beyond the modelled peak: same results and op order, one
+    more slab on every rank that offloads, slab reuse still hazard-free (CpuWalker)."""
+    sched, plan = make()
+    walkers = run_all_ranks(sched, plan, "dual", spare_slabs=1)
+    for j in range(sched.microbatches):
+        assert walkers[0].grad_out[(0, j)] == expected_input_grad(sched, j)
+    for r, w in enumerate(walkers):
+        base = lower(sched, plan, r, stream_mode="dual")
+        offloads = any(op.kind == "OFFLOAD" for op in base.ops)
+        assert w.prog.n_slabs == base.n_slabs + (1 if offloads else 0)
+        assert w.prog.compute_order == base.compute_order
 
 
 def test_arena_matches_reference_peaks_c1():
