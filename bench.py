@@ -403,9 +403,6 @@ def run_b200(args, rank, world, local_rank):
             st = select_offload_stages(po_block(d, v, c1), 1)
             sched_variants[f"{kind}_v{v}_none"] = (sv, None, "single")
             sched_variants[f"{kind}_v{v}_n1_duplex"] = (sv, plan_slots_duplex(sv, st, w1), "dual")
-            # one offload-arena slab beyond the modelled peak: memory for slack against
-            # D2H running slower than modelled (runtime/lower.py _colour)
-            sched_variants[f"{kind}_v{v}_n1_duplex_spare1"] = (sv, plan_slots_duplex(sv, st, w1), "dual", 1)
 
     tokens = torch.randint(0, vocab, (m, s + 1), generator=torch.Generator().manual_seed(0)).pin_memory()
     results = {}

@@ -134,7 +134,8 @@ def cmd_run(args) -> int:
     t_dup = Fraction(round(cal["t_duplex"] * 1e6), 1_000_000) if cal.get("t_duplex") else None
     plan = _plan(sched, args.d, args.v, costs, t_o, args.offload, args.planner, t_dup)
     res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.iters, warmup=args.warmup,
-                  stream_mode=args.stream_mode, optimizer=args.optimizer, iteration_graph=args.iteration_graph)
+                  stream_mode=args.stream_mode, optimizer=args.optimizer, iteration_graph=args.iteration_graph,
+                  spare_slabs=args.spare_slabs)
     trace = res.trace
     it = max(res.iteration_seconds)
     predicted = simulate(sched, plan, stream_mode=args.stream_mode)
@@ -192,6 +193,7 @@ def make_parser() -> argparse.ArgumentParser:
     run.add_argument("--planner", choices=("slots", "duplex"), default="slots",
                      help="slots: reference plan_slots; duplex: plan_slots_duplex (run with --stream-mode dual)")
     run.add_argument("--optimizer", choices=("none", "sgd", "adamw"), default="sgd")
+    run.add_argument("--spare-slabs", type=int, default=0, help="offload-arena slabs beyond the modelled peak")
     run.add_argument("--iters", type=int, default=2)
     run.add_argument("--warmup", type=int, default=1)
     run.set_defaults(func=cmd_run)
