@@ -21,7 +21,14 @@
 namespace ppo {
 
 constexpr int kMaxHidden = 8192;
-constexpr int kGroupsPerBlock = 4;  // rows processed concurrently by one CTA
+constexpr int kGroupsPerBlock = 4;  // rows processed concurrently by one CTA (at most)
+
+// Rows per CTA for a W-warp row group: up to 4, but never more than 16 warps per CTA, so
+// 32*W*G threads leave >= 128 registers a thread (fewer spill the double-buffered rows).
+constexpr int groups_for(int W) { return (16 / W) > kGroupsPerBlock ? kGroupsPerBlock : ((16 / W) < 1 ? 1 : 16 / W); }
+// The forward kernels hold fewer live registers: 4 rows per CTA up to 5-warp rows (measured
+// 9% faster than 3 at h = 5120), the register-safe count above that.
+constexpr int fwd_groups_for(int W) { return W <= 5 ? kGroupsPerBlock : groups_for(W); }
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -66,8 +73,8 @@ __device__ __forceinline__ void load8f(const float* p, float (&o)[8]) {
 // out = resid + dropout(branch)  (kResidual)  or  v = src  (!kResidual);  ln = LN(v).
 // The next row's vectors are requested before the current row is reduced, so DRAM
 // latency overlaps the shuffle reduction and the stores (register double-buffering).
-template <bool kResidual, int W, int kVecPerLane>
-__global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_fwd_kernel(
+template <bool kResidual, int W, int kVecPerLane, int G>
+__global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
     const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
     const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
     int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add,
@@ -80,8 +87,8 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_fwd_kernel(
   const int L = threadIdx.x % (32 * W);
   const int nvec = hidden >> 3;
   const float inv_h = 1.f / (float)hidden;
-  const int64_t step = (int64_t)gridDim.x * kGroupsPerBlock;
-  int64_t row = (int64_t)blockIdx.x * kGroupsPerBlock + group;
+  const int64_t step = (int64_t)gridDim.x * G;
+  int64_t row = (int64_t)blockIdx.x * G + group;
   uint4 ra[kVecPerLane], rb[kVecPerLane];
   auto fetch = [&](int64_t r, uint4 (&a)[kVecPerLane], uint4 (&b)[kVecPerLane]) {
 #pragma unroll
@@ -153,8 +160,8 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_fwd_kernel(
 // parameter-gradient sums live in registers for the whole row loop; at the end the
 // CTA's row groups are folded in shared memory and flushed with one 16-byte vector
 // atomic per 4 columns (one CTA per SM: ~148 atomics per address in total).
-template <int W, int kVecPerLane>
-__global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
+template <int W, int kVecPerLane, int G>
+__global__ void __launch_bounds__(32 * W * G) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma, const __nv_bfloat16* __restrict__ dy,
     const __nv_bfloat16* __restrict__ resid_grad, __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
     float* __restrict__ dbeta, int64_t rows, int hidden, float eps, __nv_bfloat16* __restrict__ drop_out,
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
   const int nvec = hidden >> 3;
   const float inv_h = 1.f / (float)hidden;
   const bool has_resid = resid_grad != nullptr;
-  const int64_t step = (int64_t)gridDim.x * kGroupsPerBlock;
+  const int64_t step = (int64_t)gridDim.x * G;
   float acc_g[kVecPerLane][8], acc_b[kVecPerLane][8];
 #pragma unroll
   for (int j = 0; j < kVecPerLane; ++j)
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
       }
     }
   };
-  int64_t row = (int64_t)blockIdx.x * kGroupsPerBlock + group;
+  int64_t row = (int64_t)blockIdx.x * G + group;
   if (row < rows) fetch(row, rx, rd, rr);
   for (; row < rows; row += step) {
     const int64_t rbase = row * hidden;
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(32 * W * kGroupsPerBlock) ln_bwd_kernel(
     }
   }
   // fold the row groups of this CTA in shared memory, one group at a time
-  for (int gi = 0; gi < kGroupsPerBlock; ++gi) {
+  for (int gi = 0; gi < G; ++gi) {
     if (group == gi) {
 #pragma unroll
       for (int j = 0; j < kVecPerLane; ++j) {
@@ -305,10 +312,10 @@ struct RowLaunch {
 // Grid = every row group resident at once when the occupancy allows, else one full
 // wave of resident CTAs (148 SMs x CTAs per SM) looping over the rows.
 template <typename K>
-static int row_launch(K kernel, int64_t rows, int64_t hidden, int vpl, int param_arrays, RowLaunch* l) {
-  const int W = warps_per_row(hidden, vpl);
-  l->block = 32 * W * kGroupsPerBlock;
-  l->smem = (size_t)param_arrays * hidden * sizeof(float) + (size_t)kGroupsPerBlock * W * 4 * sizeof(float);
+static int row_launch(K kernel, int64_t rows, int64_t hidden, int W, int param_arrays, RowLaunch* l,
+                      int groups_per_block = kGroupsPerBlock) {
+  l->block = 32 * W * groups_per_block;
+  l->smem = (size_t)param_arrays * hidden * sizeof(float) + (size_t)groups_per_block * W * 4 * sizeof(float);
   // The occupancy query and smem attribute are host work on every launch otherwise;
   // cache them per (device, kernel, block, smem).
   static std::mutex mu;
@@ -333,7 +340,7 @@ static int row_launch(K kernel, int64_t rows, int64_t hidden, int vpl, int param
     std::lock_guard<std::mutex> lock(mu);
     cache[key] = per_sm;
   }
-  const int64_t groups = (rows + kGroupsPerBlock - 1) / kGroupsPerBlock;
+  const int64_t groups = (rows + groups_per_block - 1) / groups_per_block;
   const int64_t cap = (int64_t)sm_count_current() * (per_sm > 0 ? per_sm : 1);
   l->grid = (int)(groups < cap ? (groups > 0 ? groups : 1) : cap);
   return PPO_OK;
@@ -362,8 +369,8 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
   int rc = PPO_OK;
   const int vpl = vpl_choice(hidden, 4);
 #define PPO_LN_FWD_W(W, V)                                                                                    \
-  if ((rc = row_launch(ln_fwd_kernel<false, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
-  launch_pdl(ln_fwd_kernel<false, W, V>, l.grid, l.block, l.smem, as_stream(stream),                                  \
+  if ((rc = row_launch(ln_fwd_kernel<false, W, V, fwd_groups_for(W)>, rows, hidden, W, 0, &l, fwd_groups_for(W)))) return rc; \
+  launch_pdl(ln_fwd_kernel<false, W, V, fwd_groups_for(W)>, l.grid, l.block, l.smem, as_stream(stream),                                  \
       nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta, static_cast<__nv_bfloat16*>(y), rows, \
       (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0);
 #define PPO_LN_FWD_V(V)                                               \
@@ -398,8 +405,8 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   int rc = PPO_OK;
   const int vpl = vpl_choice(hidden, 4);
 #define PPO_RES_W(W, V)                                                                                      \
-  if ((rc = row_launch(ln_fwd_kernel<true, W, V>, rows, hidden, V, 0, &l))) return rc;                       \
-  launch_pdl(ln_fwd_kernel<true, W, V>, l.grid, l.block, l.smem, as_stream(stream),                                  \
+  if ((rc = row_launch(ln_fwd_kernel<true, W, V, fwd_groups_for(W)>, rows, hidden, W, 0, &l, fwd_groups_for(W)))) return rc; \
+  launch_pdl(ln_fwd_kernel<true, W, V, fwd_groups_for(W)>, l.grid, l.block, l.smem, as_stream(stream),                                  \
       static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),                   \
       static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps, \
       dropout_threshold(p), 1.f / (1.f - p), seed, offset, offset_base, p > 0.f ? 1 : 0);
@@ -434,29 +441,33 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
   int rc = PPO_OK;
   if (!aligned16(dgamma) || !aligned16(dbeta))
     return set_error(PPO_EINVAL, "ppo_layernorm_bwd: dgamma/dbeta must be 16-byte aligned");
-  const int vpl = vpl_choice(hidden, 2);
-#define PPO_LN_BWD_W(W, V)                                                                                     \
-  if ((rc = row_launch(ln_bwd_kernel<W, V>, rows, hidden, V, 2, &l))) return rc;                              \
-  launch_pdl(ln_bwd_kernel<W, V>, l.grid, l.block, l.smem, as_stream(stream),                                          \
-      static_cast<const __nv_bfloat16*>(x), gamma, static_cast<const __nv_bfloat16*>(dy),                     \
-      static_cast<const __nv_bfloat16*>(resid_grad), static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows,    \
-      (int)hidden, eps, static_cast<__nv_bfloat16*>(drop_out), dropout_threshold(p), p > 0.f ? 1.f / (1.f - p) : 1.f, \
-      drop_seed, drop_offset, drop_offset_base);
-#define PPO_LN_BWD_V(V)                                               \
-  {                                                                   \
-    switch (warps_per_row(hidden, V)) {                               \
-      case 1: PPO_LN_BWD_W(1, V) break;                               \
-      case 2: PPO_LN_BWD_W(2, V) break;                               \
-      case 3: PPO_LN_BWD_W(3, V) break;                               \
-      case 4: PPO_LN_BWD_W(4, V) break;                               \
-      case 5: PPO_LN_BWD_W(5, V) break;                               \
-      case 6: PPO_LN_BWD_W(6, V) break;                               \
-      case 7: PPO_LN_BWD_W(7, V) break;                               \
-      default: PPO_LN_BWD_W(8, V) break;                              \
-    }                                                                 \
+  // Two vectors per lane per tensor (W = h/512 warps per row, up to 16 at h = 8192) and
+  // G = min(4, 16/W) rows per CTA, so 32*W*G threads leave >= 128 registers a thread:
+  // the kernel keeps 3 tensors x 2 vectors double-buffered plus 2 x 16 fp32 parameter-
+  // gradient accumulators in registers, and any smaller budget spills (the previous
+  // fixed 4 rows per CTA spilled 0.7-1.3 KB per thread at h = 4096 / 5120 and ran at
+  // 16% of HBM bandwidth at C4, profiles/r1_ln_bwd_spill_fix.txt).
+  const int need = warps_per_row(hidden, 2);
+#define PPO_LN_BWD_W(W)                                                                                        \
+  {                                                                                                            \
+    constexpr int G = groups_for(W);                                                                           \
+    if ((rc = row_launch(ln_bwd_kernel<W, 2, G>, rows, hidden, W, 2, &l, G))) return rc;                       \
+    launch_pdl(ln_bwd_kernel<W, 2, G>, l.grid, l.block, l.smem, as_stream(stream),                             \
+        static_cast<const __nv_bfloat16*>(x), gamma, static_cast<const __nv_bfloat16*>(dy),                   \
+        static_cast<const __nv_bfloat16*>(resid_grad), static_cast<__nv_bfloat16*>(dx), dgamma, dbeta, rows,  \
+        (int)hidden, eps, static_cast<__nv_bfloat16*>(drop_out), dropout_threshold(p),                        \
+        p > 0.f ? 1.f / (1.f - p) : 1.f, drop_seed, drop_offset, drop_offset_base);                           \
   }
-  PPO_VPL_DISPATCH(vpl, PPO_LN_BWD_V)
-#undef PPO_LN_BWD_V
+  if (need <= 1) PPO_LN_BWD_W(1)
+  else if (need <= 2) PPO_LN_BWD_W(2)
+  else if (need <= 3) PPO_LN_BWD_W(3)
+  else if (need <= 4) PPO_LN_BWD_W(4)
+  else if (need <= 5) PPO_LN_BWD_W(5)
+  else if (need <= 6) PPO_LN_BWD_W(6)
+  else if (need <= 8) PPO_LN_BWD_W(8)
+  else if (need <= 10) PPO_LN_BWD_W(10)
+  else if (need <= 12) PPO_LN_BWD_W(12)
+  else PPO_LN_BWD_W(16)
 #undef PPO_LN_BWD_W
   PPO_LAUNCHED("ln_bwd_kernel");
   return PPO_OK;

@@ -55,7 +55,7 @@ def test_layernorm_fwd(rows, h):
     np.testing.assert_allclose(npf(y), want, rtol=2 ** -8, atol=1e-3 * np.abs(gamma).max())
 
 
-@pytest.mark.parametrize("rows,h,p", [(300, 256, 0.1), (128, 2048, 0.1), (33, 4096, 0.0)])
+@pytest.mark.parametrize("rows,h,p", [(300, 256, 0.1), (128, 2048, 0.1), (33, 4096, 0.0), (45, 5120, 0.1), (20, 8192, 0.1)])
 def test_residual_dropout_ln(rows, h, p):
     rng = np.random.default_rng(h)
     resid = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32))
@@ -73,7 +73,9 @@ def test_residual_dropout_ln(rows, h, p):
     np.testing.assert_allclose(npf(ln), ref.layernorm(npf(out), gamma, beta), rtol=2 ** -7, atol=2e-2)
 
 
-@pytest.mark.parametrize("rows,h,with_resid,p", [(200, 256, True, 0.1), (64, 2048, False, 0.0), (40, 5120, True, 0.1)])
+@pytest.mark.parametrize("rows,h,with_resid,p", [(200, 256, True, 0.1), (64, 2048, False, 0.0), (40, 5120, True, 0.1),
+                                                 (70, 1536, True, 0.0), (300, 4096, True, 0.1), (30, 6144, False, 0.1),
+                                                 (50, 8192, True, 0.1)])
 def test_layernorm_bwd(rows, h, with_resid, p):
     rng = np.random.default_rng(rows + h)
     x = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32) * 2)
