@@ -69,3 +69,27 @@ def test_product_path_refuses_to_run_without_cuda():
         pytest.skip("a GPU is present")
     with pytest.raises(native.NativeUnavailable):
         native.require_cuda()
+
+
+def test_row_kernels_do_not_spill(lib):
+    """Resource usage of the built sm_100a cubins (cuobjdump -res-usage): the LayerNorm
+    backward kernels, at every (warps per row, rows per CTA) the dispatch can pick, keep
+    their double-buffered rows in registers -- a spill cost 4x at h = 5120
+    (profiles/r1_ln_bwd_spill_fix.txt).  The forward kernels at the default 4 vectors
+    per lane spill at most a word."""
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", native.LIB_PATH], capture_output=True, text=True).stdout
+    usage = dict(re.findall(r"Function (\S+):\s*\n\s*(REG:.*)", out))
+    bwd = {f: u for f, u in usage.items() if "ln_bwd_kernel" in f}
+    assert len(bwd) >= 10
+    for f, u in bwd.items():
+        assert "STACK:0 " in u and "LOCAL:0 " in u, (f, u)
+    fwd4 = {f: u for f, u in usage.items() if re.search(r"ln_fwd_kernelILb[01]ELi\d+ELi4E", f)}
+    assert fwd4
+    for f, u in fwd4.items():
+        assert int(re.search(r"STACK:(\d+)", u).group(1)) <= 8, (f, u)
