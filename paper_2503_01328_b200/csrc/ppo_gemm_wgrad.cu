@@ -10,14 +10,10 @@ using namespace ppo::gemm;
 namespace {
 using Acc = cutlass::epilogue::fusion::LinearCombination<float, float, float, float>;
 using Wgrad = Sm100Gemm<ColMajor, RowMajor, float, Acc, TileWide>;
-}  // namespace
+using WgradNarrow = Sm100Gemm<ColMajor, RowMajor, float, Acc, TileNarrow>;
 
-extern "C" {
-
-int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t N, int64_t K, float beta,
-                   void* stream) {
-  using G = Wgrad;
-  if (!dY || !X || !dW || !dims_ok(M, N, K)) return set_error(PPO_EINVAL, "ppo_gemm_wgrad: bad arguments");
+template <class G>
+int wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t N, int64_t K, float beta, void* stream) {
   auto [sa, sb, sc, sd] = G::strides(M, N, K);
   typename G::Args args{cutlass::gemm::GemmUniversalMode::kGemm,
                         {(int)M, (int)N, (int)K, 1},
@@ -27,6 +23,19 @@ int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t 
   args.epilogue.thread.alpha = 1.f;
   args.epilogue.thread.beta = beta;
   return launch<G>(PPO_GEMM_OP_WGRAD, args, stream, "ppo_gemm_wgrad");
+}
+}  // namespace
+
+extern "C" {
+
+int ppo_gemm_wgrad(const void* dY, const void* X, float* dW, int64_t M, int64_t N, int64_t K, float beta,
+                   void* stream) {
+  if (!dY || !X || !dW || !dims_ok(M, N, K)) return set_error(PPO_EINVAL, "ppo_gemm_wgrad: bad arguments");
+  static const bool narrow = [] {
+    const char* e = std::getenv("PPO_WGRAD_TILE");  // A/B experiment: 256x128 tiles
+    return e && e[0] == 'n';
+  }();
+  return narrow ? wgrad<WgradNarrow>(dY, X, dW, M, N, K, beta, stream) : wgrad<Wgrad>(dY, X, dW, M, N, K, beta, stream);
 }
 
 }  // extern "C"
