@@ -20,6 +20,9 @@ ap.add_argument("--policy", default="full")
 ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=0)
 ap.add_argument("--schedule", default="1f1b", choices=("1f1b", "gis-h", "po"))
+# fixed backends: the measured per-shape choice ("auto") is meaningless under a profiler
+ap.add_argument("--gemm", default="best", choices=("auto", "best", "tcgen05", "cublas"))
+ap.add_argument("--attn", default="cudnn", choices=("auto", "tcgen05", "cudnn"))
 a = ap.parse_args()
 cfg = ModelConfig(n_layers=24, hidden=2048, heads=16, seq=4096, vocab=50304)
 costs = PassCosts(Fraction(447), Fraction(1045), Fraction(0), Fraction(32))  # measured per layer (us)
@@ -31,7 +34,7 @@ else:  # split backward at v = 3 (1-layer chunks), as in the bench
     c1 = measured_pass_costs(0.42e-3, 0.6e-3, 0.4e-3, 30e-6)
     sched = (build_gis_h if a.schedule == "gis-h" else build_po)(8, 3, 32, c1)
 plan = plan_slots(sched, (0,), Fraction(17750)) if a.policy == "full" and a.schedule == "1f1b" else None
-res = execute(sched, plan, model=cfg, mode="emulate", rank=0, iters=a.iters, warmup=a.warmup)
+res = execute(sched, plan, model=cfg, mode="emulate", rank=0, iters=a.iters, warmup=a.warmup, gemm=a.gemm, attn=a.attn)
 print("iteration ms", [round(x * 1e3, 2) for x in res.iteration_seconds])
 if a.iters > 1 or a.warmup:
     import statistics
