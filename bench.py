@@ -417,6 +417,9 @@ def run_b200(args, rank, world, local_rank):
             results[name] = dict(results["none_cublas"] if backend == "cublas" else results["none"],
                                  note="k-aware policy keeps everything resident at this k")
             continue
+        if name == "none_tcgen05_attn" and (cfg.head_dim not in (64, 128) or s % 256):
+            results[name] = dict(results["none"], note="tcgen05 attention forward needs head_dim 64/128, seq % 256 == 0")
+            continue
         if name == "full" and rank == 0:
             sampler = ClockSampler(local_rank)
             sampler.__enter__()
