@@ -74,6 +74,10 @@ def run_point(h, s, m, d, iters, warmup, dev):
     for name in [n for n in ("full", "auto", "partial") if n in out]:
         out[name]["overhead_pct"] = 100 * (base / out[name]["tokens_per_s"] - 1)
     out["auto_stride"] = choice.stride
+    from paper_2503_01328_b200.runtime import gemm_tune
+
+    out["attn_backend"] = gemm_tune.attn_decisions()
+    out["gemm_backend"] = gemm_tune.decisions()
     return out
 
 
