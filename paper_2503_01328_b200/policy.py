@@ -10,6 +10,14 @@ searches the microbatch density instead: for stride q = 1, 2, ... it offloads
 every q-th microbatch of the chosen stages, simulates the result with the
 measured costs, and returns the plan with the lowest peak whose modelled
 makespan stays within ``tolerance`` of no offload (and has no late reloads).
+
+``choose_offload_measured`` closes the loop with the device: the runner model does
+not price the compute slowdown under concurrent DMA nor the duplex link rate, and at
+k ~ 1.1-2.7 the plan it accepts at 5% modelled overhead measures 5-8% (C5 sweep,
+DESIGN.md section 9).  It walks the same candidates from the least memory up, measures
+each (``measure(plan)`` -> overhead fraction), and keeps the first whose *measured*
+overhead is within tolerance; candidates whose modelled overhead already exceeds the
+measured-to-modelled gap seen so far are skipped without a run.
 """
 
 from __future__ import annotations
@@ -70,6 +78,64 @@ def choose_offload(
         if score(peaks) < score(best.peak_units):
             best = PolicyChoice(plan, q, tr.makespan, base.makespan, peaks, base_peaks, len(plan.offloaded_pairs()))
     return best
+
+
+def offload_candidates_by_memory(sched: Schedule, stages, t_o: Fraction, focus_rank: int | None = None,
+                                 stream_mode: str = "single", max_stride: int | None = None) -> list[PolicyChoice]:
+    """Every stride plan without late reloads that offloads something, least memory
+    (peak at ``focus_rank``, else the max over ranks) first, then least modelled time."""
+    base = simulate(sched, stream_mode=stream_mode)
+    base_peaks = _peaks(base)
+    out = []
+    for q in range(1, (max_stride or sched.microbatches) + 1):
+        pairs = {(s, j) for s in range(sched.num_stages) for j in range(sched.microbatches) if j % q == 0}
+        plan = plan_slots(sched, stages, t_o, pairs=pairs)
+        if plan.late_list() or not plan.offloaded_pairs():
+            continue
+        tr = simulate(sched, plan, stream_mode=stream_mode)
+        out.append(PolicyChoice(plan, q, tr.makespan, base.makespan, _peaks(tr), base_peaks,
+                                len(plan.offloaded_pairs())))
+
+    def key(c):
+        pk = c.peak_units[focus_rank] if focus_rank is not None else max(c.peak_units)
+        return (pk, c.makespan)
+
+    return sorted(out, key=key)
+
+
+@dataclass(frozen=True)
+class MeasuredChoice:
+    choice: PolicyChoice | None  # None: nothing measured within tolerance (keep everything resident)
+    measured_overhead: float | None
+    trials: tuple  # (stride, modelled overhead, measured overhead) per run, in order
+
+
+def choose_offload_measured(sched: Schedule, stages, t_o: Fraction, measure, tolerance: float = 0.05,
+                            focus_rank: int | None = None, stream_mode: str = "single",
+                            max_stride: int | None = None, max_trials: int = 4,
+                            model_tolerance: float = 0.25) -> MeasuredChoice:
+    """Least-memory stride plan whose *measured* overhead is within ``tolerance``.
+
+    ``measure(plan) -> float`` runs the plan on the device and returns its overhead
+    versus no offload.  Candidates are tried least memory first, at most
+    ``max_trials`` runs; one whose modelled overhead alone exceeds ``model_tolerance``
+    is never run, and after each miss the candidates whose modelled overhead plus the
+    smallest measured-minus-modelled gap seen so far exceeds ``tolerance`` are skipped."""
+    cands = [c for c in offload_candidates_by_memory(sched, stages, t_o, focus_rank, stream_mode, max_stride)
+             if c.overhead <= model_tolerance]
+    trials = []
+    gap = None
+    for c in cands:
+        if len(trials) >= max_trials:
+            break
+        if gap is not None and c.overhead + gap > tolerance:
+            continue
+        m = float(measure(c.plan))
+        trials.append((c.stride, c.overhead, m))
+        if m <= tolerance:
+            return MeasuredChoice(c, m, tuple(trials))
+        gap = m - c.overhead if gap is None else min(gap, m - c.overhead)
+    return MeasuredChoice(None, None, tuple(trials))
 
 
 @dataclass(frozen=True)

@@ -1,0 +1,65 @@
+"""k-aware policy with measured feedback (policy.choose_offload_measured), against a
+synthetic device whose measured overhead is the runner model's plus a fixed gap."""
+from fractions import Fraction
+
+import pytest
+
+import paper_2503_01328_b200 as po
+from paper_2503_01328_b200.policy import choose_offload, choose_offload_measured, offload_candidates_by_memory
+from paper_2503_01328_b200.sim import simulate
+
+
+def _setup():
+    costs = po.measured_pass_costs(2.27e-3, 5.44e-3, 0.0, 50e-6)  # C5 h=8192 s=2048 per-layer costs
+    sched = po.build_1f1b(8, 1, 16, costs)
+    t_o = Fraction(12130, 1_000_000)  # k ~ 1.5
+    return sched, t_o
+
+
+def _modelled(sched, plan):
+    base = simulate(sched).makespan
+    return float(simulate(sched, plan).makespan / base - 1)
+
+
+def test_candidates_sorted_by_memory_then_time():
+    sched, t_o = _setup()
+    cands = offload_candidates_by_memory(sched, (0,), t_o, focus_rank=0)
+    assert cands
+    keys = [(c.peak_units[0], c.makespan) for c in cands]
+    assert keys == sorted(keys)
+    assert all(not c.plan.late_list() and c.plan.offloaded_pairs() for c in cands)
+
+
+@pytest.mark.parametrize("gap", [0.02, 0.045, 0.06])
+def test_measured_choice_meets_the_measured_budget(gap):
+    sched, t_o = _setup()
+    calls = []
+
+    def measure(plan):  # the device is `gap` slower than the model
+        calls.append(plan)
+        return _modelled(sched, plan) + gap
+
+    got = choose_offload_measured(sched, (0,), t_o, measure, tolerance=0.05, focus_rank=0)
+    assert len(calls) == len(got.trials) <= 4
+    if got.choice is not None:
+        assert got.measured_overhead <= 0.05
+        # no candidate with less memory measures within budget
+        for c in offload_candidates_by_memory(sched, (0,), t_o, focus_rank=0):
+            if c.peak_units[0] < got.choice.peak_units[0]:
+                assert _modelled(sched, c.plan) + gap > 0.05
+    if gap > 0.05:
+        assert got.choice is None and len(calls) == 1  # one miss shows every candidate is over budget
+    # the model-only policy may pick a plan the synthetic device measures above budget
+    model_only = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
+    if model_only.plan is not None and got.choice is not None:
+        assert got.choice.peak_units[0] >= model_only.peak_units[0]
+
+
+def test_measured_choice_without_gap_equals_model_choice():
+    sched, t_o = _setup()
+    got = choose_offload_measured(sched, (0,), t_o, lambda plan: _modelled(sched, plan), tolerance=0.05,
+                                  focus_rank=0, max_trials=100)
+    want = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
+    assert (got.choice is None) == (want.plan is None)
+    if want.plan is not None:
+        assert got.choice.peak_units[0] == want.peak_units[0]

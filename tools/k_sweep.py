@@ -23,14 +23,14 @@ import torch  # noqa: E402
 
 from paper_2503_01328_b200.runtime.calibrate import calibrate  # noqa: E402
 from paper_2503_01328_b200 import build_1f1b, measured_pass_costs, plan_slots  # noqa: E402
-from paper_2503_01328_b200.policy import choose_offload, choose_partial_offload  # noqa: E402
+from paper_2503_01328_b200.policy import choose_offload, choose_offload_measured, choose_partial_offload  # noqa: E402
 from paper_2503_01328_b200.runtime.layout import make_layout, offload_candidates  # noqa: E402
 from paper_2503_01328_b200.runtime import native  # noqa: E402
 from paper_2503_01328_b200.runtime.executor import execute  # noqa: E402
 from paper_2503_01328_b200.runtime.model import ModelConfig, Stage  # noqa: E402
 
 
-def run_point(h, s, m, d, iters, warmup, dev):
+def run_point(h, s, m, d, iters, warmup, dev, args_measured=False):
     heads = h // 128
     cfg = ModelConfig(n_layers=d, hidden=h, heads=heads, seq=s, vocab=1024)
     st = Stage(cfg, 1, d, m, dev, layers=[0])  # a middle stage: no embedding / head
@@ -74,6 +74,26 @@ def run_point(h, s, m, d, iters, warmup, dev):
     for name in [n for n in ("full", "auto", "partial") if n in out]:
         out[name]["overhead_pct"] = 100 * (base / out[name]["tokens_per_s"] - 1)
     out["auto_stride"] = choice.stride
+    if args_measured:
+        # closed loop: stride plans least memory first, each measured, first within 5% kept
+        runs = {}
+
+        def measure(plan):
+            res = execute(sched, plan, model=cfg, mode="emulate", rank=0, device=dev, iters=iters, warmup=warmup,
+                          optimizer="sgd", stream_mode="single", iteration_graph=True)
+            it = statistics.median(res.iteration_seconds)
+            runs[id(plan)] = {"tokens_per_s": m * s / it, "ms_per_step": it * 1e3, "peak_slabs": res.programs[0].n_slabs,
+                              "peak_act_gb": res.act_bytes[0] / 1e9}
+            res.close()
+            gc.collect()
+            torch.cuda.empty_cache()
+            return base / (m * s / it) - 1
+
+        mc = choose_offload_measured(sched, (0,), t_o, measure, tolerance=0.05, focus_rank=0)
+        out["auto_measured"] = dict(runs[id(mc.choice.plan)], overhead_pct=100 * mc.measured_overhead,
+                                    stride=mc.choice.stride) if mc.choice else dict(out["none"], note="nothing within 5% measured")
+        out["auto_measured"]["trials"] = [{"stride": q, "modelled_pct": 100 * a, "measured_pct": 100 * b}
+                                          for q, a, b in mc.trials]
     from paper_2503_01328_b200.runtime import gemm_tune
 
     out["attn_backend"] = gemm_tune.attn_decisions()
@@ -89,6 +109,7 @@ def main():
     ap.add_argument("--d", type=int, default=8)
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--measured", action="store_true", help="also run the closed-loop policy (choose_offload_measured)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
@@ -97,7 +118,7 @@ def main():
         for h in map(int, a.hs.split(",")):
             for s in map(int, a.ss.split(",")):
                 try:
-                    r = run_point(h, s, a.m, a.d, a.iters, a.warmup, dev)
+                    r = run_point(h, s, a.m, a.d, a.iters, a.warmup, dev, a.measured)
                 except Exception as exc:  # keep sweeping; record the failure
                     r = {"h": h, "s": s, "error": repr(exc)[:300]}
                     torch.cuda.empty_cache()
