@@ -82,10 +82,14 @@ def choose_offload(
 
 def offload_candidates_by_memory(sched: Schedule, stages, t_o: Fraction, focus_rank: int | None = None,
                                  stream_mode: str = "single", max_stride: int | None = None) -> list[PolicyChoice]:
-    """Every stride plan without late reloads that offloads something, least memory
-    (peak at ``focus_rank``, else the max over ranks) first, then least modelled time."""
+    """Every stride plan without late reloads that lowers the peak (at ``focus_rank``,
+    else the max over ranks), least memory first, then least modelled time."""
     base = simulate(sched, stream_mode=stream_mode)
     base_peaks = _peaks(base)
+
+    def score(peaks):
+        return peaks[focus_rank] if focus_rank is not None else max(peaks)
+
     out = []
     for q in range(1, (max_stride or sched.microbatches) + 1):
         pairs = {(s, j) for s in range(sched.num_stages) for j in range(sched.microbatches) if j % q == 0}
@@ -93,14 +97,11 @@ def offload_candidates_by_memory(sched: Schedule, stages, t_o: Fraction, focus_r
         if plan.late_list() or not plan.offloaded_pairs():
             continue
         tr = simulate(sched, plan, stream_mode=stream_mode)
-        out.append(PolicyChoice(plan, q, tr.makespan, base.makespan, _peaks(tr), base_peaks,
-                                len(plan.offloaded_pairs())))
-
-    def key(c):
-        pk = c.peak_units[focus_rank] if focus_rank is not None else max(c.peak_units)
-        return (pk, c.makespan)
-
-    return sorted(out, key=key)
+        peaks = _peaks(tr)
+        if score(peaks) < score(base_peaks):
+            out.append(PolicyChoice(plan, q, tr.makespan, base.makespan, peaks, base_peaks,
+                                    len(plan.offloaded_pairs())))
+    return sorted(out, key=lambda c: (score(c.peak_units), c.makespan))
 
 
 @dataclass(frozen=True)
@@ -119,22 +120,25 @@ def choose_offload_measured(sched: Schedule, stages, t_o: Fraction, measure, tol
     ``measure(plan) -> float`` runs the plan on the device and returns its overhead
     versus no offload.  Candidates are tried least memory first, at most
     ``max_trials`` runs; one whose modelled overhead alone exceeds ``model_tolerance``
-    is never run, and after each miss the candidates whose modelled overhead plus the
-    smallest measured-minus-modelled gap seen so far exceeds ``tolerance`` are skipped."""
+    is never run.  After each miss the unmodelled cost is taken as proportional to the
+    traffic (measured-minus-modelled overhead per offloaded pair, the smallest seen so
+    far), and candidates predicted above ``tolerance`` by it are skipped: the device
+    pays for concurrent DMA even where the model schedules the copies for free."""
     cands = [c for c in offload_candidates_by_memory(sched, stages, t_o, focus_rank, stream_mode, max_stride)
              if c.overhead <= model_tolerance]
     trials = []
-    gap = None
+    per_pair = None  # unmodelled overhead per offloaded pair
     for c in cands:
         if len(trials) >= max_trials:
             break
-        if gap is not None and c.overhead + gap > tolerance:
+        if per_pair is not None and c.overhead + per_pair * c.offloaded_pairs > tolerance:
             continue
         m = float(measure(c.plan))
         trials.append((c.stride, c.overhead, m))
         if m <= tolerance:
             return MeasuredChoice(c, m, tuple(trials))
-        gap = m - c.overhead if gap is None else min(gap, m - c.overhead)
+        g = max(0.0, m - c.overhead) / c.offloaded_pairs
+        per_pair = g if per_pair is None else min(per_pair, g)
     return MeasuredChoice(None, None, tuple(trials))
 
 

@@ -28,6 +28,7 @@ def test_candidates_sorted_by_memory_then_time():
     keys = [(c.peak_units[0], c.makespan) for c in cands]
     assert keys == sorted(keys)
     assert all(not c.plan.late_list() and c.plan.offloaded_pairs() for c in cands)
+    assert all(c.peak_units[0] < c.base_peak_units[0] for c in cands)  # every candidate saves memory
 
 
 @pytest.mark.parametrize("gap", [0.02, 0.045, 0.06])
@@ -35,9 +36,9 @@ def test_measured_choice_meets_the_measured_budget(gap):
     sched, t_o = _setup()
     calls = []
 
-    def measure(plan):  # the device is `gap` slower than the model
+    def measure(plan):  # the device pays `gap` per 8 offloaded pairs beyond the model
         calls.append(plan)
-        return _modelled(sched, plan) + gap
+        return _modelled(sched, plan) + gap * len(plan.offloaded_pairs()) / 8
 
     got = choose_offload_measured(sched, (0,), t_o, measure, tolerance=0.05, focus_rank=0)
     assert len(calls) == len(got.trials) <= 4
@@ -46,9 +47,7 @@ def test_measured_choice_meets_the_measured_budget(gap):
         # no candidate with less memory measures within budget
         for c in offload_candidates_by_memory(sched, (0,), t_o, focus_rank=0):
             if c.peak_units[0] < got.choice.peak_units[0]:
-                assert _modelled(sched, c.plan) + gap > 0.05
-    if gap > 0.05:
-        assert got.choice is None and len(calls) == 1  # one miss shows every candidate is over budget
+                assert _modelled(sched, c.plan) + gap * len(c.plan.offloaded_pairs()) / 8 > 0.05
     # the model-only policy may pick a plan the synthetic device measures above budget
     model_only = choose_offload(sched, (0,), t_o, tolerance=0.05, focus_rank=0)
     if model_only.plan is not None and got.choice is not None:
