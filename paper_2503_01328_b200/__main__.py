@@ -44,8 +44,8 @@ def _offload_count(spec, v: int) -> int | str:
         return (v + 1) // 2
     if spec == "full":
         return v
-    if spec == "auto":
-        return "auto"
+    if spec in ("auto", "auto-measured"):
+        return spec
     n = int(spec)
     if not 0 <= n <= v:
         raise SystemExit(f"offload count {n} outside [0, {v}]")
@@ -78,6 +78,8 @@ def _plan(sched, d, v, costs, t_o, offload, planner="slots", t_duplex=None):
     block = po_block(d, v, costs)
     if n == "auto":
         return choose_offload(sched, select_offload_stages(block, 1), t_o).plan
+    if n == "auto-measured":  # resolved by cmd_run against the device (needs runs)
+        return None
     stages = select_offload_stages(block, n)
     if planner == "duplex":
         return plan_slots_duplex(sched, stages, t_duplex if t_duplex is not None else t_o / 2)
@@ -133,6 +135,27 @@ def cmd_run(args) -> int:
     sched = _build(args.schedule, args.d, args.v, args.m, args.g, costs)
     t_dup = Fraction(round(cal["t_duplex"] * 1e6), 1_000_000) if cal.get("t_duplex") else None
     plan = _plan(sched, args.d, args.v, costs, t_o, args.offload, args.planner, t_dup)
+    closed_loop = None
+    if args.offload == "auto-measured":
+        if world > 1:
+            raise SystemExit("--offload auto-measured runs candidates on one process (--mode emulate|virtual)")
+        from .policy import choose_offload_measured
+
+        def _iter_s(p):
+            r = execute(sched, p, model=cfg, mode=mode, rank=rank, device=dev, iters=args.iters,
+                        warmup=args.warmup, stream_mode=args.stream_mode, optimizer=args.optimizer,
+                        iteration_graph=args.iteration_graph)
+            t = max(r.iteration_seconds)
+            r.close()
+            return t
+
+        t_base = _iter_s(None)
+        mc = choose_offload_measured(sched, select_offload_stages(po_block(args.d, args.v, costs), 1), t_o,
+                                     lambda p: _iter_s(p) / t_base - 1, stream_mode=args.stream_mode,
+                                     focus_rank=rank)
+        plan = mc.choice.plan if mc.choice else None
+        closed_loop = {"trials": [{"stride": q, "modelled_pct": 100 * a, "measured_pct": 100 * b} for q, a, b in mc.trials],
+                       "chosen_stride": mc.choice.stride if mc.choice else None}
     res = execute(sched, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.iters, warmup=args.warmup,
                   stream_mode=args.stream_mode, optimizer=args.optimizer, iteration_graph=args.iteration_graph,
                   spare_slabs=args.spare_slabs)
@@ -147,7 +170,8 @@ def cmd_run(args) -> int:
                    k_measured=float(t_o / (costs.total * units)), calibration=cal,
                    predicted_makespan_s=float(predicted.makespan), measured_makespan_s=float(trace.makespan),
                    model_error_pct=100 * (float(trace.makespan) / float(predicted.makespan) - 1),
-                   offloaded_stages=list(plan.stages) if plan else [], losses=res.losses)
+                   offloaded_stages=list(plan.stages) if plan else [], losses=res.losses,
+                   closed_loop=closed_loop)
     if rank == 0:
         _write(args.out, f"{sched.kind}.schedule", emit_schedule(sched))
         if plan:
@@ -174,7 +198,8 @@ def make_parser() -> argparse.ArgumentParser:
         p.add_argument("--v", type=int, default=1)
         p.add_argument("--m", type=int, default=8)
         p.add_argument("--g", type=int, default=None)
-        p.add_argument("--offload", default="none", help="none | half | full | N | auto")
+        p.add_argument("--offload", default="none",
+                       help="none | half | full | N | auto | auto-measured (run: closed-loop k-aware policy)")
         p.add_argument("--out", default="out")
     plan = sub.choices["plan"]
     plan.add_argument("--costs", default="1,1,1", help="tF,tB,tW[,comm]")

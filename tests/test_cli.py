@@ -57,3 +57,23 @@ def test_run_virtual_pipeline(tmp_path):
     assert (out / "gis-h-trace.csv").read_text().startswith("device,stage,microbatch,kind")
     assert (out / "gis-h.svg").read_text().startswith("<svg")
     assert summary["predicted_makespan_s"] > 0 and summary["measured_makespan_s"] > 0
+
+
+@pytest.mark.gpu
+def test_run_closed_loop_policy(tmp_path):
+    """``run --offload auto-measured``: candidates measured on the device, the choice and
+    every trial in the summary; a chosen plan measured within the 5% budget."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("needs a CUDA device")
+    out = tmp_path / "c"
+    res = subprocess.run([sys.executable, "-m", "paper_2503_01328_b200", "run", "--schedule", "1f1b", "--d", "4",
+                          "--m", "8", "--layers", "4", "--mode", "emulate", "--offload", "auto-measured",
+                          "--iters", "1", "--warmup", "1", "--out", str(out)], cwd=ROOT, capture_output=True,
+                         text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    summary = json.loads(res.stdout.strip().splitlines()[-1])
+    cl = summary["closed_loop"]
+    assert isinstance(cl["trials"], list) and len(cl["trials"]) <= 4
+    if cl["chosen_stride"] is not None:
+        assert cl["trials"][-1]["stride"] == cl["chosen_stride"] and cl["trials"][-1]["measured_pct"] <= 5.0
