@@ -411,7 +411,8 @@ def run_b200(args, rank, world, local_rank):
     backend = "auto"  # GEMM backend of every policy after the two no-offload runs: the faster one end to end
     for name in ("none", "none_cublas", "none_tcgen05_attn", "auto", "full", "full_single", "full_duplex"):
         plan = plans["full" if name == "full_single" else ("none" if name.startswith("none") else name)]
-        if name == "auto" and results["none_cublas"]["tokens_per_s"] > results["none"]["tokens_per_s"]:
+        # all-cuBLAS only when it beats the per-shape measured mix by more than run-to-run noise
+        if name == "auto" and results["none_cublas"]["tokens_per_s"] > 1.01 * results["none"]["tokens_per_s"]:
             backend = "cublas"
         if name == "auto" and plan is None:
             results[name] = dict(results["none_cublas"] if backend == "cublas" else results["none"],
@@ -554,7 +555,7 @@ def run_b200(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 4},
         "gpu_launches": launches.get("full"),
         "gemm_backend": {"policies": "tcgen05/cuBLAS per shape (gemm=auto)" if backend == "auto"
-                         else "cuBLAS (faster end to end than gemm=auto in this run)",
+                         else "cuBLAS (faster end to end than gemm=auto by > 1% in this run)",
                          "per_shape": gemm_decisions()},
         "attn_backend": {"policies": "attention forward: tcgen05 (ours) or cuDNN + K1 pack, measured per shape "
                                      "(attn=auto); backward: cuDNN", "per_shape": attn_decisions()},
