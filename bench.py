@@ -391,6 +391,7 @@ def run_b200(args, rank, world, local_rank):
     # and PO, without offload and with the reference's selective plan n=1
     # (select_offload_stages(po_block(d, v), 1), cli.py:159-160) on duplex copy streams
     sched_variants = {}
+    gish_closed_loop = {}
     if args.schedules and layers_per_stage > 1 and world == 1:
         from paper_2503_01328_b200 import build_gis_h, build_po, po_block, select_offload_stages
 
@@ -403,6 +404,8 @@ def run_b200(args, rank, world, local_rank):
             st = select_offload_stages(po_block(d, v, c1), 1)
             sched_variants[f"{kind}_v{v}_none"] = (sv, None, "single")
             sched_variants[f"{kind}_v{v}_n1_duplex"] = (sv, plan_slots_duplex(sv, st, w1), "dual")
+            if kind == "gis-h":
+                gish_closed_loop["gis-h"] = (sv, st, w1)
 
     tokens = torch.randint(0, vocab, (m, s + 1), generator=torch.Generator().manual_seed(0)).pin_memory()
     results = {}
@@ -487,6 +490,35 @@ def run_b200(args, rank, world, local_rank):
         del res
         gc.collect()
         torch.cuda.empty_cache()
+    if sched_variants and "gis-h" in gish_closed_loop:
+        # closed loop on the paper's schedule: selective n=1 stride plans on duplex streams,
+        # least memory first, each measured against 1F1B without offload, first within 5% kept
+        from paper_2503_01328_b200.policy import choose_offload_measured
+
+        sv, st_sel, w1_ = gish_closed_loop["gis-h"]
+        base_tps = (results["none_cublas"] if backend == "cublas" else results["none"])["tokens_per_s"]
+        runs = {}
+
+        def measure(plan):
+            r = execute(sv, plan, model=cfg, mode=mode, rank=rank, device=dev, iters=args.steps, warmup=args.warmup,
+                        tokens=tokens, optimizer="sgd", stream_mode="dual", iteration_graph=args.iteration_graph,
+                        gemm=backend)
+            runs[id(plan)] = dict(policy_report(r, sv, plan, m, s, r.slab_bytes, rank), schedule=sv.kind,
+                                  v=sv.local_stages, stream_mode="dual")
+            r.close()
+            gc.collect()
+            torch.cuda.empty_cache()
+            return base_tps / runs[id(plan)]["tokens_per_s"] - 1
+
+        mc = choose_offload_measured(sv, st_sel, 2 * w1_, measure, tolerance=0.05, focus_rank=0, stream_mode="dual",
+                                     planner=lambda sc, st_, t, pairs: plan_slots_duplex(sc, st_, t / 2, pairs=pairs))
+        name = f"gis-h_v{sv.local_stages}_closed_loop"
+        trials = [{"stride": q, "modelled_pct": round(100 * a, 2), "measured_pct": round(100 * b, 2)} for q, a, b in mc.trials]
+        if mc.choice is not None:
+            results[name] = dict(runs[id(mc.choice.plan)], stride=mc.choice.stride, trials=trials)
+            sched_variants[name] = None
+        else:
+            results["gis-h_closed_loop_trials"] = trials
     full, auto, single = results["full"], results["auto"], results["full_single"]
     # the no-offload baseline every overhead is quoted against: the faster GEMM backend
     none = results["none_cublas"] if backend == "cublas" else results["none"]
@@ -585,6 +617,7 @@ def run_b200(args, rank, world, local_rank):
             "t_duplex_oneway_ms": cal["t_duplex"] * 1e3,
             "partial_candidates": [results[f"partial{i}"] for i in range(len(partial))],
             "schedules": {k: results[k] for k in sched_variants},
+            "gis-h_closed_loop_trials": results.get("gis-h_closed_loop_trials"),
         },
     }
     # k-aware partial offload: the least-memory measured candidate within 5% of no offload

@@ -81,9 +81,13 @@ def choose_offload(
 
 
 def offload_candidates_by_memory(sched: Schedule, stages, t_o: Fraction, focus_rank: int | None = None,
-                                 stream_mode: str = "single", max_stride: int | None = None) -> list[PolicyChoice]:
+                                 stream_mode: str = "single", max_stride: int | None = None,
+                                 planner=None) -> list[PolicyChoice]:
     """Every stride plan without late reloads that lowers the peak (at ``focus_rank``,
-    else the max over ranks), least memory first, then least modelled time."""
+    else the max over ranks), least memory first, then least modelled time.
+    ``planner(sched, stages, t_o, pairs)`` builds a plan (default ``plan_slots``; e.g.
+    ``plan_slots_duplex`` with its one-way width for dual copy streams)."""
+    planner = planner or (lambda sc, st, t, pairs: plan_slots(sc, st, t, pairs=pairs))
     base = simulate(sched, stream_mode=stream_mode)
     base_peaks = _peaks(base)
 
@@ -93,7 +97,7 @@ def offload_candidates_by_memory(sched: Schedule, stages, t_o: Fraction, focus_r
     out = []
     for q in range(1, (max_stride or sched.microbatches) + 1):
         pairs = {(s, j) for s in range(sched.num_stages) for j in range(sched.microbatches) if j % q == 0}
-        plan = plan_slots(sched, stages, t_o, pairs=pairs)
+        plan = planner(sched, stages, t_o, pairs)
         if plan.late_list() or not plan.offloaded_pairs():
             continue
         tr = simulate(sched, plan, stream_mode=stream_mode)
@@ -114,7 +118,7 @@ class MeasuredChoice:
 def choose_offload_measured(sched: Schedule, stages, t_o: Fraction, measure, tolerance: float = 0.05,
                             focus_rank: int | None = None, stream_mode: str = "single",
                             max_stride: int | None = None, max_trials: int = 4,
-                            model_tolerance: float = 0.25) -> MeasuredChoice:
+                            model_tolerance: float = 0.25, planner=None) -> MeasuredChoice:
     """Least-memory stride plan whose *measured* overhead is within ``tolerance``.
 
     ``measure(plan) -> float`` runs the plan on the device and returns its overhead
@@ -124,7 +128,7 @@ def choose_offload_measured(sched: Schedule, stages, t_o: Fraction, measure, tol
     traffic (measured-minus-modelled overhead per offloaded pair, the smallest seen so
     far), and candidates predicted above ``tolerance`` by it are skipped: the device
     pays for concurrent DMA even where the model schedules the copies for free."""
-    cands = [c for c in offload_candidates_by_memory(sched, stages, t_o, focus_rank, stream_mode, max_stride)
+    cands = [c for c in offload_candidates_by_memory(sched, stages, t_o, focus_rank, stream_mode, max_stride, planner)
              if c.overhead <= model_tolerance]
     trials = []
     per_pair = None  # unmodelled overhead per offloaded pair
