@@ -1,8 +1,9 @@
 """Recompute/pack kernels at a transformer shape, timed exactly as bench.py does
 (graph replay of 16 launches over rotating inputs larger than L2, CUDA events on the
-replay stream).  Run once per PPO_LN_MODE (tma | reg) to compare LayerNorm paths.
+replay stream).  PPO_LN_VPL=2|4|8 overrides the forward kernels' vectors per lane
+(A/B runs; the TMA-staged LayerNorm variant this tool once compared was removed).
 
-usage: PPO_LN_MODE=tma python tools/kernel_probe.py [--s 4096 --h 2048 --heads 16]"""
+usage: python tools/kernel_probe.py [--s 4096 --h 2048 --heads 16]"""
 import argparse
 import json
 import os
@@ -26,5 +27,5 @@ peak, kind, _ = bench.measured_peaks()
 res = bench.measure_kernels(a.s, a.h, a.heads, dev, torch, native)
 out = {k: {"us": round(v["avg_us"], 2), "GBps": round(v["bytes_per_launch"] / v["avg_us"] / 1e3, 1),
            "frac": round(v["bytes_per_launch"] / v["avg_us"] / 1e3 / peak, 3)} for k, v in res.items()}
-print(json.dumps({"mode": os.environ.get("PPO_LN_MODE", "tma"), "s": a.s, "h": a.h, "peak_gbs": peak,
+print(json.dumps({"ln_vpl": os.environ.get("PPO_LN_VPL", "default"), "s": a.s, "h": a.h, "peak_gbs": peak,
                   "peak_source": kind, "kernels": out}))
