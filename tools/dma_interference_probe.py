@@ -49,17 +49,19 @@ def timed(n=50):
 
 
 out = {}
-for mode in ("alone", "with_duplex_dma", "alone", "with_duplex_dma"):
+for mode in ("alone", "with_duplex_dma", "with_d2h_dma", "with_h2d_dma") * 2:
     torch.cuda.synchronize()
-    if mode == "with_duplex_dma":
+    if mode != "alone":
         for _ in range(8):
-            with torch.cuda.stream(s1):
-                hd.copy_(dd, non_blocking=True)
-            with torch.cuda.stream(s2):
-                dh.copy_(hh, non_blocking=True)
+            if mode in ("with_duplex_dma", "with_d2h_dma"):
+                with torch.cuda.stream(s1):
+                    hd.copy_(dd, non_blocking=True)
+            if mode in ("with_duplex_dma", "with_h2d_dma"):
+                with torch.cuda.stream(s2):
+                    dh.copy_(hh, non_blocking=True)
     e0, e1, n = timed()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / n
     out[mode] = min(out.get(mode, 1e9), us)
 print(json.dumps({"kind": KIND, "compute_step_us": {k: round(v, 2) for k, v in out.items()},
-                  "slowdown_pct": round(100 * (out["with_duplex_dma"] / out["alone"] - 1), 2)}))
+                  "slowdown_pct": {k: round(100 * (v / out["alone"] - 1), 2) for k, v in out.items() if k != "alone"}}))
