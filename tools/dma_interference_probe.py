@@ -1,6 +1,6 @@
 """Does concurrent host-link DMA slow the compute stream?  A C2-shaped compute loop
 (PROBE_KIND=mix: fc1 GEMM + GeLU + LayerNorm; gemm: the tcgen05 GEMM alone; hbm: the
-HBM-bound LayerNorm + GeLU alone; libppo_b200 kernels) timed alone and
+HBM-bound LayerNorm + GeLU alone; ln / gelu / lnbwd: one kernel; libppo_b200 kernels) timed alone and
 while D2H and H2D of 504 MB slabs run back to back on two copy streams (CUDA events on
 the compute stream, best of 5 of 50 iterations)."""
 import json
@@ -16,7 +16,7 @@ dev = torch.device("cuda:0")
 bf = dict(device=dev, dtype=torch.bfloat16)
 s, h = 4096, 2048
 a, w, f, g = torch.randn(s, h, **bf), torch.randn(4 * h, h, **bf), torch.empty(s, 4 * h, **bf), torch.empty(s, 4 * h, **bf)
-x, y = torch.randn(s, h, **bf), torch.empty(s, h, **bf)
+x, y = torch.randn(s, h, **bf), torch.randn(s, h, **bf)
 gam, bet = torch.ones(h, device=dev), torch.zeros(h, device=dev)
 z = torch.zeros(4 * h, device=dev)
 N = 504_102_912
@@ -31,9 +31,12 @@ KIND = os.environ.get("PROBE_KIND", "mix")
 def step():
     if KIND in ("mix", "gemm"):
         native.gemm_tn_gelu(a, w, g, f, z)
-    if KIND in ("mix", "hbm"):
+    if KIND in ("mix", "hbm", "ln"):
         native.layernorm_fwd(x, gam, bet, y)
+    if KIND in ("mix", "hbm", "gelu"):
         native.gelu_fwd(f, g)
+    if KIND == "lnbwd":
+        native.layernorm_bwd(x, gam, y, x, a, z[:h], z[h:2 * h], drop_out=None, p=0.0)
 
 
 def timed(n=50):
