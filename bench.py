@@ -366,6 +366,16 @@ def run_b200(args, rank, world, local_rank):
     n_layers = layers_per_stage * d
     cfg = ModelConfig(n_layers=n_layers, hidden=h, heads=heads, seq=s, vocab=vocab)
     mode = "emulate" if world == 1 else ("nccl" if backend == "nccl" else "gloo")
+    # backend decisions (tcgen05 vs cuBLAS per GEMM shape, attention fwd) tuned ONCE before
+    # anything runs -- by rank 0 and broadcast under torchrun -- so every rank and every
+    # policy below runs identical kernels (runtime/gemm_tune.py)
+    from paper_2503_01328_b200.runtime import gemm_tune
+
+    gemm_tune.ensure(cfg, dev)
+    table_digests = [gemm_tune.digest()]
+    if dist is not None:
+        table_digests = [None] * world
+        dist.all_gather_object(table_digests, gemm_tune.digest())
 
     # ---- calibration: measured T_F, T_B (per stage), T_o (D2H + H2D of one payload)
     cal_stage = Stage(cfg, min(rank, d - 1) if world > 1 else 0, d, m, dev, layers=list(range(layers_per_stage)))
@@ -490,6 +500,7 @@ def run_b200(args, rank, world, local_rank):
         del res
         gc.collect()
         torch.cuda.empty_cache()
+    gish_trials = None
     if sched_variants and "gis-h" in gish_closed_loop:
         # closed loop on the paper's schedule: selective n=1 stride plans on duplex streams,
         # least memory first, each measured against 1F1B without offload, first within 5% kept
@@ -518,7 +529,7 @@ def run_b200(args, rank, world, local_rank):
             results[name] = dict(runs[id(mc.choice.plan)], stride=mc.choice.stride, trials=trials)
             sched_variants[name] = None
         else:
-            results["gis-h_closed_loop_trials"] = trials
+            gish_trials = trials
     full, auto, single = results["full"], results["auto"], results["full_single"]
     # the no-offload baseline every overhead is quoted against: the faster GEMM backend
     none = results["none_cublas"] if backend == "cublas" else results["none"]
@@ -526,7 +537,8 @@ def run_b200(args, rank, world, local_rank):
     none_cublas = results["none_cublas"]
     slab_bytes = full["_res"].slab_bytes
     for v in results.values():
-        v.pop("_res", None)
+        if isinstance(v, dict):
+            v.pop("_res", None)
 
     # ---- roofline of the dominant kernel of the hot path (HBM-bound recompute)
     hbm_peak, peak_kind, _ = measured_peaks()
@@ -588,7 +600,8 @@ def run_b200(args, rank, world, local_rank):
         "gpu_launches": launches.get("full"),
         "gemm_backend": {"policies": "tcgen05/cuBLAS per shape (gemm=auto)" if backend == "auto"
                          else "cuBLAS (faster end to end than gemm=auto by > 1% in this run)",
-                         "per_shape": gemm_decisions()},
+                         "per_shape": gemm_decisions(),
+                         "table_digest_per_rank": table_digests, "misses": sorted(gemm_tune.MISSES)},
         "attn_backend": {"policies": "attention forward: tcgen05 (ours) or cuDNN + K1 pack, measured per shape "
                                      "(attn=auto); backward: cuDNN", "per_shape": attn_decisions()},
         "clocks": clocks,
@@ -617,7 +630,7 @@ def run_b200(args, rank, world, local_rank):
             "t_duplex_oneway_ms": cal["t_duplex"] * 1e3,
             "partial_candidates": [results[f"partial{i}"] for i in range(len(partial))],
             "schedules": {k: results[k] for k in sched_variants},
-            "gis-h_closed_loop_trials": results.get("gis-h_closed_loop_trials"),
+            "gis-h_closed_loop_trials": gish_trials,
         },
     }
     # k-aware partial offload: the least-memory measured candidate within 5% of no offload
@@ -647,7 +660,7 @@ def run_b200(args, rank, world, local_rank):
 def attn_decisions():
     from paper_2503_01328_b200.runtime import gemm_tune
 
-    return gemm_tune.attn_decisions()
+    return {k: v for k, v in gemm_tune.decisions().items() if k.startswith("attn_fwd")}
 
 
 def gemm_decisions():
@@ -655,7 +668,7 @@ def gemm_decisions():
     the gemm="auto" tuner (runtime/gemm_tune.py), and the backend it picked."""
     from paper_2503_01328_b200.runtime import gemm_tune
 
-    return gemm_tune.decisions()
+    return {k: v for k, v in gemm_tune.decisions().items() if not k.startswith("attn_fwd")}
 
 
 def cpu_baseline(args):

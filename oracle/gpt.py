@@ -84,6 +84,24 @@ def make_tokens(cfg: GPTConfig, microbatches: int, seed: int = 0) -> torch.Tenso
     return torch.randint(0, cfg.vocab, (microbatches, cfg.seq + 1), generator=gen)
 
 
+class _Bf16(torch.autograd.Function):
+    """Round to bf16 (nearest even) in the forward AND round the incoming gradient in
+    the backward: marks a tensor the device path stores in bf16 (activations in the
+    forward, activation gradients in the backward)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.bfloat16().float()
+
+    @staticmethod
+    def backward(ctx, g):
+        return g.bfloat16().float()
+
+
+def _id(x):
+    return x
+
+
 def _mask(cfg, iteration, layer, mb, m, branch, shape):
     keep = keep_mask(int(np.prod(shape)), cfg.p_drop, cfg.dropout_seed, dropout_offset(cfg, iteration, layer, mb, m, branch))
     scale = np.float32(1.0) / np.float32(1.0 - cfg.p_drop)  # fp32 scale, as on device
@@ -104,34 +122,41 @@ def _gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
 
-def run_layers(cfg, params, x, layers, mb, m, iteration=0):
-    """The transformer layers ``layers`` (global ids) applied to x [s, h]."""
+def run_layers(cfg, params, x, layers, mb, m, iteration=0, bf16=False):
+    """The transformer layers ``layers`` (global ids) applied to x [s, h].
+
+    ``bf16=True`` rounds every tensor the device path stores in bf16 (forward
+    activations and their gradients, ``_Bf16``) and computes in fp32 in between --
+    the device's storage precision with the oracle's exact arithmetic."""
     ln = torch.nn.functional.layer_norm
+    r = _Bf16.apply if bf16 else _id
     for l in layers:
         p = lambda k: params[f"l{l}.{k}"]  # noqa: E731
-        a = ln(x, (cfg.hidden,), p("ln1_g"), p("ln1_b"), cfg.eps)
-        o = _attention(cfg, a @ p("w_qkv").t())
-        h1 = x + (o @ p("w_proj").t()) * _mask(cfg, iteration, l, mb, m, 0, x.shape)
-        f = ln(h1, (cfg.hidden,), p("ln2_g"), p("ln2_b"), cfg.eps) @ p("w_fc1").t()
-        x = h1 + (_gelu(f) @ p("w_fc2").t()) * _mask(cfg, iteration, l, mb, m, 1, x.shape)
+        a = r(ln(x, (cfg.hidden,), p("ln1_g"), p("ln1_b"), cfg.eps))
+        o = r(_attention(cfg, r(a @ p("w_qkv").t())))
+        h1 = r(x + r(o @ p("w_proj").t()) * _mask(cfg, iteration, l, mb, m, 0, x.shape))
+        f = r(r(ln(h1, (cfg.hidden,), p("ln2_g"), p("ln2_b"), cfg.eps)) @ p("w_fc1").t())
+        x = r(h1 + r(r(_gelu(f)) @ p("w_fc2").t()) * _mask(cfg, iteration, l, mb, m, 1, x.shape))
     return x
 
 
-def microbatch_loss(cfg, params, tokens_mb, mb, m, iteration=0):
+def microbatch_loss(cfg, params, tokens_mb, mb, m, iteration=0, bf16=False):
     inp, tgt = tokens_mb[:-1], tokens_mb[1:]
     ln = torch.nn.functional.layer_norm
-    x = run_layers(cfg, params, params["wte"][inp] + params["wpe"], range(cfg.n_layers), mb, m, iteration)
-    logits = ln(x, (cfg.hidden,), params["lnf_g"], params["lnf_b"], cfg.eps) @ params["w_head"].t()
+    r = _Bf16.apply if bf16 else _id
+    x = run_layers(cfg, params, r(params["wte"][inp] + params["wpe"]), range(cfg.n_layers), mb, m, iteration, bf16)
+    logits = r(r(ln(x, (cfg.hidden,), params["lnf_g"], params["lnf_b"], cfg.eps)) @ params["w_head"].t())
     return torch.nn.functional.cross_entropy(logits, tgt)
 
 
-def forward_backward(cfg: GPTConfig, params: dict, tokens: torch.Tensor, iteration: int = 0):
-    """Mean loss over microbatches and gradients of that mean (serial fp32)."""
+def forward_backward(cfg: GPTConfig, params: dict, tokens: torch.Tensor, iteration: int = 0, bf16: bool = False):
+    """Mean loss over microbatches and gradients of that mean (serial fp32; ``bf16``:
+    bf16 storage of activations and activation gradients, see ``run_layers``)."""
     leaf = {k: v.clone().requires_grad_(True) for k, v in params.items()}
     m = tokens.shape[0]
     losses = []
     for mb in range(m):
-        loss = microbatch_loss(cfg, leaf, tokens[mb], mb, m, iteration)
+        loss = microbatch_loss(cfg, leaf, tokens[mb], mb, m, iteration, bf16)
         (loss / m).backward()
         losses.append(float(loss.detach()))
     return float(np.mean(losses)), losses, {k: v.grad.detach() for k, v in leaf.items()}

@@ -32,7 +32,7 @@ from ..ir import MemoryTimeline
 from ..offload import OffloadPlan
 from ..schedule_types import Pass, PassKind, Schedule
 from ..sim import SimTrace
-from . import native
+from . import gemm_tune, native
 from .lower import RING, Program, lower
 from .model import ModelConfig, SlabView, Stage, stage_layers
 
@@ -850,7 +850,8 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             stream_mode: str = "single", tokens: torch.Tensor | None = None, params=None, optimizer: str = "sgd",
             lr: float = 1e-4, verify_roundtrip: bool = False, probe_kernels: bool = False,
             use_graphs: bool = True, gemm: str = "auto", offload_tensors=None, attn: str = "auto",
-            iteration_graph: bool = False, pass_timing: bool = True, spare_slabs: int = 0) -> RunResult:
+            iteration_graph: bool = False, pass_timing: bool = True, spare_slabs: int = 0,
+            tune_table=None) -> RunResult:
     """Run ``sched`` (+ ``plan``) for ``warmup + iters`` iterations and measure the last.
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
@@ -868,6 +869,10 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     ``spare_slabs``: offload-arena slabs beyond the modelled peak (``lower``): device
     memory traded for slack when transfers run slower than the plan modelled.
     ``attn``: attention forward backend of every stage ("auto" | "tcgen05" | "cudnn").
+    ``tune_table``: backend decisions to install first (a ``gemm_tune.decisions()``
+    dict or a JSON path); under "auto" the missing ones are tuned before any pass --
+    in the multi-process modes by rank 0 alone and broadcast, so every rank runs the
+    same kernels (``gemm_tune.ensure``).
 
     In the multi-process modes every iteration starts after a device synchronise
     and a barrier, and the returned iteration/wall times and losses are the same on
@@ -894,6 +899,11 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     elif mode != "emulate":
         raise ValueError(f"unknown mode {mode!r}")
     dist_mode = mode in ("nccl", "gloo")
+    if tune_table is not None:
+        gemm_tune.load(tune_table) if isinstance(tune_table, str) else gemm_tune.install(tune_table)
+    if gemm == "auto" or attn == "auto":
+        with torch.cuda.device(dev):
+            gemm_tune.ensure(model, dev, gemm, attn)  # collective in the multi-process modes
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
                           use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors, attn=attn) for r in ranks]

@@ -10,7 +10,8 @@ needs anything that was not saved -- the recompute scheme of PAPER.md:439 that
 turns the reference's 34bsh coefficient into 20bsh (costs.py:1-7,18-20).
 
 Dense GEMMs run on libppo_b200's tcgen05 kernels or cuBLAS, per shape whichever the
-device measured faster (``gemm="auto"``, the default, runtime/gemm_tune.py);
+decision table says (``gemm="auto"``, the default: tuned once before the first pass and
+identical on every rank, runtime/gemm_tune.py);
 ``gemm="best"`` is the static round-1 rule (ours except narrow-N / deep-K shapes,
 profiles/r1_gemm_tuning.txt).  fc1 fuses the GeLU into its epilogue (writes f into the slab and g for fc2), the
 fc2 activation-gradient GEMM fuses the GeLU backward (df = (dm @ Wfc2) * gelu'(f)),
@@ -198,6 +199,8 @@ class Stage:
         self.iter_base = torch.zeros(1, device=self.device, dtype=torch.int64)
         self.tok = torch.zeros(cfg.seq + 1, device=self.device, dtype=torch.int64)
         self._attn_meta = None
+        if gemm == "auto" or attn == "auto":  # decisions tuned once, before any pass (gemm_tune)
+            gemm_tune.require(cfg, self.device, gemm, attn)
         self._attn_init()
         self.probe = None  # kernel name -> [bytes_per_launch, [(start_event, end_event), ...]]
 
@@ -217,17 +220,7 @@ class Stage:
             lse = torch.empty(cfg.heads * s, device=self.device, dtype=torch.float32)
             native.attn_fwd(qkv, ws["a"], lse, cfg.heads)  # creates the library's per-seq constants
             if self.attn_mode == "auto":
-                qkv.normal_()
-                dst = torch.empty(2 * s * h + 4 * cfg.heads * s, device=self.device, dtype=torch.uint8)
-
-                def make():
-                    def cudnn():
-                        r = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
-                        native.pack([(r[0], 0, 1, 2 * s * h, 0), (r[1], 2 * s * h, 1, 4 * cfg.heads * s, 0)], dst)
-                    return (lambda: native.attn_fwd(qkv, ws["a"], lse, cfg.heads)), cudnn
-
-                self.attn_ours = gemm_tune.prefer_ours_attn((s, cfg.heads, cfg.head_dim), self.device, make)
-                del dst
+                self.attn_ours = gemm_tune.attn_choice(s, cfg.heads, cfg.head_dim)
         del res
 
     def _k(self, name: str, nbytes: int, fn, *args, **kw):
@@ -248,30 +241,20 @@ class Stage:
         return self.g[f"l{l}.{k}"]
 
     # ------------------------------------------------------------------ GEMMs
-    def _ours(self, n: int, k: int) -> bool:
-        """Static rule of gemm="best": ours except narrow-N / deep-K (N <= 2048, K >= 3N)."""
+    def _tuned(self, kind: str, shape: tuple) -> bool:
+        """True if libppo_b200's kernel runs (kind, shape): the decision table under
+        gemm="auto" (tuned before the first pass, identical on every rank,
+        runtime/gemm_tune.py), the static rule under "best", else the pinned backend."""
+        if self.gemm == "auto":
+            return gemm_tune.gemm_choice(kind, shape)
         if self.gemm == "best":
-            return not (n <= 2048 and k >= 3 * n)
-        return self.gemm in ("tcgen05", "auto")
-
-    def _tuned(self, kind: str, shape: tuple, make) -> bool:
-        """gemm="auto": the measured faster backend for (kind, shape) (runtime/gemm_tune.py)."""
-        if self.gemm != "auto":
-            return self.gemm != "cublas" and (kind not in ("tn", "nn", "nn_acc") or self._ours(shape[1], shape[2]))
-        return gemm_tune.prefer_ours(kind, shape, self.device, make, fallback=True)
-
-    def _rand(self, *shape, dtype=torch.bfloat16):
-        return torch.randn(*shape, device=self.device, dtype=torch.float32).to(dtype) * 0.1
+            return gemm_tune.static_rule(kind, shape)
+        return self.gemm == "tcgen05"
 
     def mm_fwd(self, a, w, out):
         """out = a @ w^T (nn.Linear forward; w is [out, in])."""
         M, (N, K) = a.shape[0], w.shape
-
-        def make():
-            a_, w_, o_ = self._rand(M, K), self._rand(N, K), torch.empty(M, N, device=self.device, dtype=torch.bfloat16)
-            return (lambda: native.gemm_tn(a_, w_, o_)), (lambda: torch.mm(a_, w_.t(), out=o_))
-
-        if self._tuned("tn", (M, N, K), make):
+        if self._tuned("tn", (M, N, K)):
             native.gemm_tn(a, w, out)
         else:
             torch.mm(a, w.t(), out=out)
@@ -279,15 +262,7 @@ class Stage:
     def mm_fc1_gelu(self, a, w, f_out, g_out):
         """f = a @ w^T (saved GeLU input) and g = gelu(f) (fc2 operand)."""
         M, (N, K) = a.shape[0], w.shape
-
-        def make():
-            a_, w_ = self._rand(M, K), self._rand(N, K)
-            f_, g_ = (torch.empty(M, N, device=self.device, dtype=torch.bfloat16) for _ in range(2))
-            zb = self.zero_bias[:N]
-            return ((lambda: native.gemm_tn_gelu(a_, w_, g_, f_, zb)),
-                    (lambda: (torch.mm(a_, w_.t(), out=f_), native.gelu_fwd(f_, g_))))
-
-        if self._tuned("tn_gelu", (M, N, K), make):
+        if self._tuned("tn_gelu", (M, N, K)):
             native.gemm_tn_gelu(a, w, g_out, f_out, self.zero_bias[: w.shape[0]])
         else:
             torch.mm(a, w.t(), out=f_out)
@@ -296,14 +271,7 @@ class Stage:
     def mm_dgrad(self, dy, w, out, accumulate: bool = False):
         """out (+)= dy @ w (activation gradient of nn.Linear)."""
         M, (K, N) = dy.shape[0], w.shape
-
-        def make():
-            d_, w_, o_ = self._rand(M, K), self._rand(K, N), torch.zeros(M, N, device=self.device, dtype=torch.bfloat16)
-            beta = 1.0 if accumulate else 0.0
-            return ((lambda: native.gemm_nn(d_, w_, o_, beta)),
-                    (lambda: torch.addmm(o_, d_, w_, out=o_) if accumulate else torch.mm(d_, w_, out=o_)))
-
-        if self._tuned("nn_acc" if accumulate else "nn", (M, N, K), make):
+        if self._tuned("nn_acc" if accumulate else "nn", (M, N, K)):
             native.gemm_nn(dy, w, out, 1.0 if accumulate else 0.0)
         elif accumulate:
             torch.addmm(out, dy, w, out=out)
@@ -316,16 +284,9 @@ class Stage:
         When g is needed (unsplit backward) the plain dgrad GEMM + one gelu_bwd pass
         (reads f and dg once, writes df and g) is cheaper; when it is not (split
         backward: the W pass recomputes g) the GeLU backward rides in the GEMM
-        epilogue (``gemm_nn_dgelu``) unless the tuner measured GEMM + gelu_bwd faster."""
+        epilogue (``gemm_nn_dgelu``) unless the table says GEMM + gelu_bwd is faster."""
         M, (K, N) = dm.shape[0], w.shape
-
-        def make():
-            d_, w_, f_ = self._rand(M, K), self._rand(K, N), self._rand(M, N)
-            o_ = torch.empty(M, N, device=self.device, dtype=torch.bfloat16)
-            return ((lambda: native.gemm_nn_dgelu(d_, w_, f_, o_)),
-                    (lambda: (self.mm_dgrad(d_, w_, o_), native.gelu_bwd(f_, o_, None, o_))))
-
-        if g_out is None and self.gemm != "cublas" and self._tuned("nn_dgelu", (M, N, K), make):
+        if g_out is None and self.gemm != "cublas" and self._tuned("nn_dgelu", (M, N, K)):
             native.gemm_nn_dgelu(dm, w, f, df_out)
             return
         self.mm_dgrad(dm, w, df_out)
@@ -334,13 +295,7 @@ class Stage:
     def wgrad(self, acc, dy, x):
         """acc (fp32, [out, in]) += dy^T @ x with dy [tokens, out], x [tokens, in]."""
         T, (O, I) = dy.shape[0], acc.shape
-
-        def make():
-            d_, x_ = self._rand(T, O), self._rand(T, I)
-            a_ = torch.zeros(O, I, device=self.device, dtype=torch.float32)
-            return (lambda: native.gemm_wgrad(d_, x_, a_, 1.0)), (lambda: _wgrad(a_, d_.t(), x_))
-
-        if self._tuned("wgrad", (O, I, T), make):
+        if self._tuned("wgrad", (O, I, T)):
             native.gemm_wgrad(dy, x, acc, 1.0)
         else:
             _wgrad(acc, dy.t(), x)

@@ -3,8 +3,10 @@ tests/test_multiproc_gpu.py).  All ranks may share one GPU: the boundary goes
 over gloo host copies (executor.HostTransport), everything else is the product
 path (lowered per-rank program, slab arena, pinned pool, copy streams, kernels).
 
-usage: torchrun --nproc-per-node D tests/helpers/dist_worker.py KIND OUT.json
+usage: torchrun --nproc-per-node D tests/helpers/dist_worker.py KIND OUT.json [GEMM ATTN]
 KIND: 1f1b (build_1f1b_full_offload(D, 8, unit, 3/2)) or 1f1b-i (v=2, selective n=1)
+GEMM/ATTN: backends (default tcgen05/tcgen05, pinned so the single-process comparison
+run uses the same kernels; "auto" exercises the collective decision table)
 """
 import json
 import os
@@ -19,6 +21,7 @@ import torch.distributed as dist  # noqa: E402
 
 import paper_2503_01328_b200 as po  # noqa: E402
 from paper_2503_01328_b200.runtime import executor as ex  # noqa: E402
+from paper_2503_01328_b200.runtime import gemm_tune  # noqa: E402
 from paper_2503_01328_b200.runtime.model import ModelConfig  # noqa: E402
 
 CFG = ModelConfig(n_layers=4, hidden=256, heads=4, seq=512, vocab=1024)
@@ -35,6 +38,7 @@ def build(kind: str, d: int):
 
 def main():
     kind, out = sys.argv[1], sys.argv[2]
+    gemm, attn = (sys.argv[3], sys.argv[4]) if len(sys.argv) > 4 else ("tcgen05", "tcgen05")
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
@@ -42,11 +46,12 @@ def main():
     sched, plan = build(kind, world)
     tokens = torch.randint(0, CFG.vocab, (8, CFG.seq + 1), generator=torch.Generator().manual_seed(0))
     res = ex.execute(sched, plan, model=CFG, mode="gloo", rank=rank, device=dev, iters=2, warmup=0, tokens=tokens,
-                     optimizer="sgd", lr=1e-2, verify_roundtrip=True)
+                     optimizer="sgd", lr=1e-2, verify_roundtrip=True, gemm=gemm, attn=attn)
     r = res.runners[0]
     report = {"rank": rank, "losses": res.losses, "secs": res.iteration_seconds,
               "mismatches": ex.roundtrip_mismatches(res.runners), "offloaded": len(r.prog.offloaded),
-              "compute_order": [list(k) for k in r.prog.compute_order], "n_slabs": r.prog.n_slabs}
+              "compute_order": [list(k) for k in r.prog.compute_order], "n_slabs": r.prog.n_slabs,
+              "table_digest": gemm_tune.digest(), "table": gemm_tune.decisions()}
     reports = [None] * world
     dist.all_gather_object(reports, report)
     if rank == 0:

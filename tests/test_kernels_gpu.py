@@ -256,7 +256,7 @@ def test_nccl_p2p_self_loop(nbytes):
         comm.close()
 
 
-def test_gemm_swizzle_bit_identical_and_tuner():
+def test_gemm_swizzle_bit_identical_and_tuner(tmp_path):
     """The tile-scheduler swizzle only reorders whole output tiles: results are
     bit-identical across swizzles; the gemm="auto" tuner records a measured choice."""
     from paper_2503_01328_b200.runtime import gemm_tune
@@ -286,8 +286,18 @@ def test_gemm_swizzle_bit_identical_and_tuner():
     ref = x.float() @ w.float().t()
     assert float((y.float() - ref).norm() / ref.norm()) < 1e-2
     dec = gemm_tune.decisions()
-    assert "tn 512x768x256" in dec and dec["tn 512x768x256"]["choice"] in ("tcgen05", "cublas")
-    assert dec["tn 512x768x256"]["ours_swizzle"] in gemm_tune.SWIZZLES
+    assert "tn 512x768x256" in dec and dec["tn 512x768x256"]["backend"] in ("tcgen05", "cublas")
+    assert dec["tn 512x768x256"]["swizzle"] in gemm_tune.SWIZZLES
+    # every layer shape was decided at Stage construction: pass bodies only look up
+    assert not gemm_tune.MISSES
+    assert all(gemm_tune.gemm_key(k, sh) in dec for (k, *sh) in gemm_tune.layer_gemm_shapes(512, 256))
+    # a saved table reloads to the same decisions (same digest)
+    d0 = gemm_tune.digest()
+    path = str(tmp_path / "table.json")
+    gemm_tune.save(path)
+    gemm_tune.reset()
+    gemm_tune.load(path)
+    assert gemm_tune.digest() == d0
 
 
 def _attn_ref(qkv: torch.Tensor, heads: int):

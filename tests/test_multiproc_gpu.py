@@ -59,7 +59,7 @@ def test_two_process_pipeline_matches_virtual(kind, tmp_path):
     sched, plan = build(kind, 2)
     tokens = torch.randint(0, CFG.vocab, (8, CFG.seq + 1), generator=torch.Generator().manual_seed(0))
     res = ex.execute(sched, plan, model=CFG, mode="virtual", iters=2, warmup=0, tokens=tokens, optimizer="sgd",
-                     lr=1e-2)
+                     lr=1e-2, gemm="tcgen05", attn="tcgen05")  # the workers' pinned backends
     for r in res.runners:
         rep = reports[r.rank]
         assert rep["compute_order"] == [list(k) for k in r.prog.compute_order]
@@ -68,6 +68,32 @@ def test_two_process_pipeline_matches_virtual(kind, tmp_path):
     assert reports[0]["losses"][0] == res.losses[0]
     # step 2 sees weights updated with gradients that used float atomics (LN dgamma/dbeta)
     assert reports[0]["losses"][1] == pytest.approx(res.losses[1], rel=1e-3)
+
+
+def test_two_process_auto_backends_agree(tmp_path):
+    """gemm="auto" / attn="auto" under torchrun: rank 0 tunes the decision table and
+    broadcasts it (gemm_tune.ensure), so both ranks run identical kernels; the
+    single-process run replays the same table and matches the first step bit for bit."""
+    out = tmp_path / "r.json"
+    p = _torchrun(2, ["tests/helpers/dist_worker.py", "1f1b", str(out), "auto", "auto"])
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    reports = json.loads(out.read_text())
+    assert reports[0]["table_digest"] == reports[1]["table_digest"]
+    assert reports[0]["table"] and reports[0]["losses"] == reports[1]["losses"]
+    from paper_2503_01328_b200.runtime import gemm_tune
+
+    saved = dict(gemm_tune.TABLE)
+    try:
+        gemm_tune.reset()
+        sched, plan = build("1f1b", 2)
+        tokens = torch.randint(0, CFG.vocab, (8, CFG.seq + 1), generator=torch.Generator().manual_seed(0))
+        res = ex.execute(sched, plan, model=CFG, mode="virtual", iters=1, warmup=0, tokens=tokens, optimizer="sgd",
+                         lr=1e-2, tune_table=reports[0]["table"])
+        assert gemm_tune.digest() == reports[0]["table_digest"]  # nothing re-tuned
+        assert reports[0]["losses"][0] == res.losses[0]
+    finally:
+        gemm_tune.reset()
+        gemm_tune.install(saved)
 
 
 def test_bench_two_ranks(tmp_path):
