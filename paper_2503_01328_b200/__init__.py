@@ -1,9 +1,10 @@
 """B200-native PipeOffload runtime: the ``ppoff`` planner API plus a measured executor.
 
 Planner names are those of the reference package's public surface
-(``pkg/src/ppoff/__init__.py:3-65``), re-implemented here; ``execute`` (in
-``runtime``) replaces the reference's ``simulate`` as the pipeline runner and
-returns a ``SimTrace``-compatible measured trace.  The CUDA side lives in the
+(``pkg/src/ppoff/__init__.py:3-65``), re-implemented here; ``execute`` (``runner.py``,
+``simulate``'s signature) replaces the reference's ``simulate`` as the pipeline runner
+and returns a ``SimTrace`` of CUDA-measured times (``runner(**opts)`` binds it into a
+``simulate``-compatible callable).  The CUDA side lives in the
 in-tree C-ABI library ``libppo_b200.so`` (``include/ppo_b200.h``).
 """
 
@@ -68,6 +69,7 @@ from .sim import (
     peak_memory,
     simulate,
 )
+from .runner import MeasuredTrace, config_from_spec, execute, runner
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 __version__ = "0.1.0"

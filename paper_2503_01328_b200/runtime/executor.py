@@ -252,6 +252,8 @@ class RankRunner:
         self.device = torch.device(device)
         self.rank = program.rank
         self.transport = transport
+        # consecutive stages on this device (d=1 with v>1): boundary messages stay local
+        self.local = LocalTransport()
         self.emulate = emulate
         my_stages = [s for s in range(sched.num_stages) if sched.placement[s] == self.rank]
         with torch.cuda.device(self.device):
@@ -345,6 +347,23 @@ class RankRunner:
         """Device bytes held for activations: both arenas (the measured per-GPU peak)."""
         return self.prog.n_slabs * self.off_bytes + (self.prog.n_res_slabs * self.res_bytes if self.res_bytes else 0)
 
+    @property
+    def state_bytes(self) -> int:
+        """Persistent training state of this rank's stages (weights, gradients, masters,
+        AdamW moments once created): excluded from activation memory."""
+        extra = 0
+        if self.optimizer not in ("none", "sgd"):
+            extra = 2 * sum(t.numel() * t.element_size() for st in self.stages.values() for t in st.master.values())
+        return sum(st.state_bytes for st in self.stages.values()) + extra
+
+    @property
+    def wbuf_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for b in self.wbufs.values() for per in b.values() for t in per.values())
+
+    @property
+    def ws_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for st in self.stages.values() for t in st.ws.values())
+
     def _rkey(self, op):
         """Resident slot as part of a pass-graph key (None when there is no resident part)."""
         return op.res_slab if self.res_bytes else None
@@ -409,7 +428,7 @@ class RankRunner:
             for key in op.waits:
                 stream.wait_event(self.ev(key))
             buf = self.rings["recv_act" if op.kind == "RECV_ACT" else "recv_grad"][op.ring]
-            if not self.transport.recv(self.rank, op, buf, stream):
+            if not self._transport(op).recv(self.rank, op, buf, stream):
                 return False
             self.rec(op.records[0], stream)
             self.cursor += 1
@@ -426,12 +445,15 @@ class RankRunner:
             self._transfer(op, stream)
         elif op.kind in ("SEND_ACT", "SEND_GRAD"):
             buf = self.rings["send_act" if op.kind == "SEND_ACT" else "send_grad"][op.ring]
-            self.transport.send(self.rank, op, buf, stream)
+            self._transport(op).send(self.rank, op, buf, stream)
             self.rec(op.records[0], stream)
         else:  # pragma: no cover
             raise ValueError(op.kind)
         self.cursor += 1
         return True
+
+    def _transport(self, op):
+        return self.local if op.peer == self.rank else self.transport
 
     def _forward(self, op, stream):
         s, j = op.stage, op.mb
@@ -738,6 +760,8 @@ def _capture_iteration(runners, tokens_dev, origin, dev, transport):
         r.iteration -= 1  # the capture ran nothing
     if transport is not None:
         transport.end_iteration()
+    for r in runners:
+        r.local.end_iteration()
     launched = native.kernel_launches() - before
     calls = native.since(snap)
     native.credit(calls, -1)  # recorded, not executed: each replay credits them back
@@ -836,6 +860,9 @@ class RunResult:
     host_issue_seconds: list = field(default_factory=list)  # host time to enqueue one iteration
     act_bytes: dict = field(default_factory=dict)  # rank -> activation arena bytes (both parts)
     offload_fraction: float = 1.0  # share of a pair's saved set that travels when it is offloaded
+    # activation memory MEASURED the paper's way (peak minus iteration-start
+    # memory) for the ranks of this process: see ``execute``
+    mem: dict = field(default_factory=dict)
 
     def close(self):
         """Release the pinned pools and drop the runners (their device arenas, weights
@@ -904,6 +931,16 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     if gemm == "auto" or attn == "auto":
         with torch.cuda.device(dev):
             gemm_tune.ensure(model, dev, gemm, attn)  # collective in the multi-process modes
+    # activation memory, the paper's way: everything allocated from here on except the
+    # persistent training state (weights / gradients / masters) counts -- slab arenas,
+    # split-backward W buffers, recompute workspaces, boundary rings, graph pools and
+    # library temporaries.  Torch's allocator peak gives the allocated view,
+    # cudaMemGetInfo the device view (cached segments and library workspaces included).
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats(dev)
+    alloc0 = torch.cuda.memory_allocated(dev)
+    free0, total0 = torch.cuda.mem_get_info(dev)
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
                           use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors, attn=attn) for r in ranks]
@@ -948,9 +985,11 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         result = [r.result_scalar() for r in runners]
         values = [float(x) for x in result]  # D2H read of the step's result (syncs)
         wall = time.perf_counter() - wall0
+        torch.cuda.synchronize(dev)
         if transport is not None:
-            torch.cuda.synchronize(dev)
             transport.end_iteration()
+        for r in runners:  # local same-device hand-offs: snapshots freed after the sync
+            r.local.end_iteration()
         if it >= warmup:
             torch.cuda.synchronize(dev)
             sec = max(r.iteration_seconds() for r in runners)
@@ -962,10 +1001,21 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
             host_secs.append(host_issue)
             secs.append(sec)
             losses.append(loss)
+    torch.cuda.synchronize(dev)
+    state = sum(r.state_bytes for r in runners)
+    free1, _ = torch.cuda.mem_get_info(dev)
+    mem = {
+        "alloc_peak_bytes": torch.cuda.max_memory_allocated(dev) - alloc0 - state,
+        "device_bytes": (free0 - free1) - state,
+        "arena_bytes": sum(r.act_bytes for r in runners),
+        "wbuf_bytes": sum(r.wbuf_bytes for r in runners),
+        "workspace_bytes": sum(r.ws_bytes for r in runners),
+        "state_bytes": state,
+    }
     passes = [p for r in runners for p in r.measured_passes()] if (pass_timing or not whole) else []
     slab_bytes = max(r.slab_bytes for r in runners)
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
     return RunResult(trace, secs, losses, programs, runners, slab_bytes,
                      {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners},
                      walls, host_secs, {r.rank: r.act_bytes for r in runners},
-                     max(r.off_bytes for r in runners) / max(1, slab_bytes))
+                     max(r.off_bytes for r in runners) / max(1, slab_bytes), mem)

@@ -240,9 +240,9 @@ def lower(
                 op.waits.append((f"{last_use}_end",) + prev_res[1:])
             if s > 0:
                 src = placement[s - 1]
-                if src == rank and not emulate_neighbors:
-                    raise NotImplementedError("consecutive stages on one device (d=1, v>1) are not lowered")
-                if not emulate_neighbors:
+                # consecutive stages on one device (d=1, v>1) hand off through a local
+                # channel of the same rank (peer == rank), not through the transport
+                if not emulate_neighbors or src == rank:
                     ch = ("act", src, rank)
                     lst = recv_orders.setdefault(ch, [])
                     lst.append(pair)
@@ -258,7 +258,7 @@ def lower(
             compute_ops.append(op)
             if s < last_stage:
                 dst = placement[s + 1]
-                if not emulate_neighbors and dst != rank:
+                if not emulate_neighbors or dst == rank:
                     ch = ("act", rank, dst)
                     lst = send_orders.setdefault(ch, [])
                     lst.append(pair)
@@ -271,8 +271,6 @@ def lower(
                         op.waits.append(("SA", ps, pj))  # F may overwrite this send buffer
                     op.send_ring = snd.ring
                     ops.append(snd)
-                elif dst == rank and not emulate_neighbors:
-                    raise NotImplementedError("consecutive stages on one device (d=1, v>1) are not lowered")
         elif p.kind == W:
             op = Op("W", s, j, "compute", p.start)
             op.records = [("W_start", s, j), ("W_end", s, j)]
@@ -294,7 +292,7 @@ def lower(
                 op.wbuf = wbuf_of[("G",) + pair][0]
             if s < last_stage:
                 src = placement[s + 1]
-                if not emulate_neighbors and src != rank:
+                if not emulate_neighbors or src == rank:
                     ch = ("grad", src, rank)
                     lst = recv_orders.setdefault(ch, [])
                     lst.append(pair)
@@ -309,7 +307,7 @@ def lower(
                     op.ring = r.ring
             if s > 0:
                 dst = placement[s - 1]
-                if not emulate_neighbors and dst != rank:
+                if not emulate_neighbors or dst == rank:
                     ch = ("grad", rank, dst)
                     lst = send_orders.setdefault(ch, [])
                     lst.append(pair)

@@ -181,6 +181,10 @@ class Stage:
             is_matrix = t.dim() == 2
             self.w[n] = t.to(torch.bfloat16) if is_matrix else t.contiguous()
             self.g[n] = torch.zeros_like(t, dtype=torch.float32)
+        # persistent training state (bf16 weights, fp32 gradients, fp32 masters): what the
+        # paper's "iteration-start memory" holds; everything else a run allocates is
+        # activation memory (executor.RunResult.mem)
+        self.state_bytes = sum(t.numel() * t.element_size() for d in (self.w, self.g, self.master) for t in d.values())
         s, h = cfg.seq, cfg.hidden
         bf = dict(device=self.device, dtype=torch.bfloat16)
         self.ws = {

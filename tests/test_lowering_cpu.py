@@ -166,6 +166,10 @@ CASES = [
     ("gis d4 v2 n1 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(4, 2, U), 1), Fraction(1))))(po.build_gis(4, 2, 8, U))),
     ("gis-h d8 v2 n1 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(8, 2, U), 1), Fraction(3, 2))))(po.build_gis_h(8, 2, 16, U))),
     ("po d8 v2 n2 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(8, 2, U), 2), Fraction(3))))(po.build_po(8, 2, 16, U))),
+    # d = 1 with v > 1: consecutive stages on one device hand off through a local channel
+    ("1f1b-i d1 v2 no offload", lambda: (po.build_interleaved_1f1b(1, 2, 4, U), None)),
+    ("gis d1 v2 n1 (split W)", lambda: (lambda s: (s, po.plan_slots(s, po.select_offload_stages(po.po_block(1, 2, U), 1), Fraction(1))))(po.build_gis_h(1, 2, 4, U))),
+    ("po d1 v3 (split W)", lambda: (po.build_po(1, 3, 4, U), None)),
 ]
 
 

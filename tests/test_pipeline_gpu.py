@@ -7,8 +7,9 @@ Bars:
 * op order executed on every rank == Schedule.device_passes (reference order);
 * copy-stream order == OffloadPlan slot order (no late reloads at k=1/2);
 * every offloaded slab reloads bit-exact (integer digests, in situ);
-* loss within 2% and every gradient within 5% relative L2 of the serial fp32
-  oracle (bf16 activations/GEMM inputs vs fp32 everywhere);
+* loss and every gradient within the bars of tests/helpers/parity.py of the
+  serial fp32 oracle (loss 2e-4 relative; gradients 1.2e-2 relative L2 per matrix,
+  2e-2 per LayerNorm vector -- just above the bf16-storage noise floor);
 * offload on vs off: same loss to 1e-3 relative (only nondeterministic atomics
   and cuDNN's dQ accumulation differ).
 """
@@ -23,6 +24,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2503_01328_b200 as po  # noqa: E402
+from helpers.parity import violations  # noqa: E402
 from oracle import gpt as oracle_gpt  # noqa: E402
 from paper_2503_01328_b200.runtime import executor as ex  # noqa: E402
 from paper_2503_01328_b200.runtime.model import ModelConfig  # noqa: E402
@@ -67,12 +69,7 @@ def test_c1_full_offload_matches_oracle(oracle_result):
     assert ex.roundtrip_mismatches(res.runners) == []
     n_offloaded = sum(len(p.offloaded) for p in res.programs.values())
     assert n_offloaded == 24
-    loss = res.losses[-1]
-    assert abs(loss - want_loss) < 0.02 * abs(want_loss), (loss, want_loss)
-    got = _grads(res)
-    assert set(got) == set(want_grads)
-    for k, g in want_grads.items():
-        assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
+    assert violations(res.losses[-1], want_loss, _grads(res), want_grads) == []
     # measured trace is a SimTrace: the reference's metrics apply
     pk = po.peak_memory(res.trace)
     assert [u for u, _ in pk["per_device"]] == [2, 2, 2, 1]
@@ -88,7 +85,7 @@ def test_c1_offload_equals_no_offload(oracle_result):
     assert abs(on.losses[-1] - off.losses[-1]) < 1e-3 * abs(off.losses[-1])
     g_on, g_off = _grads(on), _grads(off)
     for k in g_off:
-        assert rel(g_on[k], g_off[k]) < 1e-2, k
+        assert rel(g_on[k], g_off[k]) < 1e-3, k
 
 
 def test_interleaved_selective_offload_runs():
@@ -134,11 +131,7 @@ def test_split_backward_schedules_match_oracle(kind, oracle_result):
     res = ex.execute(sched, plan, model=CFG, mode="virtual", tokens=tokens, optimizer="none", verify_roundtrip=True)
     assert ex.roundtrip_mismatches(res.runners) == []
     assert sum(p.n_wbufs for p in res.programs.values()) > 0
-    loss = res.losses[-1]
-    assert abs(loss - want_loss) < 0.02 * abs(want_loss), (loss, want_loss)
-    got = _grads(res)
-    for k, g in want_grads.items():
-        assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
+    assert violations(res.losses[-1], want_loss, _grads(res), want_grads) == []
 
 
 def _variant(name):
@@ -219,11 +212,7 @@ def test_c1_partial_offload_matches_oracle(oracle_result, tensors):
         assert r.act_bytes == r.prog.n_slabs * r.off_bytes + r.prog.n_res_slabs * r.res_bytes
         assert r.prog.n_res_slabs == [4, 3, 2, 1][r.rank]  # in-flight peak (no-offload arena)
         assert lay.host_bytes < lay.slab_bytes
-    loss = res.losses[-1]
-    assert abs(loss - want_loss) < 0.02 * abs(want_loss), (loss, want_loss)
-    got = _grads(res)
-    for k, g in want_grads.items():
-        assert rel(got[k], g) < 0.05, (k, rel(got[k], g))
+    assert violations(res.losses[-1], want_loss, _grads(res), want_grads) == []
 
 
 @pytest.mark.parametrize("mode,stream_mode", [("virtual", "single"), ("emulate", "dual")])

@@ -64,3 +64,40 @@ def test_reference_suite_passes_against_this_planner(tmp_path):
     tail = res.stdout[-2000:]
     assert res.returncode == 0, tail
     assert "235 passed" in tail, tail
+
+
+@pytest.mark.skipif(not have_reference(), reason="reference sources not mounted")
+def test_reference_analysis_accepts_the_dropin_runner(tmp_path):
+    """ppoff.analysis.reduction_curve (analysis.py:142-181) looks ``simulate`` up as a
+    module global, so rebinding that one name to a ``runner(...)``-style callable
+    routes every trace it consumes through the drop-in.  Here the callable is a
+    counting wrapper over the runner model (no GPU in this container); the GPU test
+    tests/test_dropin_gpu.py runs the same call pattern over measured traces."""
+    shim = tmp_path / "shim" / "ppoff"
+    shim.mkdir(parents=True)
+    (shim / "__init__.py").write_text(SHIM)
+    script = textwrap.dedent(
+        """
+        from fractions import Fraction
+        import ppoff
+        calls = []
+        real = ppoff.analysis.simulate
+        def counting(sched, plan=None, costs=None, hw=None, contention=None, model=None, stream_mode="single"):
+            calls.append(plan is not None)
+            return real(sched, plan, costs, hw, contention, model, stream_mode)
+        U = ppoff.PassCosts.unit()
+        want = ppoff.analysis.reduction_curve(4, 2, 8, U, Fraction(1, 2))
+        ppoff.analysis.simulate = counting
+        got = ppoff.analysis.reduction_curve(4, 2, 8, U, Fraction(1, 2))
+        assert calls == [False, True, True], calls
+        assert got.points == want.points
+        import paper_2503_01328_b200 as po, inspect
+        assert list(inspect.signature(po.runner()).parameters) == list(inspect.signature(real).parameters)
+        assert list(inspect.signature(po.execute).parameters)[:7] == list(inspect.signature(real).parameters)
+        print("OK")
+        """
+    )
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", PYTHONPATH=f"{tmp_path / 'shim'}:{ROOT}")
+    res = subprocess.run([sys.executable, "-c", script], cwd=tmp_path, env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert res.returncode == 0 and res.stdout.strip().endswith("OK"), res.stdout[-2000:] + res.stderr[-2000:]

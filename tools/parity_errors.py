@@ -31,8 +31,12 @@ def grads(res):
 def report(name, loss, want_loss, got, want, **extra):
     errs = {k: rel(got[k], g) for k, g in want.items()}
     worst = max(errs, key=errs.get)
+    mat = {k: e for k, e in errs.items() if want[k].dim() == 2}
+    vec = {k: e for k, e in errs.items() if want[k].dim() == 1}
     print(json.dumps(dict(case=name, loss=loss, oracle_loss=want_loss, loss_rel=abs(loss - want_loss) / abs(want_loss),
                           grad_rel_max=errs[worst], grad_rel_worst=worst,
+                          matrix_max=max(mat.values()), matrix_worst=max(mat, key=mat.get),
+                          vector_max=max(vec.values()), vector_worst=max(vec, key=vec.get),
                           grad_rel_median=sorted(errs.values())[len(errs) // 2], **extra)), flush=True)
 
 
