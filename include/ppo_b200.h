@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 7
+#define PPO_ABI_VERSION 8
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -56,11 +56,18 @@ uint64_t ppo_kernel_launches(void);
 int ppo_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 
 /* ------------------------------------------------ K2: pinned host pool + copies */
-/* A preallocated, page-locked host arena (cudaHostAlloc, portable + NUMA-local by
- * first touch from the calling process).  No per-step allocation: slabs are carved
+/* A preallocated, page-locked host arena (cudaHostAlloc, portable; NUMA-bound to the
+ * GPU's node with ppo_pool_create_numa).  No per-step allocation: slabs are carved
  * at plan time.  Replaces the modelled host residency of sim.py:462-487. */
 typedef struct ppo_pool ppo_pool;
 int ppo_pool_create(uint64_t bytes, ppo_pool** out);
+/* NUMA-local variant (SURVEY 8(b) `po_pool_create(device, numa_node, ...)`): the pages
+ * are mbind()-bound to `numa_node` before first touch, then cudaHostRegister'ed.
+ * numa_node -1: the node of `device`'s PCI function (sysfs); -2: no binding (as
+ * ppo_pool_create).  Single-node hosts fall back to cudaHostAlloc.  *node_out (may be
+ * NULL) receives the bound node or -1. */
+int ppo_pool_create_numa(uint64_t bytes, int device, int numa_node, ppo_pool** out, int* node_out);
+int ppo_pool_numa_node(const ppo_pool* pool);
 int ppo_pool_destroy(ppo_pool* pool);
 void* ppo_pool_base(const ppo_pool* pool);
 uint64_t ppo_pool_bytes(const ppo_pool* pool);

@@ -6,6 +6,12 @@
 // (sim.py:462-487).  Here they are real copies on a dedicated copy stream.
 #include <cuda_runtime.h>
 
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cctype>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -198,33 +204,114 @@ int ppo_device_info(int device, int* sm_count, int* cc_major, int* cc_minor) {
 struct ppo_pool {
   void* base;
   uint64_t bytes;
+  int numa_node;   // node the pages are bound to, -1: first touch (cudaHostAlloc)
+  bool registered; // mmap + mbind + cudaHostRegister (else cudaHostAlloc)
 };
 
-int ppo_pool_create(uint64_t bytes, ppo_pool** out) {
-  if (!out || bytes == 0) return set_error(PPO_EINVAL, "ppo_pool_create: bad arguments");
-  *out = nullptr;
+// NUMA node of a GPU's PCI function (sysfs), -1 if unknown / not a NUMA system.
+static int gpu_numa_node(int device) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return -1;
+  for (char* c = bus; *c; ++c) *c = (char)std::tolower(*c);
+  char path[128];
+  std::snprintf(path, sizeof(path), "/sys/bus/pci/devices/%s/numa_node", bus);
+  FILE* f = std::fopen(path, "r");
+  if (!f) return -1;
+  int node = -1;
+  if (std::fscanf(f, "%d", &node) != 1) node = -1;
+  std::fclose(f);
+  return node;
+}
+
+static int numa_nodes_online() {
+  FILE* f = std::fopen("/sys/devices/system/node/online", "r");
+  if (!f) return 1;
+  int lo = 0, hi = 0;
+  int n = std::fscanf(f, "%d-%d", &lo, &hi);
+  std::fclose(f);
+  return n == 2 ? hi - lo + 1 : 1;
+}
+
+static int pool_from_host_alloc(uint64_t bytes, ppo_pool* p) {
   void* base = nullptr;
-  // Portable so every context of the process may DMA from it; the pages are
-  // first-touched by this process, which the launcher binds to the GPU's NUMA node.
+  // Portable so every context of the process may DMA from it; pages land on the node
+  // of the first-touching thread.
   PPO_TRY_CUDA(cudaHostAlloc(&base, bytes, cudaHostAllocPortable));
-  ppo_pool* p = static_cast<ppo_pool*>(std::malloc(sizeof(ppo_pool)));
-  if (!p) {
-    cudaFreeHost(base);
-    return set_error(PPO_ENOMEM, "ppo_pool_create: host malloc failed");
-  }
   p->base = base;
   p->bytes = bytes;
+  p->numa_node = -1;
+  p->registered = false;
+  return PPO_OK;
+}
+
+int ppo_pool_create_numa(uint64_t bytes, int device, int numa_node, ppo_pool** out, int* node_out) {
+  if (!out || bytes == 0) return set_error(PPO_EINVAL, "ppo_pool_create_numa: bad arguments");
+  *out = nullptr;
+  if (node_out) *node_out = -1;
+  ppo_pool* p = static_cast<ppo_pool*>(std::calloc(1, sizeof(ppo_pool)));
+  if (!p) return set_error(PPO_ENOMEM, "ppo_pool_create_numa: host malloc failed");
+  int node = numa_node == -1 ? gpu_numa_node(device) : numa_node;
+  if (node < 0 || numa_node == -2 || numa_nodes_online() < 2 || node >= 1024) {
+    int rc = pool_from_host_alloc(bytes, p);
+    if (rc != PPO_OK) {
+      std::free(p);
+      return rc;
+    }
+    *out = p;
+    return PPO_OK;
+  }
+  // Bind the pages to the GPU's node BEFORE they are touched, touch them, then pin
+  // them for the copy engines.  (A remote node halves the host-link rate a DMA
+  // engine sees on 2-socket HGX boxes.)
+  const long page = sysconf(_SC_PAGESIZE);
+  const uint64_t len = (bytes + page - 1) / page * page;
+  void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (base == MAP_FAILED) {
+    std::free(p);
+    return set_error(PPO_ENOMEM, "ppo_pool_create_numa: mmap of %llu bytes failed", (unsigned long long)len);
+  }
+  unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+  mask[node / (8 * sizeof(unsigned long))] |= 1UL << (node % (8 * sizeof(unsigned long)));
+  const int kMpolBind = 2;
+  if (syscall(SYS_mbind, base, len, kMpolBind, mask, (unsigned long)1024, 0u) != 0) {
+    munmap(base, len);
+    std::free(p);
+    return set_error(PPO_EINVAL, "ppo_pool_create_numa: mbind to node %d failed", node);
+  }
+  for (uint64_t off = 0; off < len; off += page) static_cast<volatile char*>(base)[off] = 0;  // fault in on `node`
+  cudaError_t e = cudaHostRegister(base, len, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(base, len);
+    std::free(p);
+    return cuda_error(e, "cudaHostRegister");
+  }
+  p->base = base;
+  p->bytes = len;
+  p->numa_node = node;
+  p->registered = true;
+  if (node_out) *node_out = node;
   *out = p;
   return PPO_OK;
 }
 
+int ppo_pool_create(uint64_t bytes, ppo_pool** out) { return ppo_pool_create_numa(bytes, 0, -2, out, nullptr); }
+
 int ppo_pool_destroy(ppo_pool* pool) {
   if (!pool) return PPO_OK;
-  cudaError_t e = cudaFreeHost(pool->base);
+  cudaError_t e = cudaSuccess;
+  const bool registered = pool->registered;
+  if (registered) {
+    e = cudaHostUnregister(pool->base);
+    munmap(pool->base, pool->bytes);
+  } else {
+    e = cudaFreeHost(pool->base);
+  }
   std::free(pool);
-  if (e != cudaSuccess) return cuda_error(e, "cudaFreeHost");
+  if (e != cudaSuccess) return cuda_error(e, registered ? "cudaHostUnregister" : "cudaFreeHost");
   return PPO_OK;
 }
+
+int ppo_pool_numa_node(const ppo_pool* pool) { return pool ? pool->numa_node : -1; }
 
 void* ppo_pool_base(const ppo_pool* pool) { return pool ? pool->base : nullptr; }
 

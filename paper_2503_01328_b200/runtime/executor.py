@@ -191,6 +191,39 @@ class HostTransport:
         self.end_iteration()
 
 
+class NcclLoopbackTransport:
+    """``mode="nccl_loopback"``: one rank alone whose stage-boundary messages still go
+    through NCCL -- a 1-rank communicator, each message a grouped self send/recv --
+    with the neighbours emulated: a send's payload lands in a sink, a receive gets
+    the runner's synthetic upstream activation / downstream gradient.  It exercises
+    the NCCL path (incl. capture into the whole-iteration CUDA graph) on a one-GPU box
+    with the same numerics as ``mode="emulate"``."""
+
+    def __init__(self, device: int):
+        self.comm = native.NcclComm(native.NcclComm.unique_id(), 1, 0, device)
+        self.runner = None  # set by execute: the synthetic tensors live on the runner
+        self.sink = None
+
+    def send(self, rank, op, buf, stream) -> bool:
+        if self.sink is None or self.sink.numel() < buf.numel():
+            self.sink = torch.empty_like(buf)
+        n = buf.numel() * buf.element_size()
+        self.comm.p2p([(True, 0, buf.data_ptr(), n), (False, 0, self.sink.data_ptr(), n)], stream.cuda_stream)
+        return True
+
+    def recv(self, rank, op, buf, stream) -> bool:
+        src = self.runner.synthetic_x if op.kind == "RECV_ACT" else self.runner.synthetic_dy
+        n = buf.numel() * buf.element_size()
+        self.comm.p2p([(True, 0, src.data_ptr(), n), (False, 0, buf.data_ptr(), n)], stream.cuda_stream)
+        return True
+
+    def end_iteration(self):
+        pass
+
+    def close(self):
+        self.comm.close()
+
+
 _NCCL_TRANSPORTS = {}
 
 
@@ -257,9 +290,11 @@ class RankRunner:
         self.emulate = emulate
         my_stages = [s for s in range(sched.num_stages) if sched.placement[s] == self.rank]
         with torch.cuda.device(self.device):
+            ws = Stage.new_workspace(cfg, self.device)  # one workspace for all of this rank's stages
             self.stages = {
                 s: Stage(cfg, s, sched.num_stages, microbatches, self.device, params=params,
-                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm, offload=offload_tensors, attn=attn)
+                         layers=stage_layers(cfg, sched.num_stages, s), seed=seed, gemm=gemm, offload=offload_tensors,
+                         attn=attn, workspace=ws)
                 for s in my_stages
             }
             lays = [st.layout for st in self.stages.values()]
@@ -277,7 +312,8 @@ class RankRunner:
             if program.n_host_slots:
                 slot_bytes = (self.host_bytes + 4095) // 4096 * 4096
                 check_host_memory(program.n_host_slots * slot_bytes)
-                self.pool = native.PinnedPool(program.n_host_slots * slot_bytes)
+                # NUMA-bound to this GPU's node before first touch (ppo_pool_create_numa)
+                self.pool = native.PinnedPool(program.n_host_slots * slot_bytes, device=self.device.index)
                 self.host_slot_base = [self.pool.carve(slot_bytes) for _ in range(program.n_host_slots)]
             s_, h = cfg.seq, cfg.hidden
             mk = lambda: torch.empty(s_, h, dtype=torch.bfloat16, device=self.device)  # noqa: E731
@@ -362,7 +398,8 @@ class RankRunner:
 
     @property
     def ws_bytes(self) -> int:
-        return sum(t.numel() * t.element_size() for st in self.stages.values() for t in st.ws.values())
+        uniq = {t.data_ptr(): t for st in self.stages.values() for t in st.ws.values()}  # shared across stages
+        return sum(t.numel() * t.element_size() for t in uniq.values())
 
     def _rkey(self, op):
         """Resident slot as part of a pass-graph key (None when there is no resident part)."""
@@ -653,6 +690,9 @@ class RankRunner:
         if self.pool is not None:
             self.pool.close()
             self.pool = None
+        if isinstance(self.transport, NcclLoopbackTransport):
+            self.transport.close()
+            self.transport = None
 
 
 def host_memory_available() -> int:
@@ -883,13 +923,14 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
 
     mode: "virtual" (all ranks, one GPU), "emulate" (``rank`` alone, loopback
     boundary) or "nccl" (this process is ``rank`` of a torchrun job; "gloo" is the
-    same over host copies, for ranks that share a GPU in tests).
+    same over host copies, for ranks that share a GPU in tests; "nccl_loopback" is
+    ``rank`` alone with its boundary messages through a 1-rank NCCL communicator).
     ``tokens``: [m, s+1] int64 host tensor (pinned for the e2e path).
     ``offload_tensors``: None (an offloaded pair moves its whole saved set) or the
     (local layer, name) tensors that move (partial offload, ``layout.make_layout``).
     ``iteration_graph``: after one eager iteration, capture a whole iteration -- every
     stream, event edge, pass, D2H/H2D and the optimizer step -- into ONE CUDA graph and
-    replay it (modes "emulate" / "virtual"): no host issue and no per-launch command
+    replay it (every mode but "gloo"; NCCL p2p kernels become graph nodes): no host issue and no per-launch command
     fetch over the host link the copy engines are saturating.
     ``pass_timing=False`` (graph mode): no per-pass timestamps inside the graph, only
     the iteration's start/end -- the returned trace then has no passes.
@@ -914,6 +955,8 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         ranks = [rank if rank is not None else 0]
     programs = {r: lower(sched, plan, r, stream_mode=stream_mode, emulate_neighbors=(mode == "emulate"),
                       spare_slabs=spare_slabs) for r in ranks}
+    if mode == "nccl_loopback" and len(ranks) != 1:  # pragma: no cover
+        raise ValueError("nccl_loopback runs one rank")
     transport = None
     if mode == "virtual":
         transport = LocalTransport()
@@ -923,6 +966,8 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         transport = nccl_transport(ranks[0], dist.get_world_size(), dev.index, pipeline_edges(sched))
     elif mode == "gloo":
         transport = HostTransport(ranks[0])
+    elif mode == "nccl_loopback":
+        transport = NcclLoopbackTransport(dev.index)
     elif mode != "emulate":
         raise ValueError(f"unknown mode {mode!r}")
     dist_mode = mode in ("nccl", "gloo")
@@ -944,12 +989,16 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     runners = [RankRunner(programs[r], model, sched, m, dev, transport=transport, emulate=(mode == "emulate"),
                           params=params, optimizer=optimizer, lr=lr, verify_roundtrip=verify_roundtrip,
                           use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors, attn=attn) for r in ranks]
+    if mode == "nccl_loopback":
+        transport.runner = runners[0]
     if tokens is None:
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
     tokens_dev = torch.empty(tokens.shape, dtype=torch.int64, device=dev)
     secs, losses, walls, host_secs = [], [], [], []
-    whole = (iteration_graph and mode in ("emulate", "virtual") and not probe_kernels
+    # the host-copy transport (gloo) cannot be captured; NCCL p2p can (also across ranks:
+    # every rank captures the same per-rank program and replays it after a barrier)
+    whole = (iteration_graph and mode in ("emulate", "virtual", "nccl", "nccl_loopback") and not probe_kernels
              and optimizer in ("none", "sgd") and warmup + iters > 1)
     origin = torch.cuda.Stream(dev) if whole else None
     graph = None
@@ -1011,6 +1060,7 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
         "wbuf_bytes": sum(r.wbuf_bytes for r in runners),
         "workspace_bytes": sum(r.ws_bytes for r in runners),
         "state_bytes": state,
+        "pool_numa_node": {r.rank: (r.pool.numa_node if r.pool is not None else None) for r in runners},
     }
     passes = [p for r in runners for p in r.measured_passes()] if (pass_timing or not whole) else []
     slab_bytes = max(r.slab_bytes for r in runners)

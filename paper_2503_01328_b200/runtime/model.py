@@ -138,7 +138,7 @@ class Stage:
 
     def __init__(self, cfg: ModelConfig, stage: int, num_stages: int, microbatches: int, device, params=None,
                  layers: list[int] | None = None, seed: int = 1234, gemm: str = "auto", offload=None,
-                 attn: str = "auto"):
+                 attn: str = "auto", workspace: dict | None = None):
         native.require_cuda()
         if gemm not in ("auto", "best", "tcgen05", "cublas"):
             raise ValueError(f"gemm backend {gemm!r}")
@@ -187,12 +187,10 @@ class Stage:
         self.state_bytes = sum(t.numel() * t.element_size() for d in (self.w, self.g, self.master) for t in d.values())
         s, h = cfg.seq, cfg.hidden
         bf = dict(device=self.device, dtype=torch.bfloat16)
-        self.ws = {
-            "ln": torch.empty(s, h, **bf), "a": torch.empty(s, h, **bf), "g": torch.empty(s, 4 * h, **bf),
-            "big": torch.empty(s, 4 * h, **bf), "dm": torch.empty(s, h, **bf), "dh1": torch.empty(s, h, **bf),
-            "da": torch.empty(s, h, **bf), "t": torch.empty(s, h, **bf), "dy": torch.empty(s, h, **bf),
-            "dqkv": torch.empty(s, 3 * h, **bf),
-        }
+        # recompute / GEMM workspace (17 s*h bf16): read and written only inside one pass, so
+        # the stages of one rank share a single copy (``workspace=``; passes of a rank run
+        # one at a time on its compute stream)
+        self.ws = workspace if workspace is not None else self.new_workspace(cfg, self.device)
         self.zero_bias = torch.zeros(4 * h, device=self.device, dtype=torch.float32)
         self.loss_sum = torch.zeros((), device=self.device, dtype=torch.float32)
         # Per-pass context in device memory, so a captured pass (CUDA graph) serves every
@@ -207,6 +205,17 @@ class Stage:
             gemm_tune.require(cfg, self.device, gemm, attn)
         self._attn_init()
         self.probe = None  # kernel name -> [bytes_per_launch, [(start_event, end_event), ...]]
+
+    @staticmethod
+    def new_workspace(cfg: ModelConfig, device) -> dict:
+        s, h = cfg.seq, cfg.hidden
+        bf = dict(device=device, dtype=torch.bfloat16)
+        return {
+            "ln": torch.empty(s, h, **bf), "a": torch.empty(s, h, **bf), "g": torch.empty(s, 4 * h, **bf),
+            "big": torch.empty(s, 4 * h, **bf), "dm": torch.empty(s, h, **bf), "dh1": torch.empty(s, h, **bf),
+            "da": torch.empty(s, h, **bf), "t": torch.empty(s, h, **bf), "dy": torch.empty(s, h, **bf),
+            "dqkv": torch.empty(s, 3 * h, **bf),
+        }
 
     def _attn_init(self):
         """One eager attention call on scratch buffers before any capture: records the

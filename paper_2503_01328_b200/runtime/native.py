@@ -52,6 +52,7 @@ class P2POp(ctypes.Structure):
 
 
 _VP, _U64, _I64, _F32, _I32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_float, ctypes.c_int
+ABI_VERSION = 8  # include/ppo_b200.h PPO_ABI_VERSION
 _FP = ctypes.POINTER(ctypes.c_float)
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -63,6 +64,8 @@ SIGNATURES = {
     "ppo_kernel_launches": [],
     "ppo_device_info": [_I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
     "ppo_pool_create": [_U64, ctypes.POINTER(_VP)],
+    "ppo_pool_create_numa": [_U64, _I32, _I32, ctypes.POINTER(_VP), ctypes.POINTER(_I32)],
+    "ppo_pool_numa_node": [_VP],
     "ppo_pool_destroy": [_VP],
     "ppo_pool_base": [_VP],
     "ppo_pool_bytes": [_VP],
@@ -114,7 +117,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.ppo_abi_version() != 7:
+        if lib.ppo_abi_version() != ABI_VERSION:
             raise NativeUnavailable("libppo_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -368,11 +371,23 @@ def timestamp(slot_ptr: int, stream) -> None:
 
 
 class PinnedPool:
-    """Preallocated page-locked host arena carved into host bins (no per-step alloc)."""
+    """Preallocated page-locked host arena carved into host bins (no per-step alloc).
 
-    def __init__(self, nbytes: int):
+    ``numa_node`` -1 (default): pages bound to the NUMA node of ``device``'s PCI
+    function before first touch (``ppo_pool_create_numa``); -2: no binding; >= 0: that
+    node.  ``self.numa_node`` is the node the pages are bound to (-1: single-node host
+    or unbound)."""
+
+    def __init__(self, nbytes: int, device: int | None = None, numa_node: int = -1):
         self._h = ctypes.c_void_p()
-        call("ppo_pool_create", int(nbytes), ctypes.byref(self._h))
+        if device is None:
+            import torch
+
+            device = torch.cuda.current_device()
+        node = _I32(-1)
+        call("ppo_pool_create_numa", int(nbytes), int(device), int(numa_node), ctypes.byref(self._h),
+             ctypes.byref(node))
+        self.numa_node = int(node.value)
         self.base = int(load().ppo_pool_base(self._h))
         self.nbytes = int(nbytes)
         self._cursor = 0
