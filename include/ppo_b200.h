@@ -144,11 +144,23 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
  *   dx = resid_grad + LN_bwd(dy; x, gamma)           (bf16; resid_grad may be NULL)
  *   dgamma += sum_rows(dy * xhat), dbeta += sum_rows(dy)   (fp32 accumulators)
  * and, when drop_out != NULL, drop_out = dropout_bwd(dx; drop_seed, drop_offset, p):
- * the mask replay of the dropout that produced the residual branch feeding x. */
+ * the mask replay of the dropout that produced the residual branch feeding x; and, when
+ * ln_out != NULL, ln_out = LN(x) * gamma + beta -- the LayerNorm recompute the consuming
+ * GEMM's weight gradient needs, from the statistics already in registers (no separate
+ * ppo_layernorm_fwd pass over x). */
 int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const void* resid_grad,
                       void* dx, float* dgamma, float* dbeta, int64_t rows, int64_t hidden,
                       float eps, void* drop_out, float p, uint64_t drop_seed,
-                      uint64_t drop_offset, const uint64_t* drop_offset_base, void* stream);
+                      uint64_t drop_offset, const uint64_t* drop_offset_base, const float* beta,
+                      void* ln_out, void* stream);
+
+/* W-pass recompute of a split backward (GIS / GIS-H / PO; reference builders.py:91-112,
+ * 175-245): ln1 = LN1(x), ln2 = LN2(h1) and g = gelu_tanh(f) in one launch --
+ * the three unsaved operands of the deferred weight-gradient GEMMs.  x, h1, ln1, ln2:
+ * [rows, hidden] bf16; f, g: [rows, 4*hidden] bf16. */
+int ppo_wpass_recompute(const void* x, const void* h1, const void* f, const float* ln1_g,
+                        const float* ln1_b, const float* ln2_g, const float* ln2_b, void* ln1,
+                        void* ln2, void* g, int64_t rows, int64_t hidden, float eps, void* stream);
 
 /* Standalone dropout (forward: y = dropout(x); backward: dx = dropout_bwd(dy) -- the
  * same mask applied to the gradient). */

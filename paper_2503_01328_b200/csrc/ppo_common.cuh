@@ -109,6 +109,23 @@ __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
                "r"(v.z), "r"(v.w));
 }
 
+// gelu_tanh(x) = 0.5 x (1 + tanh(k0 (x + k1 x^3))); tanh on the SFU (tanh.approx.f32,
+// ~2^-11 relative error, far below the bf16 output rounding of 2^-8).
+__device__ __forceinline__ float fast_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x2 = x * x;
+  const float u = k0 * x * fmaf(k1, x2, 1.f);
+  const float th = fast_tanh(u);
+  g = 0.5f * x * (1.f + th);
+  dg = 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * fmaf(3.f * k1, x2, 1.f);
+}
+
 // ------------------------------------------------------------ Philox4x32-10
 struct U32x4 {
   uint32_t v[4];

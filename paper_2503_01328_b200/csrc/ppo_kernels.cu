@@ -34,23 +34,6 @@ __global__ void __launch_bounds__(256) dropout_kernel(const __nv_bfloat16* __res
   }
 }
 
-// gelu_tanh(x) = 0.5 x (1 + tanh(k0 (x + k1 x^3))); tanh on the SFU (tanh.approx.f32,
-// ~2^-11 relative error, far below the bf16 output rounding of 2^-8).
-__device__ __forceinline__ float fast_tanh(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float x2 = x * x;
-  const float u = k0 * x * fmaf(k1, x2, 1.f);
-  const float th = fast_tanh(u);
-  g = 0.5f * x * (1.f + th);
-  dg = 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * fmaf(3.f * k1, x2, 1.f);
-}
-
 // Elementwise kernels move two bf16x8 vectors per thread per iteration (grid stride),
 // all loads of an iteration issued before any math.
 constexpr int kVec = 2;

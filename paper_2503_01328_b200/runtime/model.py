@@ -187,7 +187,7 @@ class Stage:
         self.state_bytes = sum(t.numel() * t.element_size() for d in (self.w, self.g, self.master) for t in d.values())
         s, h = cfg.seq, cfg.hidden
         bf = dict(device=self.device, dtype=torch.bfloat16)
-        # recompute / GEMM workspace (17 s*h bf16): read and written only inside one pass, so
+        # recompute / GEMM workspace (18 s*h bf16): read and written only inside one pass, so
         # the stages of one rank share a single copy (``workspace=``; passes of a rank run
         # one at a time on its compute stream)
         self.ws = workspace if workspace is not None else self.new_workspace(cfg, self.device)
@@ -211,7 +211,8 @@ class Stage:
         s, h = cfg.seq, cfg.hidden
         bf = dict(device=device, dtype=torch.bfloat16)
         return {
-            "ln": torch.empty(s, h, **bf), "a": torch.empty(s, h, **bf), "g": torch.empty(s, 4 * h, **bf),
+            "ln": torch.empty(s, h, **bf), "ln1": torch.empty(s, h, **bf), "a": torch.empty(s, h, **bf),
+            "g": torch.empty(s, 4 * h, **bf),
             "big": torch.empty(s, 4 * h, **bf), "dm": torch.empty(s, h, **bf), "dh1": torch.empty(s, h, **bf),
             "da": torch.empty(s, h, **bf), "t": torch.empty(s, h, **bf), "dy": torch.empty(s, h, **bf),
             "dqkv": torch.empty(s, 3 * h, **bf),
@@ -483,13 +484,15 @@ class Stage:
             self.mm_dgrad_dgelu(dm, self.p(l, "w_fc2"), f, df, None if split else ws["g"])
             if not split:
                 self.wgrad(self.gp(l, "w_fc2"), dm, ws["g"])
-                self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)  # LN2 recompute
-                self.wgrad(self.gp(l, "w_fc1"), df, ws["ln"])
             self.mm_dgrad(df, self.p(l, "w_fc1"), ws["t"])
-            # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay)
-            self._k("layernorm_bwd", 10 * s * h, native.layernorm_bwd, h1, self.p(l, "ln2_g"), ws["t"], dy_cur, ws["dh1"],
-                    self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=da, p=p, drop_seed=seed, drop_offset=off_a, eps=eps,
-                    offset_base=self.ctx)
+            # dh1 = dy + LN2_bwd(dln2); da = dropout_bwd(dh1) (attention-branch mask replay);
+            # unsplit: the same kernel emits the LN2 recompute ln = LN2(h1) for dWfc1
+            self._k("layernorm_bwd", (12 if not split else 10) * s * h, native.layernorm_bwd, h1, self.p(l, "ln2_g"),
+                    ws["t"], dy_cur, ws["dh1"], self.gp(l, "ln2_g"), self.gp(l, "ln2_b"), drop_out=da, p=p,
+                    drop_seed=seed, drop_offset=off_a, eps=eps, offset_base=self.ctx,
+                    beta=None if split else self.p(l, "ln2_b"), ln_out=None if split else ws["ln"])
+            if not split:
+                self.wgrad(self.gp(l, "w_fc1"), df, ws["ln"])
             # attention projection and core
             if not split:
                 self.wgrad(self.gp(l, "w_proj"), da, o)
@@ -501,24 +504,29 @@ class Stage:
             cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
             dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
                 do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
+            grads = None
             if split:
                 self._gather_dqkv(dq, dk, dv, dqkv)  # the W pass needs them after cuDNN's buffers are reused
                 self.mm_dgrad(dqkv, self.p(l, "w_qkv"), ws["t"])
             else:
                 grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
-                self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)  # LN1 recompute
-                w_qkv, g_qkv = self.p(l, "w_qkv"), self.gp(l, "w_qkv")
+                w_qkv = self.p(l, "w_qkv")
                 for j, gj in enumerate(grads):
-                    self.wgrad(g_qkv[j * h:(j + 1) * h], gj, ws["ln"])
                     self.mm_dgrad(gj, w_qkv[j * h:(j + 1) * h], ws["t"], accumulate=j > 0)
-            # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay
+            # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay;
+            # unsplit: the same kernel emits the LN1 recompute ln = LN1(x) for dWqkv
             below = i > 0
             dx_target = ws["dy"] if (below or self.first or dx_out is None) else dx_out
             drop_below = dm_of(i - 1) if below else None
             off_below = self._offsets(self.layers[i - 1])[1] if below else 0
             native.layernorm_bwd(x, self.p(l, "ln1_g"), ws["t"], ws["dh1"], dx_target, self.gp(l, "ln1_g"),
                                  self.gp(l, "ln1_b"), drop_out=drop_below, p=p if below else 0.0,
-                                 drop_seed=seed, drop_offset=off_below, eps=eps, offset_base=self.ctx)
+                                 drop_seed=seed, drop_offset=off_below, eps=eps, offset_base=self.ctx,
+                                 beta=None if split else self.p(l, "ln1_b"), ln_out=None if split else ws["ln"])
+            if grads is not None:
+                g_qkv = self.gp(l, "w_qkv")
+                for j, gj in enumerate(grads):
+                    self.wgrad(g_qkv[j * h:(j + 1) * h], gj, ws["ln"])
             dy_cur = dx_target
         if self.first:
             native.embed_bwd(self.tok[:-1], dy_cur, self.g["wte"], self.g["wpe"])
@@ -531,13 +539,13 @@ class Stage:
         for i, l in enumerate(self.layers):
             x, o, h1, f = (slab.get(i, n) for n in ("x", "o", "h1", "f"))
             b = wbuf[i]
-            self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])  # GeLU recompute
+            # LN1, LN2 and GeLU recompute in one launch (12 s*h*2 bytes)
+            self._k("wpass_recompute", 24 * s * h, native.wpass_recompute, x, h1, f, self.p(l, "ln1_g"),
+                    self.p(l, "ln1_b"), self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln1"], ws["ln"], ws["g"], eps)
             self.wgrad(self.gp(l, "w_fc2"), b["dm"], ws["g"])
-            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)
             self.wgrad(self.gp(l, "w_fc1"), b["df"], ws["ln"])
             self.wgrad(self.gp(l, "w_proj"), b["da"], o)
-            self._k("layernorm_fwd", 4 * s * h, native.layernorm_fwd, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"), ws["ln"], eps)
-            self.wgrad(self.gp(l, "w_qkv"), b["dqkv"], ws["ln"])
+            self.wgrad(self.gp(l, "w_qkv"), b["dqkv"], ws["ln1"])
 
     # -------------------------------------------------------------- optimizer
     def sgd_step(self, lr: float = 1e-4):

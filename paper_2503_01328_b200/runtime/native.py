@@ -73,7 +73,9 @@ SIGNATURES = {
     "ppo_pack": [ctypes.POINTER(GatherItem), _I32, _VP, _VP],
     "ppo_layernorm_fwd": [_VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP],
     "ppo_residual_dropout_ln_fwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _F32, _U64, _U64, _VP, _VP],
-    "ppo_layernorm_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP, _F32, _U64, _U64, _VP, _VP],
+    "ppo_layernorm_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP, _F32, _U64, _U64, _VP, _VP, _VP,
+                          _VP],
+    "ppo_wpass_recompute": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP],
     "ppo_dropout": [_VP, _VP, _I64, _F32, _U64, _U64, _VP, _VP],
     "ppo_gelu_fwd": [_VP, _VP, _I64, _VP],
     "ppo_gelu_bwd": [_VP, _VP, _VP, _VP, _I64, _VP],
@@ -212,14 +214,24 @@ def residual_dropout_ln_fwd(resid, branch, out, gamma, beta, ln, p, seed, offset
 
 
 def layernorm_bwd(x, gamma, dy, resid_grad, dx, dgamma, dbeta, drop_out=None, p=0.0, drop_seed=0,
-                  drop_offset=0, eps=1e-5, stream=None, offset_base=None):
-    _check_bf16(x, dy, resid_grad, dx, drop_out)
+                  drop_offset=0, eps=1e-5, stream=None, offset_base=None, beta=None, ln_out=None):
+    """dx = resid_grad + LN_bwd(dy; x); dgamma/dbeta += ...; drop_out = dropout_bwd(dx);
+    ln_out = LN(x)*gamma + beta (the recompute, when given)."""
+    _check_bf16(x, dy, resid_grad, dx, drop_out, ln_out)
     h = x.shape[-1]
     call(
         "ppo_layernorm_bwd", _ptr(x), _ptr(gamma), _ptr(dy), _ptr(resid_grad), _ptr(dx), _ptr(dgamma),
         _ptr(dbeta), x.numel() // h, h, eps, _ptr(drop_out), p, drop_seed, drop_offset, _ptr(offset_base),
-        _stream(stream),
+        _ptr(beta), _ptr(ln_out), _stream(stream),
     )
+
+
+def wpass_recompute(x, h1, f, ln1_g, ln1_b, ln2_g, ln2_b, ln1, ln2, g, eps=1e-5, stream=None):
+    """ln1 = LN1(x), ln2 = LN2(h1), g = gelu(f) in one launch (split-backward W pass)."""
+    _check_bf16(x, h1, f, ln1, ln2, g)
+    h = x.shape[-1]
+    call("ppo_wpass_recompute", _ptr(x), _ptr(h1), _ptr(f), _ptr(ln1_g), _ptr(ln1_b), _ptr(ln2_g), _ptr(ln2_b),
+         _ptr(ln1), _ptr(ln2), _ptr(g), x.numel() // h, h, eps, _stream(stream))
 
 
 def dropout(x, y, p, seed, offset, stream=None, offset_base=None):

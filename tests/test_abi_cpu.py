@@ -85,7 +85,8 @@ def test_row_kernels_do_not_spill(lib):
         pytest.skip("cuobjdump not available")
     out = subprocess.run([tool, "-res-usage", native.LIB_PATH], capture_output=True, text=True).stdout
     usage = dict(re.findall(r"Function (\S+):\s*\n\s*(REG:.*)", out))
-    bwd = {f: u for f, u in usage.items() if "ln_bwd_kernel" in f}
+    # the default dispatch (register accumulators, next-row prefetch: ...Lb0ELb1ELi1E)
+    bwd = {f: u for f, u in usage.items() if "ln_bwd_kernel" in f and "Lb0ELb1ELi1E" in f}
     assert len(bwd) >= 10
     for f, u in bwd.items():
         assert "STACK:0 " in u and "LOCAL:0 " in u, (f, u)

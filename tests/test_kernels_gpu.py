@@ -101,6 +101,55 @@ def test_layernorm_bwd(rows, h, with_resid, p):
         assert torch.equal(alone, drop)
 
 
+@pytest.mark.parametrize("rows,h", [(200, 256), (64, 2048), (40, 5120), (30, 8192)])
+def test_layernorm_bwd_emits_ln_recompute(rows, h):
+    """ln_out: the LN recompute emitted by the backward equals LN(x) (oracle, bf16
+    rounding) and is 1 ulp-close to the standalone forward; dx is unchanged by it."""
+    rng = np.random.default_rng(3 * rows + h)
+    x = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32) * 2)
+    dy = ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32))
+    gamma = (1 + 0.1 * rng.standard_normal(h)).astype(np.float32)
+    beta = (0.1 * rng.standard_normal(h)).astype(np.float32)
+    g_, b_ = torch.from_numpy(gamma).to(DEV), torch.from_numpy(beta).to(DEV)
+    outs = []
+    for with_ln in (False, True):
+        dx = torch.empty(rows, h, device=DEV, dtype=torch.bfloat16)
+        ln = torch.empty_like(dx) if with_ln else None
+        dgamma, dbeta = torch.zeros(h, device=DEV), torch.zeros(h, device=DEV)
+        native.layernorm_bwd(bf(x), g_, bf(dy), None, dx, dgamma, dbeta, beta=b_ if with_ln else None, ln_out=ln)
+        outs.append((dx, ln))
+    assert torch.equal(outs[0][0], outs[1][0])
+    ln = outs[1][1]
+    np.testing.assert_allclose(npf(ln), ref.layernorm(x, gamma, beta), rtol=2 ** -7, atol=2e-2)
+    alone = torch.empty_like(ln)
+    native.layernorm_fwd(bf(x), g_, b_, alone)
+    assert ref.bf16_ulp_diff(npf(ln), npf(alone)).max() <= 1
+    with pytest.raises(native.PpoError):  # ln_out needs beta
+        native.layernorm_bwd(bf(x), g_, bf(dy), None, outs[0][0], dgamma, dbeta, ln_out=ln)
+
+
+@pytest.mark.parametrize("rows,h", [(100, 256), (64, 2048), (33, 4096), (20, 5120), (12, 8192)])
+def test_wpass_recompute(rows, h):
+    """ln1 = LN1(x), ln2 = LN2(h1), g = gelu(f) in one launch == the three standalone kernels."""
+    rng = np.random.default_rng(rows * 7 + h)
+    x, h1 = (ref.bf16_round(rng.standard_normal((rows, h)).astype(np.float32) * 2) for _ in range(2))
+    f = ref.bf16_round(rng.standard_normal((rows, 4 * h)).astype(np.float32) * 3)
+    p = [torch.from_numpy((1 + 0.1 * rng.standard_normal(h)).astype(np.float32)).to(DEV) for _ in range(2)]
+    q = [torch.from_numpy((0.1 * rng.standard_normal(h)).astype(np.float32)).to(DEV) for _ in range(2)]
+    ln1, ln2 = (torch.empty(rows, h, device=DEV, dtype=torch.bfloat16) for _ in range(2))
+    g = torch.empty(rows, 4 * h, device=DEV, dtype=torch.bfloat16)
+    native.wpass_recompute(bf(x), bf(h1), bf(f), p[0], q[0], p[1], q[1], ln1, ln2, g)
+    g_alone = torch.empty_like(g)
+    native.gelu_fwd(bf(f), g_alone)
+    assert torch.equal(g, g_alone)
+    for got, src, gm, bt in ((ln1, x, p[0], q[0]), (ln2, h1, p[1], q[1])):
+        alone = torch.empty_like(got)
+        native.layernorm_fwd(bf(src), gm, bt, alone)
+        assert ref.bf16_ulp_diff(npf(got), npf(alone)).max() <= 1
+        np.testing.assert_allclose(npf(got), ref.layernorm(src, gm.cpu().numpy(), bt.cpu().numpy()), rtol=2 ** -7,
+                                   atol=2e-2)
+
+
 @pytest.mark.parametrize("n", [8, 4096, 1 << 20])
 def test_gelu_fwd_bwd(n):
     rng = np.random.default_rng(n)
