@@ -141,6 +141,53 @@ def workload_config(config: str, world: int) -> dict:
 # ----------------------------------------------------------------------- reference arm
 
 
+def reference_simulator(config: str, reps: int = 5) -> dict:
+    """The reference's OWN CPU path for this workload, unmodified: ``ppoff`` 0.1.0
+    installed into baseline/_ref (pip --target from /root/reference/pkg), timed on the
+    host: plan (``build_1f1b_full_offload``) + ``simulate`` of the configured schedule,
+    single-threaded CPython (the reference is pure Python), median of ``reps`` after one
+    warm-up.  B200 pass costs from the reference's own FLOP model at 50% of the dense
+    bf16 peak and a 55 GB/s host link."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "ppoff")):
+        return {"unavailable": "baseline/_ref has no ppoff install"}
+    import importlib
+
+    saved = {k: v for k, v in sys.modules.items() if k == "ppoff" or k.startswith("ppoff.")}
+    sys.path.insert(0, ref_dir)
+    try:
+        for k in saved:
+            del sys.modules[k]
+        ppoff = importlib.import_module("ppoff")
+        L, h, heads, s, _v, pp, m = CONFIGS[config]
+        model = ppoff.ModelSpec(h, s, 1, L // pp, 2)
+        hw = ppoff.HardwareSpec(compute_bandwidth=0.5 * 2.25e15, transfer_bandwidth=55e9)
+        costs = ppoff.estimate_pass_costs(model, hw)
+        t_o = ppoff.offload_round_trip(model, hw)
+        times = []
+        for _ in range(reps + 1):
+            t0 = time.perf_counter()
+            sched, plan = ppoff.build_1f1b_full_offload(pp, m, costs, t_o)
+            t1 = time.perf_counter()
+            trace = ppoff.simulate(sched, plan, costs, hw, None, model)
+            t2 = time.perf_counter()
+            times.append((t1 - t0, t2 - t1))
+        plan_s = statistics.median(t[0] for t in times[1:])
+        sim_s = statistics.median(t[1] for t in times[1:])
+        return {"source": f"unmodified ppoff from baseline/_ref ({ppoff.__file__})", "cores": 1,
+                "workload": f"build_1f1b_full_offload({pp}, {m}) + simulate, ModelSpec({h}, {s}, 1, {L // pp})",
+                "plan_ms": 1e3 * plan_s, "simulate_ms": 1e3 * sim_s,
+                "modelled_tokens_per_s": m * s / float(trace.makespan),
+                "modelled_peak_units_rank0": ppoff.peak_memory(trace)["per_device"][0][0]}
+    except Exception as e:  # noqa: BLE001 - a baseline report, never the product
+        return {"unavailable": f"{type(e).__name__}: {e}"[:300]}
+    finally:
+        sys.path.remove(ref_dir)
+        for k in [k for k in sys.modules if k == "ppoff" or k.startswith("ppoff.")]:
+            del sys.modules[k]
+        sys.modules.update(saved)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU implementation of the path (oracle port), rank 0 only."""
     if rank != 0:
@@ -163,7 +210,8 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload_config(args.config, world),
                        reference_step=f"one microbatch F+B of the {layers}-layer stage on the host cores (bounded sample)"),
-        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": vals[0]["sample"]},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": vals[0]["sample"],
+                         "reference_simulator": reference_simulator(args.config)},
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -183,15 +231,17 @@ def measure_kernels(s, h, heads, dev, torch, native, launches=16, sets=4):
     for _ in range(sets):
         sets_.append({
             "x": torch.randn(s, h, **bf), "y": torch.randn(s, h, **bf), "z": torch.randn(s, h, **bf),
-            "o": torch.empty(s, h, **bf), "u": torch.empty(s, h, **bf),
+            "o": torch.empty(s, h, **bf), "u": torch.empty(s, h, **bf), "w": torch.empty(s, h, **bf),
             "f": torch.randn(s, 4 * h, **bf), "g": torch.empty(s, 4 * h, **bf), "d": torch.randn(s, 4 * h, **bf),
             "lse": torch.randn(heads, s, device=dev), "slab": torch.empty(E + 4 * heads * s + 512, dtype=torch.uint8, device=dev),
         })
     gam, bet = torch.ones(h, device=dev), torch.zeros(h, device=dev)
     dg, db = torch.zeros(h, device=dev), torch.zeros(h, device=dev)
     cases = {
-        "layernorm_bwd": ("ppo_layernorm_bwd", 5 * E, lambda t: native.layernorm_bwd(
-            t["x"], gam, t["y"], t["z"], t["o"], dg, db, drop_out=t["u"], p=0.1, drop_seed=4, drop_offset=5)),
+        # as the unsplit backward runs it: dx, the dropout replay below AND the LN recompute
+        "layernorm_bwd": ("ppo_layernorm_bwd", 6 * E, lambda t: native.layernorm_bwd(
+            t["x"], gam, t["y"], t["z"], t["o"], dg, db, drop_out=t["u"], p=0.1, drop_seed=4, drop_offset=5,
+            beta=bet, ln_out=t["w"])),
         "residual_dropout_ln_fwd": ("ppo_residual_dropout_ln_fwd", 4 * E, lambda t: native.residual_dropout_ln_fwd(
             t["x"], t["y"], t["o"], gam, bet, t["u"], 0.1, 42, 1)),
         "layernorm_fwd": ("ppo_layernorm_fwd", 2 * E, lambda t: native.layernorm_fwd(t["x"], gam, bet, t["o"])),
@@ -752,7 +802,7 @@ def cpu_baseline(args):
     stage_sample(256, 4, 512, 1)
     r = stage_sample(h, heads, s, L // pp)
     return {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-            "sample": r["sample"]}
+            "sample": r["sample"], "reference_simulator": reference_simulator(args.config)}
 
 
 def main():

@@ -154,13 +154,13 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
                       uint64_t drop_offset, const uint64_t* drop_offset_base, const float* beta,
                       void* ln_out, void* stream);
 
-/* W-pass recompute of a split backward (GIS / GIS-H / PO; reference builders.py:91-112,
- * 175-245): ln1 = LN1(x), ln2 = LN2(h1) and g = gelu_tanh(f) in one launch --
- * the three unsaved operands of the deferred weight-gradient GEMMs.  x, h1, ln1, ln2:
- * [rows, hidden] bf16; f, g: [rows, 4*hidden] bf16. */
-int ppo_wpass_recompute(const void* x, const void* h1, const void* f, const float* ln1_g,
-                        const float* ln1_b, const float* ln2_g, const float* ln2_b, void* ln1,
-                        void* ln2, void* g, int64_t rows, int64_t hidden, float eps, void* stream);
+/* Two independent LayerNorms in one launch (the W pass of a split backward recomputes
+ * LN1(x) and LN2(h1) for the deferred weight gradients; reference builders.py:91-112,
+ * 175-245): y_a = LN(x_a)*gamma_a + beta_a, y_b = LN(x_b)*gamma_b + beta_b,
+ * all [rows, hidden] bf16. */
+int ppo_layernorm_fwd2(const void* x_a, const float* gamma_a, const float* beta_a, void* y_a,
+                       const void* x_b, const float* gamma_b, const float* beta_b, void* y_b,
+                       int64_t rows, int64_t hidden, float eps, void* stream);
 
 /* Standalone dropout (forward: y = dropout(x); backward: dx = dropout_bwd(dy) -- the
  * same mask applied to the gradient). */

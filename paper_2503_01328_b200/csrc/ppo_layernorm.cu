@@ -73,12 +73,18 @@ __device__ __forceinline__ void load8f(const float* p, float (&o)[8]) {
 // out = resid + dropout(branch)  (kResidual)  or  v = src  (!kResidual);  ln = LN(v).
 // The next row's vectors are requested before the current row is reduced, so DRAM
 // latency overlaps the shuffle reduction and the stores (register double-buffering).
-template <bool kResidual, int W, int kVecPerLane, int G>
+//
+// kDual (no residual): two independent LayerNorms in one launch -- rows [0, rows_a) are
+// LN(src) * gamma + beta -> ln, rows [rows_a, rows) are LN(resid) * gamma_b + beta_b -> out
+// (the W pass's LN1 and LN2 recompute: one 4E launch instead of two 2E launches).
+template <bool kResidual, int W, int kVecPerLane, int G, bool kDual = false>
 __global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
     const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
     const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
     int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add,
-    const uint64_t* __restrict__ offset_base, int use_dropout) {
+    const uint64_t* __restrict__ offset_base, int use_dropout, const float* __restrict__ gamma_b = nullptr,
+    const float* __restrict__ beta_b = nullptr, int64_t rows_a = 0) {
+  static_assert(!(kDual && kResidual), "dual LayerNorm has no residual");
   pdl_wait();
   extern __shared__ __align__(16) float sm[];
   const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
@@ -95,7 +101,10 @@ __global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
     for (int j = 0; j < kVecPerLane; ++j) {
       const int v = L + 32 * W * j;
       if (v < nvec) {
-        b[j] = ld_stream(src + r * hidden + 8 * v);
+        if (kDual)
+          b[j] = ld_stream(r < rows_a ? src + r * hidden + 8 * v : resid + (r - rows_a) * hidden + 8 * v);
+        else
+          b[j] = ld_stream(src + r * hidden + 8 * v);
         if (kResidual) a[j] = ld_stream(resid + r * hidden + 8 * v);
       }
     }
@@ -133,17 +142,21 @@ __global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
       group_sum<W, 2>(sums, scratch, group);
       const float mean = sums[0] * inv_h;
       const float rstd = rsqrtf(fmaxf(sums[1] * inv_h - mean * mean, 0.f) + eps);
+      const bool second = kDual && row >= rows_a;
+      const float* gm = second ? gamma_b : gamma;
+      const float* bt = second ? beta_b : beta;
+      __nv_bfloat16* dst = second ? out + (rbase - rows_a * hidden) : ln + rbase;
 #pragma unroll
       for (int j = 0; j < kVecPerLane; ++j) {
         const int v = L + 32 * W * j;
         if (v >= nvec) continue;
         float val[8], g[8], b[8], y[8];
         unpack8(rb[j], val);
-        load8f(gamma + 8 * v, g);
-        load8f(beta + 8 * v, b);
+        load8f(gm + 8 * v, g);
+        load8f(bt + 8 * v, b);
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = (val[i] - mean) * rstd * g[i] + b[i];
-        st_stream(ln + rbase + 8 * v, pack8(y));
+        st_stream(dst + 8 * v, pack8(y));
       }
     }
 #pragma unroll
@@ -156,20 +169,20 @@ __global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
 
 // dx = resid_grad + LN_bwd(dy; x) (statistics recomputed from x);
 // dgamma += sum_rows dy*xhat, dbeta += sum_rows dy;  drop_out = dropout_bwd(bf16(dx));
-// ln_out = LN(x) * gamma + beta (optional): the LayerNorm RECOMPUTE the weight gradient
-// of the GEMM that consumed LN(x) in the forward needs, emitted from the statistics and
-// the x already in registers -- one extra write instead of a separate read-x/write-ln
+// kLnOut: ln_out = LN(x) * gamma + beta -- the LayerNorm RECOMPUTE the weight gradient of
+// the GEMM that consumed LN(x) in the forward needs, emitted from the statistics and the
+// x already in registers: one extra write instead of a separate read-x / write-ln
 // kernel (K3 fused into the backward).
 //
-// gamma / beta are staged in shared memory once per CTA (every row reads the same h
-// parameters).  The parameter-gradient sums either live in registers for the whole row
-// loop (kAccSmem = false: a lane owns the same VPL x 8 columns on every row it visits;
-// folded per CTA at the end) or go straight to shared memory with red.shared.add per
-// row (kAccSmem = true: 32 fewer registers a thread, more resident warps).  kPrefetch:
-// the next row's vectors are requested before the current row is reduced (register
-// double-buffering) -- latency hiding by ILP instead of by more warps.
-template <int W, int kVecPerLane, int G, bool kAccSmem, bool kPrefetch, int kMinBlocks>
-__global__ void __launch_bounds__(32 * W * G, kMinBlocks) ln_bwd_kernel(
+// A lane owns the same kVecPerLane x 8 columns on every row it visits, so the
+// parameter-gradient sums live in registers for the whole row loop; at the end the
+// CTA's row groups are folded in shared memory and flushed with one 16-byte vector
+// atomic per 4 columns.  kPrefetch: the next row's vectors are requested before the
+// current row is reduced (register double-buffering).  (Shared-memory accumulation per
+// row and shared-memory staging of gamma were measured 1.6-3x slower / spilling,
+// profiles/r2_ln_bwd_variants.jsonl.)
+template <int W, int kVecPerLane, int G, bool kLnOut, bool kPrefetch>
+__global__ void __launch_bounds__(32 * W * G) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ resid_grad, __nv_bfloat16* __restrict__ dx,
     float* __restrict__ dgamma, float* __restrict__ dbeta, __nv_bfloat16* __restrict__ ln_out, int64_t rows,
@@ -178,30 +191,19 @@ __global__ void __launch_bounds__(32 * W * G, kMinBlocks) ln_bwd_kernel(
   pdl_wait();
   extern __shared__ __align__(16) float sm[];
   const uint64_t offset = offset_add + (offset_base ? __ldg(offset_base) : 0ull);
-  float* s_gamma = sm;               // [h]
-  float* s_beta = sm + hidden;       // [h] (ln_out only)
-  float* s_acc = sm + 2 * hidden;    // [2h]: dgamma partials, then dbeta partials
-  float* scratch = sm + 4 * hidden;  // group reductions
-  for (int c = 4 * threadIdx.x; c < hidden; c += 4 * blockDim.x) {
-    *reinterpret_cast<float4*>(s_gamma + c) = __ldg(reinterpret_cast<const float4*>(gamma + c));
-    if (ln_out) *reinterpret_cast<float4*>(s_beta + c) = __ldg(reinterpret_cast<const float4*>(beta + c));
-    *reinterpret_cast<float4*>(s_acc + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(s_acc + hidden + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncthreads();
+  float* s_acc = sm;                 // [2h]: dgamma partials, then dbeta partials
+  float* scratch = sm + 2 * hidden;  // group reductions
   const int group = threadIdx.x / (32 * W);
   const int L = threadIdx.x % (32 * W);
   const int nvec = hidden >> 3;
   const float inv_h = 1.f / (float)hidden;
   const bool has_resid = resid_grad != nullptr;
   const int64_t step = (int64_t)gridDim.x * G;
-  float acc_g[kAccSmem ? 1 : kVecPerLane][8], acc_b[kAccSmem ? 1 : kVecPerLane][8];
-  if constexpr (!kAccSmem) {
+  float acc_g[kVecPerLane][8], acc_b[kVecPerLane][8];
 #pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j)
+  for (int j = 0; j < kVecPerLane; ++j)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc_g[j][i] = acc_b[j][i] = 0.f;
-  }
+    for (int i = 0; i < 8; ++i) acc_g[j][i] = acc_b[j][i] = 0.f;
   uint4 rx[kVecPerLane], rd[kVecPerLane], rr[kVecPerLane];
   auto fetch = [&](int64_t r, uint4 (&a)[kVecPerLane], uint4 (&b)[kVecPerLane], uint4 (&c)[kVecPerLane]) {
 #pragma unroll
@@ -229,12 +231,10 @@ __global__ void __launch_bounds__(32 * W * G, kMinBlocks) ln_bwd_kernel(
     for (int j = 0; j < kVecPerLane; ++j) {
       const int v = L + 32 * W * j;
       if (v >= nvec) continue;
-      float xv[8], dv[8];
+      float xv[8], dv[8], g[8];
       unpack8(rx[j], xv);
       unpack8(rd[j], dv);
-      const float4 g0 = *reinterpret_cast<const float4*>(s_gamma + 8 * v);
-      const float4 g1 = *reinterpret_cast<const float4*>(s_gamma + 8 * v + 4);
-      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      load8f(gamma + 8 * v, g);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float gi = dv[i] * g[i];
@@ -253,40 +253,24 @@ __global__ void __launch_bounds__(32 * W * G, kMinBlocks) ln_bwd_kernel(
     for (int j = 0; j < kVecPerLane; ++j) {
       const int v = L + 32 * W * j;
       if (v >= nvec) continue;
-      float xv[8], dv[8], rg[8], d[8];
+      float xv[8], dv[8], g[8], rg[8], d[8];
       unpack8(rx[j], xv);
       unpack8(rd[j], dv);
-      const float4 g0 = *reinterpret_cast<const float4*>(s_gamma + 8 * v);
-      const float4 g1 = *reinterpret_cast<const float4*>(s_gamma + 8 * v + 4);
-      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      load8f(gamma + 8 * v, g);
       if (has_resid) unpack8(rr[j], rg);
-      float xh[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        xh[i] = (xv[i] - mean) * rstd;
-        d[i] = rstd * (dv[i] * g[i] - mg - xh[i] * mgx) + (has_resid ? rg[i] : 0.f);
+        const float xh = (xv[i] - mean) * rstd;
+        d[i] = rstd * (dv[i] * g[i] - mg - xh * mgx) + (has_resid ? rg[i] : 0.f);
+        acc_g[j][i] += dv[i] * xh;
+        acc_b[j][i] += dv[i];
       }
-      if constexpr (kAccSmem) {
+      if constexpr (kLnOut) {
+        float b[8];
+        load8f(beta + 8 * v, b);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          atomicAdd(s_acc + 8 * v + i, dv[i] * xh[i]);
-          atomicAdd(s_acc + hidden + 8 * v + i, dv[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc_g[j][i] += dv[i] * xh[i];
-          acc_b[j][i] += dv[i];
-        }
-      }
-      if (ln_out) {
-        const float4 b0 = *reinterpret_cast<const float4*>(s_beta + 8 * v);
-        const float4 b1 = *reinterpret_cast<const float4*>(s_beta + 8 * v + 4);
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        float y[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = xh[i] * g[i] + bb[i];
-        st_stream(ln_out + rbase + 8 * v, pack8(y));
+        for (int i = 0; i < 8; ++i) xv[i] = (xv[i] - mean) * rstd * g[i] + b[i];
+        st_stream(ln_out + rbase + 8 * v, pack8(xv));
       }
       const uint4 packed = pack8(d);
       st_stream(dx + rbase + 8 * v, packed);
@@ -307,120 +291,27 @@ __global__ void __launch_bounds__(32 * W * G, kMinBlocks) ln_bwd_kernel(
       }
     }
   }
-  if constexpr (!kAccSmem) {  // fold the row groups' register partials into the CTA's
+  // fold the row groups of this CTA in shared memory, one group at a time
+  for (int gi = 0; gi < G; ++gi) {
+    if (group == gi) {
 #pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      const int v = L + 32 * W * j;
-      if (v >= nvec) continue;
+      for (int j = 0; j < kVecPerLane; ++j) {
+        const int v = L + 32 * W * j;
+        if (v >= nvec) continue;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        atomicAdd(s_acc + 8 * v + i, acc_g[j][i]);
-        atomicAdd(s_acc + hidden + 8 * v + i, acc_b[j][i]);
+        for (int i = 0; i < 8; ++i) {
+          const float pg = gi ? s_acc[8 * v + i] : 0.f;
+          const float pb = gi ? s_acc[hidden + 8 * v + i] : 0.f;
+          s_acc[8 * v + i] = pg + acc_g[j][i];
+          s_acc[hidden + 8 * v + i] = pb + acc_b[j][i];
+        }
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
   for (int c = 4 * threadIdx.x; c < hidden; c += 4 * blockDim.x) {
     atomicAdd(reinterpret_cast<float4*>(dgamma + c), *reinterpret_cast<const float4*>(s_acc + c));
     atomicAdd(reinterpret_cast<float4*>(dbeta + c), *reinterpret_cast<const float4*>(s_acc + hidden + c));
-  }
-}
-
-// W-pass recompute of a split backward (GIS / GIS-H / PO, reference builders.py:91-112,
-// 175-245): everything the deferred weight gradients need that was not saved, in ONE
-// launch instead of three -- ln1 = LN1(x), ln2 = LN2(h1) and g = gelu(f) -- so the
-// 12E bytes (E = 2sh) stream through one kernel with enough work to hide the launch
-// ramp the 2E LayerNorm launches could not (profiles/r1_ncu_full_fwd_kernels.txt).
-// A W-warp row group owns row r of all three tensors (f is 4h wide: 4 VPL vectors a lane).
-template <int W, int kVecPerLane>
-__global__ void __launch_bounds__(512) wpass_recompute_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ h1, const __nv_bfloat16* __restrict__ f,
-    const float* __restrict__ ln1_g, const float* __restrict__ ln1_b, const float* __restrict__ ln2_g,
-    const float* __restrict__ ln2_b, __nv_bfloat16* __restrict__ ln1, __nv_bfloat16* __restrict__ ln2,
-    __nv_bfloat16* __restrict__ g, int64_t rows, int hidden, float eps) {
-  pdl_wait();
-  extern __shared__ __align__(16) float sm[];
-  float* sp = sm;                    // [4h]: ln1_g, ln1_b, ln2_g, ln2_b
-  float* scratch = sm + 4 * hidden;  // group reductions
-  for (int c = 4 * threadIdx.x; c < hidden; c += 4 * blockDim.x) {
-    *reinterpret_cast<float4*>(sp + c) = __ldg(reinterpret_cast<const float4*>(ln1_g + c));
-    *reinterpret_cast<float4*>(sp + hidden + c) = __ldg(reinterpret_cast<const float4*>(ln1_b + c));
-    *reinterpret_cast<float4*>(sp + 2 * hidden + c) = __ldg(reinterpret_cast<const float4*>(ln2_g + c));
-    *reinterpret_cast<float4*>(sp + 3 * hidden + c) = __ldg(reinterpret_cast<const float4*>(ln2_b + c));
-  }
-  __syncthreads();
-  const int G = blockDim.x / (32 * W);
-  const int group = threadIdx.x / (32 * W);
-  const int L = threadIdx.x % (32 * W);
-  const int nvec = hidden >> 3;
-  const float inv_h = 1.f / (float)hidden;
-  const int64_t step = (int64_t)gridDim.x * G;
-  for (int64_t row = (int64_t)blockIdx.x * G + group; row < rows; row += step) {
-    const int64_t rbase = row * hidden;
-    uint4 rx[kVecPerLane], rh[kVecPerLane], rf[4 * kVecPerLane];
-#pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      const int v = L + 32 * W * j;
-      if (v < nvec) {
-        rx[j] = ld_stream(x + rbase + 8 * v);
-        rh[j] = ld_stream(h1 + rbase + 8 * v);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4 * kVecPerLane; ++j) {
-      const int v = L + 32 * W * j;
-      if (v < 4 * nvec) rf[j] = ld_stream(f + 4 * rbase + 8 * v);
-    }
-    float sums[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      const int v = L + 32 * W * j;
-      if (v >= nvec) continue;
-      float a[8], b[8];
-      unpack8(rx[j], a);
-      unpack8(rh[j], b);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        sums[0] += a[i];
-        sums[1] += a[i] * a[i];
-        sums[2] += b[i];
-        sums[3] += b[i] * b[i];
-      }
-    }
-    // GeLU while the row statistics are reduced (independent work for the scheduler)
-#pragma unroll
-    for (int j = 0; j < 4 * kVecPerLane; ++j) {
-      const int v = L + 32 * W * j;
-      if (v >= 4 * nvec) continue;
-      float in[8], out[8];
-      unpack8(rf[j], in);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float dg;
-        gelu_and_grad(in[i], out[i], dg);
-      }
-      st_stream(g + 4 * rbase + 8 * v, pack8(out));
-    }
-    group_sum<W, 4>(sums, scratch, group);
-    const float m1 = sums[0] * inv_h, m2 = sums[2] * inv_h;
-    const float r1 = rsqrtf(fmaxf(sums[1] * inv_h - m1 * m1, 0.f) + eps);
-    const float r2 = rsqrtf(fmaxf(sums[3] * inv_h - m2 * m2, 0.f) + eps);
-#pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      const int v = L + 32 * W * j;
-      if (v >= nvec) continue;
-      float a[8], b[8], ya[8], yb[8];
-      unpack8(rx[j], a);
-      unpack8(rh[j], b);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = 8 * v + i;
-        ya[i] = (a[i] - m1) * r1 * sp[c] + sp[hidden + c];
-        yb[i] = (b[i] - m2) * r2 * sp[2 * hidden + c] + sp[3 * hidden + c];
-      }
-      st_stream(ln1 + rbase + 8 * v, pack8(ya));
-      st_stream(ln2 + rbase + 8 * v, pack8(yb));
-    }
   }
 }
 
@@ -574,21 +465,14 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   return PPO_OK;
 }
 
-// LayerNorm-backward launch variant (PPO_LN_BWD=<id> for A/B runs; tools/ln_bwd_sweep.py,
-// profiles/r2_ln_bwd_variants.jsonl):
-//   0: register accumulators + next-row prefetch, <= 128 registers (the round-1 kernel)
-//   1: shared-memory accumulators, no prefetch, 2 CTAs / SM (<= 64 registers at 512 threads)
-//   2: shared-memory accumulators + prefetch
-//   3: register accumulators, no prefetch
-//   4: shared-memory accumulators, no prefetch, 1 CTA / SM
-static int ln_bwd_variant() {
+// PPO_LN_BWD=1: no next-row prefetch (A/B runs; tools/ln_bwd_sweep.py)
+static bool ln_bwd_prefetch() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PPO_LN_BWD");
-    v = e ? atoi(e) : 0;
-    if (v < 0 || v > 4) v = 0;
+    v = (e && atoi(e) == 1) ? 0 : 1;
   }
-  return v;
+  return v == 1;
 }
 
 int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const void* resid_grad, void* dx,
@@ -606,11 +490,11 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
     return set_error(PPO_EINVAL, "ppo_layernorm_bwd: gamma/beta/dgamma/dbeta must be 16-byte aligned");
   // Two vectors per lane per tensor: W = h/512 warps per row (up to 16 at h = 8192).
   const int need = warps_per_row(hidden, 2);
-#define PPO_LN_BWD_K(W, A, P, MB)                                                                              \
+#define PPO_LN_BWD_K(W, O, P)                                                                                  \
   {                                                                                                            \
     constexpr int G = groups_for(W);                                                                           \
-    if ((rc = row_launch(ln_bwd_kernel<W, 2, G, A, P, MB>, rows, hidden, W, 4, &l, G))) return rc;            \
-    launch_pdl(ln_bwd_kernel<W, 2, G, A, P, MB>, l.grid, l.block, l.smem, as_stream(stream),                   \
+    if ((rc = row_launch(ln_bwd_kernel<W, 2, G, O, P>, rows, hidden, W, 2, &l, G))) return rc;                \
+    launch_pdl(ln_bwd_kernel<W, 2, G, O, P>, l.grid, l.block, l.smem, as_stream(stream),                       \
         static_cast<const __nv_bfloat16*>(x), gamma, beta, static_cast<const __nv_bfloat16*>(dy),             \
         static_cast<const __nv_bfloat16*>(resid_grad), static_cast<__nv_bfloat16*>(dx), dgamma, dbeta,        \
         static_cast<__nv_bfloat16*>(ln_out), rows, (int)hidden, eps, static_cast<__nv_bfloat16*>(drop_out),   \
@@ -618,12 +502,11 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
   }
 #define PPO_LN_BWD_W(W)                                            \
   {                                                                \
-    switch (ln_bwd_variant()) {                                    \
-      case 1: PPO_LN_BWD_K(W, true, false, 2) break;               \
-      case 2: PPO_LN_BWD_K(W, true, true, 1) break;                \
-      case 3: PPO_LN_BWD_K(W, false, false, 1) break;              \
-      case 4: PPO_LN_BWD_K(W, true, false, 1) break;               \
-      default: PPO_LN_BWD_K(W, false, true, 1) break;              \
+    const bool pf = ln_bwd_prefetch();                             \
+    if (ln_out) {                                                  \
+      if (pf) PPO_LN_BWD_K(W, true, true) else PPO_LN_BWD_K(W, true, false) \
+    } else {                                                       \
+      if (pf) PPO_LN_BWD_K(W, false, true) else PPO_LN_BWD_K(W, false, false) \
     }                                                              \
   }
   if (need <= 1) PPO_LN_BWD_W(1)
@@ -642,36 +525,40 @@ int ppo_layernorm_bwd(const void* x, const float* gamma, const void* dy, const v
   return PPO_OK;
 }
 
-int ppo_wpass_recompute(const void* x, const void* h1, const void* f, const float* ln1_g, const float* ln1_b,
-                        const float* ln2_g, const float* ln2_b, void* ln1, void* ln2, void* g, int64_t rows,
-                        int64_t hidden, float eps, void* stream) {
-  if (int rc = check_rows("ppo_wpass_recompute", rows, hidden)) return rc;
-  if (!x || !h1 || !f || !ln1_g || !ln1_b || !ln2_g || !ln2_b || !ln1 || !ln2 || !g)
-    return set_error(PPO_EINVAL, "ppo_wpass_recompute: null pointer");
-  if (!aligned16(ln1_g) || !aligned16(ln1_b) || !aligned16(ln2_g) || !aligned16(ln2_b))
-    return set_error(PPO_EINVAL, "ppo_wpass_recompute: LayerNorm parameters must be 16-byte aligned");
+int ppo_layernorm_fwd2(const void* x_a, const float* gamma_a, const float* beta_a, void* y_a, const void* x_b,
+                       const float* gamma_b, const float* beta_b, void* y_b, int64_t rows, int64_t hidden, float eps,
+                       void* stream) {
+  if (int rc = check_rows("ppo_layernorm_fwd2", rows, hidden)) return rc;
+  if (!x_a || !gamma_a || !beta_a || !y_a || !x_b || !gamma_b || !beta_b || !y_b)
+    return set_error(PPO_EINVAL, "ppo_layernorm_fwd2: null pointer");
   if (rows == 0) return PPO_OK;
   RowLaunch l;
   int rc = PPO_OK;
-  // one vector per lane per h-wide tensor (four for f): W = h/256 warps a row, <= 512 threads
-  const int need = warps_per_row(hidden, 1);
-#define PPO_WPASS_W(W, V)                                                                                         \
-  {                                                                                                               \
-    constexpr int G = (512 / (32 * W)) < 1 ? 1 : (512 / (32 * W)) > 4 ? 4 : 512 / (32 * W);                      \
-    if ((rc = row_launch(wpass_recompute_kernel<W, V>, rows, hidden, W, 4, &l, G))) return rc;                   \
-    launch_pdl(wpass_recompute_kernel<W, V>, l.grid, l.block, l.smem, as_stream(stream),                         \
-        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(h1),                             \
-        static_cast<const __nv_bfloat16*>(f), ln1_g, ln1_b, ln2_g, ln2_b, static_cast<__nv_bfloat16*>(ln1),     \
-        static_cast<__nv_bfloat16*>(ln2), static_cast<__nv_bfloat16*>(g), rows, (int)hidden, eps);             \
+  const int vpl = vpl_choice(hidden, 4);
+#define PPO_LN_FWD2_W(W, V)                                                                                   \
+  if ((rc = row_launch(ln_fwd_kernel<false, W, V, fwd_groups_for(W), true>, 2 * rows, hidden, W, 0, &l,       \
+                       fwd_groups_for(W)))) return rc;                                                        \
+  launch_pdl(ln_fwd_kernel<false, W, V, fwd_groups_for(W), true>, l.grid, l.block, l.smem, as_stream(stream),  \
+      static_cast<const __nv_bfloat16*>(x_b), static_cast<const __nv_bfloat16*>(x_a),                        \
+      static_cast<__nv_bfloat16*>(y_b), gamma_a, beta_a, static_cast<__nv_bfloat16*>(y_a), 2 * rows,          \
+      (int)hidden, eps, 0u, 1.f, (uint64_t)0, (uint64_t)0, (const uint64_t*)nullptr, 0, gamma_b, beta_b, rows);
+#define PPO_LN_FWD2_V(V)                                              \
+  {                                                                   \
+    switch (warps_per_row(hidden, V)) {                               \
+      case 1: PPO_LN_FWD2_W(1, V) break;                              \
+      case 2: PPO_LN_FWD2_W(2, V) break;                              \
+      case 3: PPO_LN_FWD2_W(3, V) break;                              \
+      case 4: PPO_LN_FWD2_W(4, V) break;                              \
+      case 5: PPO_LN_FWD2_W(5, V) break;                              \
+      case 6: PPO_LN_FWD2_W(6, V) break;                              \
+      case 7: PPO_LN_FWD2_W(7, V) break;                              \
+      default: PPO_LN_FWD2_W(8, V) break;                             \
+    }                                                                 \
   }
-  if (need <= 1) PPO_WPASS_W(1, 1)
-  else if (need <= 2) PPO_WPASS_W(2, 1)
-  else if (need <= 4) PPO_WPASS_W(4, 1)
-  else if (need <= 8) PPO_WPASS_W(8, 1)
-  else if (need <= 16) PPO_WPASS_W(8, 2)
-  else PPO_WPASS_W(16, 2)
-#undef PPO_WPASS_W
-  PPO_LAUNCHED("wpass_recompute_kernel");
+  PPO_VPL_DISPATCH(vpl, PPO_LN_FWD2_V)
+#undef PPO_LN_FWD2_V
+#undef PPO_LN_FWD2_W
+  PPO_LAUNCHED("ln_fwd_kernel<dual>");
   return PPO_OK;
 }
 

@@ -539,9 +539,10 @@ class Stage:
         for i, l in enumerate(self.layers):
             x, o, h1, f = (slab.get(i, n) for n in ("x", "o", "h1", "f"))
             b = wbuf[i]
-            # LN1, LN2 and GeLU recompute in one launch (12 s*h*2 bytes)
-            self._k("wpass_recompute", 24 * s * h, native.wpass_recompute, x, h1, f, self.p(l, "ln1_g"),
-                    self.p(l, "ln1_b"), self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln1"], ws["ln"], ws["g"], eps)
+            # GeLU recompute, then LN1 and LN2 recompute in one launch (4E bytes)
+            self._k("gelu_fwd", 16 * s * h, native.gelu_fwd, f, ws["g"])
+            self._k("layernorm_fwd2", 8 * s * h, native.layernorm_fwd2, x, self.p(l, "ln1_g"), self.p(l, "ln1_b"),
+                    ws["ln1"], h1, self.p(l, "ln2_g"), self.p(l, "ln2_b"), ws["ln"], eps)
             self.wgrad(self.gp(l, "w_fc2"), b["dm"], ws["g"])
             self.wgrad(self.gp(l, "w_fc1"), b["df"], ws["ln"])
             self.wgrad(self.gp(l, "w_proj"), b["da"], o)

@@ -75,7 +75,7 @@ SIGNATURES = {
     "ppo_residual_dropout_ln_fwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _F32, _U64, _U64, _VP, _VP],
     "ppo_layernorm_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP, _F32, _U64, _U64, _VP, _VP, _VP,
                           _VP],
-    "ppo_wpass_recompute": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP],
+    "ppo_layernorm_fwd2": [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _F32, _VP],
     "ppo_dropout": [_VP, _VP, _I64, _F32, _U64, _U64, _VP, _VP],
     "ppo_gelu_fwd": [_VP, _VP, _I64, _VP],
     "ppo_gelu_bwd": [_VP, _VP, _VP, _VP, _I64, _VP],
@@ -226,12 +226,14 @@ def layernorm_bwd(x, gamma, dy, resid_grad, dx, dgamma, dbeta, drop_out=None, p=
     )
 
 
-def wpass_recompute(x, h1, f, ln1_g, ln1_b, ln2_g, ln2_b, ln1, ln2, g, eps=1e-5, stream=None):
-    """ln1 = LN1(x), ln2 = LN2(h1), g = gelu(f) in one launch (split-backward W pass)."""
-    _check_bf16(x, h1, f, ln1, ln2, g)
-    h = x.shape[-1]
-    call("ppo_wpass_recompute", _ptr(x), _ptr(h1), _ptr(f), _ptr(ln1_g), _ptr(ln1_b), _ptr(ln2_g), _ptr(ln2_b),
-         _ptr(ln1), _ptr(ln2), _ptr(g), x.numel() // h, h, eps, _stream(stream))
+def layernorm_fwd2(x_a, gamma_a, beta_a, y_a, x_b, gamma_b, beta_b, y_b, eps=1e-5, stream=None):
+    """Two LayerNorms of equal shape in one launch (W-pass LN1 + LN2 recompute)."""
+    _check_bf16(x_a, y_a, x_b, y_b)
+    h = x_a.shape[-1]
+    if x_b.shape != x_a.shape:
+        raise ValueError("layernorm_fwd2: both inputs must have one shape")
+    call("ppo_layernorm_fwd2", _ptr(x_a), _ptr(gamma_a), _ptr(beta_a), _ptr(y_a), _ptr(x_b), _ptr(gamma_b),
+         _ptr(beta_b), _ptr(y_b), x_a.numel() // h, h, eps, _stream(stream))
 
 
 def dropout(x, y, p, seed, offset, stream=None, offset_base=None):

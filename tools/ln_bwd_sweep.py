@@ -1,10 +1,11 @@
-"""LayerNorm-backward launch variants and the fused W-pass recompute, timed at the
+"""LayerNorm-backward launch variants and the dual LayerNorm, timed at the
 bench shapes (C2 4096x2048, C3 8192x4096, C4 16384x5120).
 
 Each variant (PPO_LN_BWD=<id>, read once per process by the library) runs in its own
 subprocess; one JSON line per (variant, shape, ln_out).  Timing: CUDA-graph replay of
 16 launches over 4 rotating input sets (> L2), CUDA events on the replay stream.
-usage: python tools/ln_bwd_sweep.py [--variants 0,1,2,3,4] > profiles/r2_ln_bwd_variants.jsonl
+usage: python tools/ln_bwd_sweep.py [--variants 0,1] > profiles/r2_ln_bwd_variants.jsonl
+(variant 0: next-row prefetch, the default; 1: none)
 """
 import argparse
 import json
@@ -67,18 +68,11 @@ def worker(variant):
             print(json.dumps({"kernel": "layernorm_bwd", "variant": variant, "s": s, "h": h, "ln_out": ln_out,
                               "us": round(us, 2), "gbs": round(nbytes / us / 1e3, 1),
                               "frac": round(nbytes / us / 1e3 / peak, 3)}), flush=True)
-        if variant == 0:  # variant-independent kernels once: W-pass fused recompute vs its parts
-            fsets = [{"f": torch.randn(s, 4 * h, **bf), "g": torch.empty(s, 4 * h, **bf)} for _ in range(4)]
-            fns = [lambda t=t, u=u: native.wpass_recompute(t["x"], t["r"], u["f"], gam, bet, gam, bet, t["ln"], t["dx"],
-                                                            u["g"]) for t, u in zip(sets, fsets)]
-            us = graph_us(fns, torch)
-            print(json.dumps({"kernel": "wpass_recompute", "s": s, "h": h, "us": round(us, 2),
-                              "gbs": round(12 * E / us / 1e3, 1), "frac": round(12 * E / us / 1e3 / peak, 3)}), flush=True)
-            parts = [lambda t=t, u=u: (native.gelu_fwd(u["f"], u["g"]), native.layernorm_fwd(t["x"], gam, bet, t["ln"]),
-                                       native.layernorm_fwd(t["r"], gam, bet, t["dx"])) for t, u in zip(sets, fsets)]
-            us3 = graph_us(parts, torch) / 1.0
-            print(json.dumps({"kernel": "gelu_fwd+2x layernorm_fwd", "s": s, "h": h, "us": round(us3, 2),
-                              "gbs": round(12 * E / us3 / 1e3, 1), "frac": round(12 * E / us3 / 1e3 / peak, 3)}),
+        if variant == 0:  # variant-independent kernels once
+            dual = [lambda t=t: native.layernorm_fwd2(t["x"], gam, bet, t["ln"], t["r"], gam, bet, t["dx"]) for t in sets]
+            us2 = graph_us(dual, torch)
+            print(json.dumps({"kernel": "layernorm_fwd2 (LN1+LN2, one launch)", "s": s, "h": h, "us": round(us2, 2),
+                              "gbs": round(4 * E / us2 / 1e3, 1), "frac": round(4 * E / us2 / 1e3 / peak, 3)}),
                   flush=True)
             ln = [lambda t=t: native.layernorm_fwd(t["x"], gam, bet, t["ln"]) for t in sets]
             us1 = graph_us(ln, torch)
@@ -94,7 +88,7 @@ def worker(variant):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variants", default="0,1,2,3,4")
+    ap.add_argument("--variants", default="0,1")
     ap.add_argument("--worker", type=int, default=None)
     a = ap.parse_args()
     if a.worker is not None:
