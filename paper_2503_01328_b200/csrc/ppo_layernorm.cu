@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
     const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
     const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
     int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add,
-    const uint64_t* __restrict__ offset_base, int use_dropout, const float* __restrict__ gamma_b = nullptr,
-    const float* __restrict__ beta_b = nullptr, int64_t rows_a = 0) {
+    const uint64_t* __restrict__ offset_base, int use_dropout, const float* __restrict__ gamma_b,
+    const float* __restrict__ beta_b, int64_t rows_a) {
   static_assert(!(kDual && kResidual), "dual LayerNorm has no residual");
   pdl_wait();
   extern __shared__ __align__(16) float sm[];
@@ -407,7 +407,7 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
   if ((rc = row_launch(ln_fwd_kernel<false, W, V, fwd_groups_for(W)>, rows, hidden, W, 0, &l, fwd_groups_for(W)))) return rc; \
   launch_pdl(ln_fwd_kernel<false, W, V, fwd_groups_for(W)>, l.grid, l.block, l.smem, as_stream(stream),                                  \
       nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta, static_cast<__nv_bfloat16*>(y), rows, \
-      (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0);
+      (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0, nullptr, nullptr, (int64_t)0);
 #define PPO_LN_FWD_V(V)                                               \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \
@@ -444,7 +444,8 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   launch_pdl(ln_fwd_kernel<true, W, V, fwd_groups_for(W)>, l.grid, l.block, l.smem, as_stream(stream),                                  \
       static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),                   \
       static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps, \
-      dropout_threshold(p), 1.f / (1.f - p), seed, offset, offset_base, p > 0.f ? 1 : 0);
+      dropout_threshold(p), 1.f / (1.f - p), seed, offset, offset_base, p > 0.f ? 1 : 0, nullptr, nullptr,      \
+      (int64_t)0);
 #define PPO_RES_V(V)                                                  \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \
