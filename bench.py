@@ -364,6 +364,9 @@ def policy_report(res, sched, plan, m, seq, slab_bytes, rank):
     gbs = lambda ps: (len(ps) * moved / float(sum(p.duration for p in ps)) / 1e9) if ps else None  # noqa: E731
     comp = [p for p in res.trace.compute_passes()]
     busy = float(sum(p.duration for p in comp))
+    per_kind = {}
+    for p in comp:
+        per_kind.setdefault(str(p.kind), []).append(float(p.duration))
     return {
         "tokens_per_s": m * seq / it,
         "e2e_tokens_per_s": m * seq / wall,
@@ -385,6 +388,9 @@ def policy_report(res, sched, plan, m, seq, slab_bytes, rank):
         "compute_busy_frac": busy / float(res.trace.makespan) if res.trace.makespan else None,
         "host_issue_ms": 1e3 * statistics.median(res.host_issue_seconds) if res.host_issue_seconds else None,
         "witness_peak_units": prog.witness_peak_units,
+        # mean measured pass duration per kind (ms) and passes per iteration
+        "pass_ms": {k: round(1e3 * statistics.mean(v), 4) for k, v in sorted(per_kind.items())},
+        "passes": {k: len(v) for k, v in sorted(per_kind.items())},
     }
 
 
@@ -596,8 +602,11 @@ def run_b200(args, rank, world, local_rank):
             return none["tokens_per_s"] / rep["tokens_per_s"] - 1
 
         try:
+            from paper_2503_01328_b200.policy import DmaSlowdown as _Dma
+
             mc = choose_offload_measured(sv, st_sel, 2 * w1_, measure, tolerance=0.05, focus_rank=0, stream_mode="dual",
-                                         planner=lambda sc, st_, t, pairs: plan_slots_duplex(sc, st_, t / 2, pairs=pairs))
+                                         planner=lambda sc, st_, t, pairs: plan_slots_duplex(sc, st_, t / 2, pairs=pairs),
+                                         dma=_Dma.from_calibration(cal, split=True), dma_slack=0.03)
             gish_trials = [{"stride": q, "modelled_pct": round(100 * a, 2), "measured_pct": round(100 * b, 2)}
                            for q, a, b in mc.trials]
             if mc.choice is not None:
@@ -656,6 +665,41 @@ def run_b200(args, rank, world, local_rank):
 
     def pct(r):
         return 100 * (none["tokens_per_s"] / r["tokens_per_s"] - 1) if r else None
+
+    # ---- runner model vs device: modelled overhead of every offload plan (reference model
+    # alone, and with the measured DMA slowdown of calibrate.dma_slowdown) next to the
+    # measured one, each against the same schedule without offload
+    from paper_2503_01328_b200.policy import DmaSlowdown, modelled_overheads
+
+    dma_check = []
+    try:
+        checks = [("1f1b_full_single_stream", "full_single", sched, plans["full"], "single", "none"),
+                  ("1f1b_full_duplex_plan", "full_duplex", sched, plans["full_duplex"], "dual", "none")]
+        checks += [(f"1f1b_partial{i}", f"partial{i}", sched, c.plan, c.stream_mode, "none") for i, c in enumerate(partial)]
+        for name in sched_variants:
+            if name in variant_kw and variant_kw[name][1] is not None:
+                sv, pv, kw = variant_kw[name]
+                checks.append((name, name, sv, pv, kw["stream_mode"], f"{sv.kind}_v{sv.local_stages}_none"))
+        base_cache = {}
+        for label, rk, sv, pv, sm, base_key in checks:
+            if rk not in results or base_key not in results or pv is None:
+                continue
+            split = sv.split_backward
+            dma = DmaSlowdown.from_calibration(cal, split=split)
+            key = (id(sv), sm)
+            if key not in base_cache:
+                from paper_2503_01328_b200.sim import simulate as _sim
+
+                base_cache[key] = _sim(sv, stream_mode=sm)
+            mo = modelled_overheads(sv, pv, 0, dma, sm, base=base_cache[key])
+            measured = 100 * (results[base_key]["tokens_per_s"] / results[rk]["tokens_per_s"] - 1)
+            entry = {"policy": label, "measured_pct": round(measured, 2), "modelled_pct": round(100 * mo["model"], 2),
+                     "modelled_dma_pct": round(100 * mo["model_dma"], 2),
+                     "dma_error_pts": round(100 * mo["model_dma"] - measured, 2)}
+            results[rk].update(modelled_pct=entry["modelled_pct"], modelled_dma_pct=entry["modelled_dma_pct"])
+            dma_check.append(entry)
+    except Exception as e:  # noqa: BLE001
+        errors["dma_model_check"] = f"{type(e).__name__}: {e}"[:500]
 
     # ---- roofline of the dominant kernel of the hot path (HBM-bound recompute)
     hbm_peak, peak_kind, _ = measured_peaks()
@@ -734,6 +778,8 @@ def run_b200(args, rank, world, local_rank):
         "offload": {
             "k_measured": k_measured,
             "T_F_ms": cal["t_f"] * 1e3, "T_B_ms": cal["t_b"] * 1e3, "T_o_ms": float(t_o) * 1e3,
+            "T_B_split_ms": cal["t_b_split"] * 1e3, "T_W_split_ms": cal["t_w_split"] * 1e3,
+            "dma_slowdown": cal.get("dma_slowdown"),
             "slab_bytes": slab_bytes,
             "no_offload": none, "no_offload_auto_gemms": results["none"], "no_offload_cublas_gemms": none_cublas,
             "no_offload_tcgen05_attention_fwd": results.get("none_tcgen05_attn"),
@@ -748,6 +794,7 @@ def run_b200(args, rank, world, local_rank):
             "partial_candidates": [results[f"partial{i}"] for i in range(len(partial)) if f"partial{i}" in results],
             "schedules": {k: results[k] for k in sched_variants if k in results},
             "gis-h_closed_loop_trials": gish_trials,
+            "dma_model_check": dma_check,
             "memory_method": ("peak_act_gb = torch allocator peak over the run minus the persistent training "
                               "state (bf16 weights, fp32 grads and masters): slab arenas, W-pass buffers, "
                               "workspaces, boundary rings, graph pools, library temporaries (PAPER.md:265 "

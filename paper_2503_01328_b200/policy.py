@@ -26,8 +26,84 @@ from dataclasses import dataclass
 from fractions import Fraction
 
 from .offload import OffloadPlan, plan_slots
-from .schedule_types import Schedule
+from .schedule_types import PassKind, Schedule
 from .sim import peak_memory, simulate
+
+
+@dataclass(frozen=True)
+class DmaSlowdown:
+    """Measured compute slowdown while the copy engines stream (``runtime.calibrate
+    .dma_slowdown``): fractional extra time of F, B and W passes with D2H alone, H2D
+    alone or both directions in flight.  The reference runner model prices link
+    contention only (sim.py:274-304); copy-engine reads of HBM also cost the SMs DRAM
+    bandwidth (profiles/r1_dma_interference.txt), so a plan the model schedules "for
+    free" still slows the compute it overlaps."""
+
+    f: tuple = (0.0, 0.0, 0.0)  # (d2h, h2d, duplex)
+    b: tuple = (0.0, 0.0, 0.0)
+    w: tuple = (0.0, 0.0, 0.0)
+
+    @classmethod
+    def from_calibration(cls, cal: dict, split: bool = False) -> "DmaSlowdown":
+        d = cal["dma_slowdown"]
+        pick = lambda k: tuple(max(0.0, float(d[k][m])) for m in ("d2h", "h2d", "duplex"))  # noqa: E731
+        if split:
+            return cls(pick("F"), pick("Bs"), pick("W"))
+        return cls(pick("F"), pick("B"), pick("B"))
+
+    def of(self, kind) -> tuple:
+        return {PassKind.F: self.f, PassKind.B: self.b, PassKind.W: self.w}[kind]
+
+
+def _overlaps(a: float, b: float, transfers) -> tuple[float, float, float]:
+    """Seconds of [a, b) with D2H only, H2D only and both directions in flight."""
+    cuts = {a, b}
+    for s, e, _ in transfers:
+        if e > a and s < b:
+            cuts.update(x for x in (s, e) if a < x < b)
+    cuts = sorted(cuts)
+    d_only = h_only = both = 0.0
+    for lo, hi in zip(cuts, cuts[1:]):
+        mid = 0.5 * (lo + hi)
+        d = any(s <= mid < e for s, e, k in transfers if k == PassKind.OFFLOAD)
+        h = any(s <= mid < e for s, e, k in transfers if k == PassKind.RELOAD)
+        if d and h:
+            both += hi - lo
+        elif d:
+            d_only += hi - lo
+        elif h:
+            h_only += hi - lo
+    return d_only, h_only, both
+
+
+def dma_adjusted_end(trace, device: int, dma: DmaSlowdown | None) -> float:
+    """End of ``device``'s last compute pass with every pass stretched by the measured
+    slowdown for the copy traffic it overlaps (first order: a device that computes
+    back to back is delayed by the sum of its passes' stretches)."""
+    comp = [p for p in trace.compute_passes() if p.device == device]
+    if not comp:
+        return 0.0
+    end = float(max(p.end for p in comp))
+    if dma is None:
+        return end
+    xfer = [(float(p.start), float(p.end), p.kind) for p in trace.transfer_passes() if p.device == device]
+    extra = 0.0
+    for p in comp:
+        sd, sh, sx = dma.of(p.kind)
+        od, oh, ox = _overlaps(float(p.start), float(p.end), xfer)
+        extra += od * sd + oh * sh + ox * sx
+    return end + extra
+
+
+def modelled_overheads(sched: Schedule, plan, device: int, dma: DmaSlowdown | None = None,
+                       stream_mode: str = "single", base=None) -> dict:
+    """Modelled overhead of ``plan`` at ``device`` versus no offload: the reference runner
+    model alone, and with the measured DMA slowdown (``dma_adjusted_end``)."""
+    base = base or simulate(sched, stream_mode=stream_mode)
+    tr = simulate(sched, plan, stream_mode=stream_mode)
+    b = dma_adjusted_end(base, device, None)
+    return {"model": dma_adjusted_end(tr, device, None) / b - 1,
+            "model_dma": dma_adjusted_end(tr, device, dma) / b - 1 if dma is not None else None}
 
 
 @dataclass(frozen=True)
@@ -57,7 +133,10 @@ def choose_offload(
     focus_rank: int | None = None,
     stream_mode: str = "single",
     max_stride: int | None = None,
+    dma: DmaSlowdown | None = None,
 ) -> PolicyChoice:
+    """Least-peak stride plan within ``tolerance`` of no offload.  With ``dma`` (and a
+    ``focus_rank``) the overhead is the DMA-aware one of ``modelled_overheads``."""
     base = simulate(sched, stream_mode=stream_mode)
     base_peaks = _peaks(base)
     best = PolicyChoice(None, None, base.makespan, base.makespan, base_peaks, base_peaks, 0)
@@ -74,6 +153,10 @@ def choose_offload(
         tr = simulate(sched, plan, stream_mode=stream_mode)
         if tr.makespan > limit:
             continue
+        if dma is not None and focus_rank is not None:
+            over = dma_adjusted_end(tr, focus_rank, dma) / dma_adjusted_end(base, focus_rank, None) - 1
+            if over > tolerance:
+                continue
         peaks = _peaks(tr)
         if score(peaks) < score(best.peak_units):
             best = PolicyChoice(plan, q, tr.makespan, base.makespan, peaks, base_peaks, len(plan.offloaded_pairs()))
@@ -118,7 +201,8 @@ class MeasuredChoice:
 def choose_offload_measured(sched: Schedule, stages, t_o: Fraction, measure, tolerance: float = 0.05,
                             focus_rank: int | None = None, stream_mode: str = "single",
                             max_stride: int | None = None, max_trials: int = 4,
-                            model_tolerance: float = 0.25, planner=None) -> MeasuredChoice:
+                            model_tolerance: float = 0.25, planner=None,
+                            dma: DmaSlowdown | None = None, dma_slack: float = 0.02) -> MeasuredChoice:
     """Least-memory stride plan whose *measured* overhead is within ``tolerance``.
 
     ``measure(plan) -> float`` runs the plan on the device and returns its overhead
@@ -127,9 +211,17 @@ def choose_offload_measured(sched: Schedule, stages, t_o: Fraction, measure, tol
     is never run.  After each miss the unmodelled cost is taken as proportional to the
     traffic (measured-minus-modelled overhead per offloaded pair, the smallest seen so
     far), and candidates predicted above ``tolerance`` by it are skipped: the device
-    pays for concurrent DMA even where the model schedules the copies for free."""
+    pays for concurrent DMA even where the model schedules the copies for free.  With
+    ``dma`` (measured slowdowns) candidates whose DMA-aware modelled overhead exceeds
+    ``tolerance + dma_slack`` are not run at all."""
     cands = [c for c in offload_candidates_by_memory(sched, stages, t_o, focus_rank, stream_mode, max_stride, planner)
              if c.overhead <= model_tolerance]
+    if dma is not None and focus_rank is not None:
+        base = simulate(sched, stream_mode=stream_mode)
+        b_end = dma_adjusted_end(base, focus_rank, None)
+        cands = [c for c in cands
+                 if dma_adjusted_end(simulate(sched, c.plan, stream_mode=stream_mode), focus_rank, dma) / b_end - 1
+                 <= tolerance + dma_slack]
     trials = []
     per_pair = None  # unmodelled overhead per offloaded pair
     for c in cands:
@@ -175,6 +267,7 @@ def choose_partial_offload(
     tolerance: float = 0.05,
     stream_modes=("single", "dual"),
     max_stride: int = 4,
+    dma: DmaSlowdown | None = None,
 ) -> list[PartialChoice]:
     """Per-tensor partial offload (B200 extension).
 
@@ -215,8 +308,12 @@ def choose_partial_offload(
                 tr = simulate(sched, plan, stream_mode=mode)
                 if tr.makespan > limit:
                     continue
+                over = float(tr.makespan / base.makespan - 1)
+                if dma is not None:  # the DMA-aware overhead at ``rank`` must fit too
+                    over = max(over, dma_adjusted_end(tr, rank, dma) / dma_adjusted_end(base, rank, None) - 1)
+                    if over > tolerance:
+                        continue
                 off_peak = tr.memory.peak(rank) // units
-                out.append(PartialChoice(label, tensors, off_b, res_b, plan, mode, q,
-                                         float(tr.makespan / base.makespan - 1), off_peak, res_peak))
+                out.append(PartialChoice(label, tensors, off_b, res_b, plan, mode, q, over, off_peak, res_peak))
     out.sort(key=lambda c: (c.act_bytes, c.overhead))
     return out

@@ -106,15 +106,65 @@ def calibrate(stage, reps: int = 3, split: bool = True) -> dict:
         torch.cuda.synchronize()
         if r:
             dup.append(max(ea[0].elapsed_time(ea[1]), eb[0].elapsed_time(eb[1])) / 1e3)
+    # compute slowdown under concurrent copy-engine traffic, per pass kind and direction
+    # (copy-engine reads of HBM cost the SMs DRAM bandwidth: profiles/r1_dma_interference.txt);
+    # the runner model prices link contention only (reference sim.py:274-304), policy.DmaSlowdown
+    # adds this measured term
+    slow = dma_slowdown(stage, slab, tok, out, dy, segs, segs2, copy, copy2, split=split)
     pool2.close()
     pool.close()
     nbytes = sum(lay.bin_used)
     return {
+        "dma_slowdown": slow,
         "t_f": min(tf), "t_b": min(tb), "t_d2h": min(d2h), "t_h2d": min(h2d), "transfer_bytes": nbytes,
         "t_b_split": min(tbs), "t_w_split": min(tws),
         "t_duplex": statistics.median(dup), "duplex_gbs_per_direction": nbytes / statistics.median(dup) / 1e9,
         "d2h_gbs": nbytes / min(d2h) / 1e9, "h2d_gbs": nbytes / min(h2d) / 1e9,
     }
+
+
+def dma_slowdown(stage, slab, tok, out, dy, segs, segs2, copy, copy2, split: bool = True, reps: int = 3,
+                 passes: int = 4) -> dict:
+    """Fractional slowdown of F, B (and split B / W) passes while D2H, H2D or both copy
+    directions stream on the copy engines: t(with copies) / t(alone) - 1.  Each sample
+    runs ``passes`` passes back to back under a chain of slab transfers long enough to
+    cover them (eager issue, as ``calibrate`` times F and B); medians of ``reps``."""
+    wbuf = stage.new_wbuffer() if split else None
+    d2h, h2d = (segs, copy, native.PPO_D2H), (segs2, copy2, native.PPO_H2D)
+
+    def run(kind):
+        stage.set_pass_context(0, 0, tok)
+        if kind == "F":
+            stage.forward_body(slab, None if stage.last else out)
+        elif kind == "B":
+            stage.backward_body(slab, None if stage.last else dy, None if stage.first else out)
+        elif kind == "Bs":
+            stage.backward_body(slab, None if stage.last else dy, None if stage.first else out, wbuf)
+        else:
+            stage.wgrad_body(slab, wbuf)
+
+    def sample(kind, copies):
+        comp = torch.cuda.current_stream()
+        torch.cuda.synchronize()
+        for _ in range(2 if copies else 0):
+            for seg_list, stream, direction in copies:
+                native.transfer(direction, seg_list, stream.cuda_stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(comp)
+        for _ in range(passes):
+            run(kind)
+        b.record(comp)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / passes
+
+    out_ = {}
+    for kind in ["F", "B"] + (["Bs", "W"] if split else []):
+        run(kind)  # warm
+        t = {mode: statistics.median(sample(kind, copies) for _ in range(reps))
+             for mode, copies in (("none", ()), ("d2h", (d2h,)), ("h2d", (h2d,)), ("duplex", (d2h, h2d)))}
+        out_[kind] = {m: t[m] / t["none"] - 1 for m in ("d2h", "h2d", "duplex")}
+        out_[kind]["t_alone"] = t["none"]
+    return out_
 
 
 def calibrate_costs(cfg, n_stages: int, microbatches: int, device, units: int = 1, split: bool = False):

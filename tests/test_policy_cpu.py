@@ -62,3 +62,52 @@ def test_measured_choice_without_gap_equals_model_choice():
     assert (got.choice is None) == (want.plan is None)
     if want.plan is not None:
         assert got.choice.peak_units[0] == want.peak_units[0]
+
+
+def test_dma_overlap_accounting():
+    """policy._overlaps splits a pass into D2H-only / H2D-only / both seconds."""
+    from paper_2503_01328_b200.policy import _overlaps
+    from paper_2503_01328_b200.schedule_types import PassKind
+
+    x = [(0.0, 4.0, PassKind.OFFLOAD), (2.0, 6.0, PassKind.RELOAD)]
+    assert _overlaps(1.0, 5.0, x) == (1.0, 1.0, 2.0)
+    assert _overlaps(6.0, 7.0, x) == (0.0, 0.0, 0.0)
+
+
+def test_dma_adjusted_overhead_monotone():
+    """Zero slowdown reproduces the runner model; a positive slowdown stretches exactly
+    the compute that overlaps copies, and never makes a plan look cheaper."""
+    from fractions import Fraction
+
+    import paper_2503_01328_b200 as po
+    from paper_2503_01328_b200.policy import DmaSlowdown, dma_adjusted_end, modelled_overheads
+
+    U = po.PassCosts.unit()
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    tr = po.simulate(sched, plan)
+    end = float(max(p.end for p in tr.compute_passes() if p.device == 0))
+    assert dma_adjusted_end(tr, 0, None) == end
+    assert dma_adjusted_end(tr, 0, DmaSlowdown()) == end
+    slow = DmaSlowdown(f=(0.1, 0.1, 0.2), b=(0.3, 0.1, 0.4), w=(0.3, 0.1, 0.4))
+    assert dma_adjusted_end(tr, 0, slow) > end
+    m = modelled_overheads(sched, plan, 0, slow)
+    assert m["model_dma"] > m["model"] >= 0
+    # no transfers on the last rank (its window is zero): no stretch there
+    tr3 = [p for p in tr.transfer_passes() if p.device == 3]
+    assert not tr3 and dma_adjusted_end(tr, 3, slow) == dma_adjusted_end(tr, 3, None)
+
+
+def test_choose_offload_respects_dma_model():
+    """With a large measured slowdown the DMA-aware planner keeps fewer pairs (or none)."""
+    from fractions import Fraction
+
+    import paper_2503_01328_b200 as po
+    from paper_2503_01328_b200.policy import DmaSlowdown, choose_offload
+
+    U = po.PassCosts.unit()
+    sched = po.build_1f1b(8, 1, 16, U)
+    plain = choose_offload(sched, (0,), Fraction(3, 2), tolerance=0.05, focus_rank=0)
+    heavy = choose_offload(sched, (0,), Fraction(3, 2), tolerance=0.05, focus_rank=0,
+                           dma=DmaSlowdown(f=(0.5, 0.5, 0.9), b=(0.5, 0.5, 0.9), w=(0.5, 0.5, 0.9)))
+    assert plain.plan is not None
+    assert heavy.offloaded_pairs <= plain.offloaded_pairs
