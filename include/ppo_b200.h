@@ -99,6 +99,17 @@ int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_s
  * Replaces the reference runner's clock bookkeeping of pass start/end (sim.py:334-353). */
 int ppo_timestamp(uint64_t* slot, void* stream);
 
+/* Cross-rank transfer ordering (topology-synchronised plans, reference offload.py:223-248,
+ * honoured by sim.py:186-189): a sync edge is a 32-bit flag.  The producing copy stream
+ * writes `value` after its transfer (cuStreamWriteValue32); the consuming copy stream
+ * waits until *addr == value (cuStreamWaitValue32) -- stream-ordered, no host thread, no
+ * SM.  `addr` is device memory or host memory mapped with ppo_host_register (flags shared
+ * by rank processes through POSIX shared memory). */
+int ppo_stream_write_u32(void* stream, void* addr, uint32_t value);
+int ppo_stream_wait_u32(void* stream, void* addr, uint32_t value);
+int ppo_host_register(void* ptr, uint64_t bytes, void** dev_ptr);
+int ppo_host_unregister(void* ptr);
+
 /* ------------------------------------------------------------ K1: pack / gather */
 /* Gather `n` 2-D byte ranges into one destination: item i copies `rows[i]` rows of
  * `row_bytes[i]` from src[i] (row pitch `src_pitch[i]`, 0 = dense) to

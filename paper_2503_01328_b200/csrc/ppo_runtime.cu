@@ -4,6 +4,7 @@
 // (pkg/src/ppoff/costs.py:99-105), the single-stream transfer slots
 // (offload.py:133-220), host bins (offload.py:305-340) and residency
 // (sim.py:462-487).  Here they are real copies on a dedicated copy stream.
+#include <cuda.h>  // driver-API types only: entry points come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 
 #include <sys/mman.h>
@@ -14,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "ppo_common.cuh"
@@ -333,6 +335,66 @@ int ppo_transfer(int direction, const ppo_segment* segs, int nsegs, void* copy_s
     PPO_TRY_CUDA(cudaMemcpyAsync(dst, src, segs[i].bytes, kind, s));
   }
   if (done_event) PPO_TRY_CUDA(cudaEventRecord(as_event(done_event), s));
+  return PPO_OK;
+}
+
+// ------------------------------------------- cross-rank transfer ordering (sync edges)
+// Topology-synchronised plans (reference offload.py:223-248; honoured by sim.py:186-189)
+// order transfers of two devices that share a PCIe switch.  On the GPU an edge is a
+// 32-bit flag: the producer's copy stream writes 1 after its transfer, the consumer's
+// copy stream waits for 1 (cuStreamWaitValue32, no host involvement, no SM) and resets
+// it to 0.  Flags live in device memory (ranks in one process) or in host memory shared
+// by the rank processes and mapped into each GPU's address space.
+using WriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static int driver_fn(const char* name, void** fn) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn)
+    return set_error(PPO_ENOTSUP, "driver entry point %s unavailable", name);
+  return PPO_OK;
+}
+
+int ppo_stream_write_u32(void* stream, void* addr, uint32_t value) {
+  static WriteValue32 fn = nullptr;
+  if (!addr) return set_error(PPO_EINVAL, "ppo_stream_write_u32: null address");
+  if (!fn) {
+    void* p = nullptr;
+    if (int rc = driver_fn("cuStreamWriteValue32", &p)) return rc;
+    fn = reinterpret_cast<WriteValue32>(p);
+  }
+  CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value, 0);
+  if (r != CUDA_SUCCESS) return set_error(PPO_ENOTSUP + 0, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return PPO_OK;
+}
+
+int ppo_stream_wait_u32(void* stream, void* addr, uint32_t value) {
+  static WaitValue32 fn = nullptr;
+  if (!addr) return set_error(PPO_EINVAL, "ppo_stream_wait_u32: null address");
+  if (!fn) {
+    void* p = nullptr;
+    if (int rc = driver_fn("cuStreamWaitValue32", &p)) return rc;
+    fn = reinterpret_cast<WaitValue32>(p);
+  }
+  CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                  CU_STREAM_WAIT_VALUE_EQ);
+  if (r != CUDA_SUCCESS) return set_error(PPO_ENOTSUP, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return PPO_OK;
+}
+
+int ppo_host_register(void* ptr, uint64_t bytes, void** dev_ptr) {
+  if (!ptr || !bytes || !dev_ptr) return set_error(PPO_EINVAL, "ppo_host_register: bad arguments");
+  PPO_TRY_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+  PPO_TRY_CUDA(cudaHostGetDevicePointer(dev_ptr, ptr, 0));
+  return PPO_OK;
+}
+
+int ppo_host_unregister(void* ptr) {
+  if (!ptr) return PPO_OK;
+  PPO_TRY_CUDA(cudaHostUnregister(ptr));
   return PPO_OK;
 }
 

@@ -224,6 +224,57 @@ class NcclLoopbackTransport:
         self.comm.close()
 
 
+class FlagBoard:
+    """The 32-bit flags of a topology-synchronised plan's cross-rank sync edges
+    (``lower``: Op.flag_waits / Op.signals; reference offload.py:223-248).
+
+    One process (virtual ranks): device memory.  Rank processes: one POSIX shared-memory
+    page created by rank 0, attached by every rank and mapped into each GPU
+    (``native.host_register``), so a copy stream on one GPU can wait for a flag another
+    GPU's copy stream writes -- no host thread in the loop."""
+
+    def __init__(self, n: int, device, dist_mode: bool):
+        self.n = n
+        self.shm = None
+        self.tensor = None
+        self.host_ptr = None
+        if not dist_mode:
+            self.tensor = torch.zeros(max(1, n), dtype=torch.int32, device=device)
+            self.base = self.tensor.data_ptr()
+            return
+        import ctypes
+        import uuid
+        from multiprocessing import shared_memory
+
+        dist = _dist()
+        box = [f"ppo_flags_{uuid.uuid4().hex[:16]}" if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        size = max(4096, (4 * n + 4095) // 4096 * 4096)
+        if dist.get_rank() == 0:
+            self.shm = shared_memory.SharedMemory(name=box[0], create=True, size=size)
+            self.shm.buf[:size] = bytes(size)
+        dist.barrier()
+        if dist.get_rank() != 0:
+            self.shm = shared_memory.SharedMemory(name=box[0], create=False)
+        self.owner = dist.get_rank() == 0
+        self.host_ptr = ctypes.addressof(ctypes.c_char.from_buffer(self.shm.buf))
+        with torch.cuda.device(device):
+            self.base = native.host_register(self.host_ptr, size)
+        dist.barrier()
+
+    def addr(self, idx: int) -> int:
+        return self.base + 4 * idx
+
+    def close(self):
+        if self.shm is not None:
+            native.host_unregister(self.host_ptr)
+            self.host_ptr = None
+            self.shm.close()
+            if self.owner:
+                self.shm.unlink()
+            self.shm = None
+
+
 _NCCL_TRANSPORTS = {}
 
 
@@ -285,6 +336,7 @@ class RankRunner:
         self.device = torch.device(device)
         self.rank = program.rank
         self.transport = transport
+        self.flags = None  # FlagBoard of a topology-synchronised plan (set by execute)
         # consecutive stages on this device (d=1 with v>1): boundary messages stay local
         self.local = LocalTransport()
         self.emulate = emulate
@@ -594,9 +646,14 @@ class RankRunner:
         slab_ptr = self.arena.data_ptr() + op.slab * self.off_bytes
         segs = lay.segments(slab_ptr, self.host_bins(op.host_slot, s))
         tag = "D2H" if op.kind == "OFFLOAD" else "H2D"
+        for f in op.flag_waits:  # cross-rank sync edge: the paired device's transfer is done
+            native.stream_wait_u32(stream, self.flags.addr(f), 1)
+            native.stream_write_u32(stream, self.flags.addr(f), 0)
         self.rec((tag + "_start", s, j), stream)
         native.transfer(native.PPO_D2H if op.kind == "OFFLOAD" else native.PPO_H2D, segs, stream.cuda_stream)
         self.rec((tag, s, j), stream)
+        for f in op.signals:
+            native.stream_write_u32(stream, self.flags.addr(f), 1)
 
     def end_iteration(self, timed: bool = True):
         comp = self.streams["compute"]
@@ -693,6 +750,11 @@ class RankRunner:
         if isinstance(self.transport, NcclLoopbackTransport):
             self.transport.close()
             self.transport = None
+        owned = getattr(self, "owned_flags", None)
+        if owned is not None:
+            torch.cuda.synchronize(self.device)
+            owned.close()
+            self.owned_flags = None
 
 
 def host_memory_available() -> int:
@@ -991,6 +1053,13 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
                           use_graphs=use_graphs, gemm=gemm, offload_tensors=offload_tensors, attn=attn) for r in ranks]
     if mode == "nccl_loopback":
         transport.runner = runners[0]
+    n_flags = max(p.n_flags for p in programs.values())
+    flags = None
+    if n_flags and any(op.flag_waits or op.signals for p in programs.values() for op in p.ops) or \
+            (n_flags and dist_mode):  # every rank joins the board's set-up collectives
+        flags = FlagBoard(n_flags, dev, dist_mode)
+        for r in runners:
+            r.flags = flags
     if tokens is None:
         gen = torch.Generator().manual_seed(0)
         tokens = torch.randint(0, model.vocab, (m, model.seq + 1), generator=gen)
@@ -1065,6 +1134,8 @@ def execute(sched: Schedule, plan: OffloadPlan | None = None, *, model: ModelCon
     passes = [p for r in runners for p in r.measured_passes()] if (pass_timing or not whole) else []
     slab_bytes = max(r.slab_bytes for r in runners)
     trace = measured_trace(sched, passes, units_bytes=slab_bytes // sched.units_per_stage)
+    if flags is not None:
+        runners[0].owned_flags = flags
     return RunResult(trace, secs, losses, programs, runners, slab_bytes,
                      {r.rank: r.prog.n_slabs for r in runners}, {r.rank: r.prog.n_host_slots for r in runners},
                      walls, host_secs, {r.rank: r.act_bytes for r in runners},

@@ -62,6 +62,10 @@ class Op:
     anchor: tuple | None = None  # reload anchor event
     send_ring: int | None = None  # ring slot of the boundary send this compute op feeds
     wbuf: int | None = None  # split backward: gradient buffer shared by a B and its W
+    # topology-synchronised plans (OffloadPlan.sync_edges): flags this transfer waits for
+    # before it starts / raises when it is done (index into the plan's sync_edges)
+    flag_waits: list = field(default_factory=list)
+    signals: list = field(default_factory=list)
 
     @property
     def key(self):
@@ -84,6 +88,7 @@ class Program:
     copy_order: dict  # stream -> [(kind, stage, mb)]
     recv_orders: dict  # channel -> [(stage, mb)]
     send_orders: dict
+    n_flags: int = 0  # len(plan.sync_edges): the flag board every rank of the run shares
 
     def ops_on(self, stream: str):
         return [op for op in self.ops if op.stream == stream]
@@ -323,6 +328,32 @@ def lower(
             compute_ops.append(op)
     ops.extend(compute_ops)
 
+    # ------------------------------------------------------ sync edges / pinned
+    # A topology-synchronised plan (offload.py:223-248) orders transfers of paired
+    # devices: edge (a -> b) makes transfer b wait for the end of transfer a
+    # (sim.py:186-189).  Same-rank edges are event waits; cross-rank edges are flags
+    # (executor FlagBoard); with emulated neighbours the cross-rank ones are dropped.
+    # A pinned plan also floors every transfer at its slot start (sim.py:184-185).
+    flag_wait_of: dict = {}
+    signal_of: dict = {}
+    local_after: dict = {}
+    if plan is not None and plan.sync_edges:
+        by_slot = {(t.device, t.slot): t for stm in plan.streams for t in stm.transfers}
+        tag = lambda t: ("OFFLOAD" if t.direction == OFF else "RELOAD", t.stage, t.microbatch)  # noqa: E731
+        for idx, (a, b) in enumerate(plan.sync_edges):
+            ta, tb = by_slot.get(a), by_slot.get(b)
+            if ta is None or tb is None:
+                continue
+            if ta.device == rank and tb.device == rank:
+                local_after.setdefault(tag(tb), []).append(tag(ta))
+            elif emulate_neighbors:
+                continue
+            elif ta.device == rank:
+                signal_of.setdefault(tag(ta), []).append(idx)
+            elif tb.device == rank:
+                flag_wait_of.setdefault(tag(tb), []).append(idx)
+    pinned = plan is not None and plan.pinned
+
     # ------------------------------------------------------------- transfers
     copy_order: dict = {}
     for p in transfers:
@@ -352,6 +383,17 @@ def lower(
                 op.anchor = ((f"{kind}_start" if which == "start" else f"{kind}_end"), as_, aj)
                 op.waits.append(op.anchor)
             op.records = [("H2D", s, j)]
+        if pinned and op.kind == "OFFLOAD":  # floor at the slot start: anchor like a reload
+            anc = _anchor_for(p.start, my_passes)
+            if anc is not None:
+                which, kind, as_, aj = anc
+                op.anchor = ((f"{kind}_start" if which == "start" else f"{kind}_end"), as_, aj)
+                if op.anchor != ("F_end", s, j):
+                    op.waits.append(op.anchor)
+        for k_, s_, j_ in local_after.get((op.kind, s, j), ()):
+            op.waits.append(("D2H" if k_ == "OFFLOAD" else "H2D", s_, j_))
+        op.flag_waits = list(flag_wait_of.get((op.kind, s, j), ()))
+        op.signals = list(signal_of.get((op.kind, s, j), ()))
         copy_order.setdefault(stream, []).append((op.kind, s, j))
         ops.append(op)
 
@@ -366,6 +408,7 @@ def lower(
         n_wbufs=n_wbufs,
         offloaded=offloaded, witness_makespan=trace.makespan, witness_peak_units=peak,
         compute_order=want, copy_order=copy_order, recv_orders=recv_orders, send_orders=send_orders,
+        n_flags=len(plan.sync_edges) if plan is not None else 0,
     )
 
 

@@ -60,6 +60,10 @@ SIGNATURES = {
     "ppo_abi_version": [],
     "ppo_last_error": [],
     "ppo_timestamp": [_VP, _VP],
+    "ppo_stream_write_u32": [_VP, _VP, ctypes.c_uint32],
+    "ppo_stream_wait_u32": [_VP, _VP, ctypes.c_uint32],
+    "ppo_host_register": [_VP, _U64, ctypes.POINTER(_VP)],
+    "ppo_host_unregister": [_VP],
     "ppo_gemm_set_swizzle": [_I32, _I64, _I64, _I64, _I32],
     "ppo_kernel_launches": [],
     "ppo_device_info": [_I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
@@ -377,6 +381,27 @@ GEMM_OPS = {"tn": 0, "tn_gelu": 1, "nn": 2, "nn_acc": 2, "nn_dgelu": 3, "wgrad":
 def gemm_set_swizzle(kind: str, M: int, N: int, K: int, swizzle: int) -> None:
     """Tile-scheduler swizzle for libppo_b200 GEMM ``kind`` at M x N x K (tuner hook)."""
     call("ppo_gemm_set_swizzle", GEMM_OPS[kind], M, N, K, swizzle)
+
+
+def stream_write_u32(stream, addr: int, value: int) -> None:
+    """Stream-ordered 32-bit store (cuStreamWriteValue32): signal a sync-edge flag."""
+    call("ppo_stream_write_u32", stream.cuda_stream, addr, value)
+
+
+def stream_wait_u32(stream, addr: int, value: int) -> None:
+    """Block ``stream`` until *addr == value (cuStreamWaitValue32): wait on a sync-edge flag."""
+    call("ppo_stream_wait_u32", stream.cuda_stream, addr, value)
+
+
+def host_register(ptr: int, nbytes: int) -> int:
+    """Pin and map host memory (e.g. POSIX shared memory) into the GPU; returns the device pointer."""
+    out = ctypes.c_void_p()
+    call("ppo_host_register", ptr, nbytes, ctypes.byref(out))
+    return int(out.value)
+
+
+def host_unregister(ptr: int) -> None:
+    call("ppo_host_unregister", ptr)
 
 
 def timestamp(slot_ptr: int, stream) -> None:

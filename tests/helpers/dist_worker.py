@@ -4,7 +4,8 @@ over gloo host copies (executor.HostTransport), everything else is the product
 path (lowered per-rank program, slab arena, pinned pool, copy streams, kernels).
 
 usage: torchrun --nproc-per-node D tests/helpers/dist_worker.py KIND OUT.json [GEMM ATTN]
-KIND: 1f1b (build_1f1b_full_offload(D, 8, unit, 3/2)) or 1f1b-i (v=2, selective n=1)
+KIND: 1f1b (build_1f1b_full_offload(D, 8, unit, 3/2)), 1f1b-i (v=2, selective n=1) or
+1f1b-i-sync (the same plan through apply_topology_sync: cross-rank sync-edge flags)
 GEMM/ATTN: backends (default tcgen05/tcgen05, pinned so the single-process comparison
 run uses the same kernels; "auto" exercises the collective decision table)
 """
@@ -31,6 +32,11 @@ def build(kind: str, d: int):
     U = po.PassCosts.unit()
     if kind == "1f1b":
         return po.build_1f1b_full_offload(d, 8, U, Fraction(3, 2))
+    if kind == "1f1b-i-sync":  # topology-synchronised plan: cross-process flags in shared memory
+        sched = po.build_interleaved_1f1b(d, 2, 8, U)
+        plan = po.plan_slots(sched, po.select_offload_stages(po.po_block(d, 2, U), 1), Fraction(1, 2) * U.total)
+        hw = po.HardwareSpec(compute_bandwidth=1.0, transfer_bandwidth=1.0, devices_per_switch=2)
+        return sched, po.apply_topology_sync(plan, hw)
     sched = po.build_interleaved_1f1b(d, 2, 8, U)
     stages = po.select_offload_stages(po.po_block(d, 2, U), 1)
     return sched, po.plan_slots(sched, stages, Fraction(1, 2) * U.total)

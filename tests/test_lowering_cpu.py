@@ -48,10 +48,20 @@ class CpuWalker:
     def done(self):
         return self.cursor >= len(self.prog.ops)
 
+    board = None  # sync-edge flags shared by all walkers of a run (set by run_all_ranks)
+    done_order = None  # global completion order of transfers: [(rank, kind, stage, mb)]
+
     def step(self):
         op = self.prog.ops[self.cursor]
         last = self.sched.num_stages - 1
         pair = (op.stage, op.mb)
+        if op.flag_waits:
+            if not all(self.board.get(f) for f in op.flag_waits):
+                raise Blocked()
+            for f in op.flag_waits:
+                self.board[f] = False
+        if op.kind in ("OFFLOAD", "RELOAD") and self.done_order is not None:
+            self.done_order.append((self.prog.rank, op.kind, op.stage, op.mb))
         if op.kind == "F":
             x = float(op.mb) if op.stage == 0 else self.rings["recv_act"][op.ring]
             if x is None:
@@ -106,6 +116,8 @@ class CpuWalker:
             self.rings["recv_act" if op.kind == "RECV_ACT" else "recv_grad"][op.ring] = val
         else:  # pragma: no cover
             raise ValueError(op.kind)
+        for f in op.signals:
+            self.board[f] = True
         self.cursor += 1
 
 
@@ -136,6 +148,9 @@ def run_all_ranks(sched, plan, stream_mode="single", spare_slabs=0):
     chans = LocalChannels()
     walkers = [CpuWalker(sched, lower(sched, plan, r, stream_mode=stream_mode, spare_slabs=spare_slabs), chans.bind(r))
                for r in range(sched.devices)]
+    board, order = {}, []
+    for w in walkers:
+        w.board, w.done_order = board, order
     while not all(w.done() for w in walkers):
         progressed = False
         for w in walkers:
@@ -289,3 +304,34 @@ def test_two_ranks_over_gloo():
         p.join(timeout=120)
     results = [q.get(timeout=5) for _ in range(2)]
     assert all(r == ("ok", True) for r in results), results
+
+
+@pytest.mark.parametrize("stream_mode", ["single", "dual"])
+def test_topology_synced_plans_lower_and_execute(stream_mode):
+    """apply_topology_sync plans (reference offload.py:223-248): cross-rank sync edges
+    become flags the consumer's copy stream waits on (executed here by the walker), the
+    pinned floors become anchors on every transfer; the run completes with correct
+    results and every edge's producer completes before its consumer starts."""
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    hw = po.HardwareSpec(compute_bandwidth=1.0, transfer_bandwidth=1.0, devices_per_switch=2)
+    synced = po.apply_topology_sync(plan, hw)
+    assert synced.sync_edges and synced.pinned
+    walkers = run_all_ranks(sched, synced, stream_mode)
+    for j in range(sched.microbatches):
+        assert walkers[0].grad_out[(0, j)] == expected_input_grad(sched, j)
+    progs = [w.prog for w in walkers]
+    assert all(p.n_flags == len(synced.sync_edges) for p in progs)
+    n_waits = sum(len(op.flag_waits) for p in progs for op in p.ops)
+    n_sig = sum(len(op.signals) for p in progs for op in p.ops)
+    assert n_waits == n_sig > 0
+    # every cross-rank edge: the producer transfer is done before the consumer runs
+    by_slot = {(t.device, t.slot): t for stm in synced.streams for t in stm.transfers}
+    pos = {x: i for i, x in enumerate(walkers[0].done_order)}
+    tag = lambda t: (t.device, "OFFLOAD" if t.direction == po.PassKind.OFFLOAD else "RELOAD", t.stage, t.microbatch)
+    for a, b in synced.sync_edges:
+        ta, tb = by_slot.get(a), by_slot.get(b)
+        if ta is not None and tb is not None and ta.device != tb.device:
+            assert pos[tag(ta)] < pos[tag(tb)]
+    # emulated neighbours drop the cross-rank edges
+    emu = lower(sched, synced, 0, emulate_neighbors=True)
+    assert not any(op.flag_waits or op.signals for op in emu.ops)

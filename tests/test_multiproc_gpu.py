@@ -42,7 +42,7 @@ def _torchrun(nproc, args, env=None, timeout=600):
     return subprocess.run(cmd, cwd=ROOT, env=e, capture_output=True, text=True, timeout=timeout)
 
 
-@pytest.mark.parametrize("kind", ["1f1b", "1f1b-i"])
+@pytest.mark.parametrize("kind", ["1f1b", "1f1b-i", "1f1b-i-sync"])
 def test_two_process_pipeline_matches_virtual(kind, tmp_path):
     out = tmp_path / "r.json"
     p = _torchrun(2, ["tests/helpers/dist_worker.py", kind, str(out)])

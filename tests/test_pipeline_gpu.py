@@ -163,6 +163,12 @@ def _variant(name):
     if name == "m_not_multiple_of_d":
         sched, plan = po.build_1f1b_full_offload(4, 6, U, Fraction(3, 2))
         return sched, plan, "single"
+    if name == "topology_synced":  # paired devices' transfers ordered by cross-rank flags, pinned floors
+        sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+        hw = po.HardwareSpec(compute_bandwidth=1.0, transfer_bandwidth=1.0, devices_per_switch=2)
+        plan = po.apply_topology_sync(plan, hw)
+        assert plan.sync_edges and plan.pinned
+        return sched, plan, "single"
     if name == "gis_g":
         sched = po.build_gis_g(4, 2, 8, 3, U)
         assert sched.kind == "gis-g"
@@ -172,7 +178,7 @@ def _variant(name):
 
 
 @pytest.mark.parametrize("name", ["late_reloads_k2", "dual_streams", "duplex_plan", "k_aware_stride",
-                                  "pp1_all_skipped", "m_not_multiple_of_d", "gis_g"])
+                                  "pp1_all_skipped", "m_not_multiple_of_d", "gis_g", "topology_synced"])
 def test_plan_variants_exact(name, oracle_result):
     """Every plan shape the planner can emit runs with bit-exact round trips, and the
     first step's loss is bit-identical to the same schedule without offload (the
@@ -238,5 +244,24 @@ def test_whole_iteration_graph(oracle_result, mode, stream_mode):
     assert len(got.trace.compute_passes()) == n_passes
     assert all(p.duration > 0 for p in got.trace.passes)
     assert 0 < got.iteration_seconds[-1] < 10
+    got.close()
+    ref.close()
+
+
+def test_topology_synced_plan_in_iteration_graph(oracle_result):
+    """Sync-edge flags (cuStreamWaitValue32 / WriteValue32 on the copy streams) inside
+    the one-graph-per-iteration replay: same losses as the host-issued run over 3 SGD
+    steps, bit-exact round trips, flags back to 0 after every iteration."""
+    tokens, _, _ = oracle_result
+    sched, plan, _m = _variant("topology_synced")
+    kw = dict(model=CFG, mode="virtual", tokens=tokens, optimizer="sgd", lr=1e-2, iters=3, warmup=1,
+              verify_roundtrip=True, gemm="tcgen05", attn="tcgen05")
+    ref = ex.execute(sched, plan, **kw)
+    got = ex.execute(sched, plan, iteration_graph=True, **kw)
+    assert "iteration" in got.runners[0].graph_native_launches
+    assert ex.roundtrip_mismatches(got.runners) == []
+    for a, b in zip(got.losses, ref.losses):
+        assert abs(a - b) < 1e-3 * abs(b), (got.losses, ref.losses)
+    assert int(got.runners[0].flags.tensor.abs().sum()) == 0
     got.close()
     ref.close()
