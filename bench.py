@@ -624,6 +624,25 @@ def run_b200(args, rank, world, local_rank):
         if isinstance(v, dict):
             v.pop("_slab_bytes", None)
 
+    # ---- in-situ round trip at the workload shape: one host-issued iteration of the headline
+    # plan with integer digests of every offloaded slab at F end and at B start (bit-exact
+    # offload -> reload through the pinned pool, executor.roundtrip_mismatches)
+    roundtrip = None
+    try:
+        from paper_2503_01328_b200.runtime.executor import roundtrip_mismatches
+
+        rt_res = execute(sched, plans["full"], **dict(base_kw, iters=1, warmup=0, iteration_graph=False,
+                                                      verify_roundtrip=True, stream_mode="dual", gemm=backend))
+        mism = roundtrip_mismatches(rt_res.runners)
+        roundtrip = {"offloaded_pairs_checked": sum(len(r.digests) for r in rt_res.runners),
+                     "mismatches": len(mism), "slab_bytes": rt_res.slab_bytes}
+        rt_res.close()
+        del rt_res
+        gc.collect()
+        torch.cuda.empty_cache()
+    except Exception as e:  # noqa: BLE001
+        errors["roundtrip_check"] = f"{type(e).__name__}: {e}"[:500]
+
     # ---- north star: the least-memory measured policy within 5% of 1F1B without offload,
     # confirmed by re-measuring it against the baseline (alternating, 3 runs each, medians;
     # the 5% gate applies to the medians)
@@ -800,6 +819,7 @@ def run_b200(args, rank, world, local_rank):
                               "workspaces, boundary rings, graph pools, library temporaries (PAPER.md:265 "
                               "'peak minus iteration-start'); device_act_gb = the cudaMemGetInfo delta"),
         },
+        "roundtrip_check": roundtrip,
         "errors": errors,
     }
     for r in [full, auto, single, duplex] + line["offload"]["partial_candidates"] + \
