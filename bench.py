@@ -380,6 +380,7 @@ def policy_report(res, sched, plan, m, seq, slab_bytes, rank):
         "wbuf_gb": res.mem["wbuf_bytes"] / 1e9,  # split-backward W-pass gradient buffers
         "workspace_gb": res.mem["workspace_bytes"] / 1e9,  # recompute / GEMM workspaces
         "_offload_fraction": res.offload_fraction,
+        "_trace": res.trace,  # for the in-situ DMA fit (dropped before printing)
         "host_slots": prog.n_host_slots,
         "offloaded_pairs": len(prog.offloaded),
         "late_reloads": len(plan.late_list()) if plan is not None else 0,
@@ -691,6 +692,7 @@ def run_b200(args, rank, world, local_rank):
     from paper_2503_01328_b200.policy import DmaSlowdown, modelled_overheads
 
     dma_check = []
+    insitu = {}
     try:
         checks = [("1f1b_full_single_stream", "full_single", sched, plans["full"], "single", "none"),
                   ("1f1b_full_duplex_plan", "full_duplex", sched, plans["full_duplex"], "dual", "none")]
@@ -699,6 +701,15 @@ def run_b200(args, rank, world, local_rank):
             if name in variant_kw and variant_kw[name][1] is not None:
                 sv, pv, kw = variant_kw[name]
                 checks.append((name, name, sv, pv, kw["stream_mode"], f"{sv.kind}_v{sv.local_stages}_none"))
+        # in-situ slowdowns: fitted on one measured run per schedule family (the heaviest
+        # duplex traffic), then used to predict every other plan (out of sample)
+        from paper_2503_01328_b200.policy import fit_dma_slowdown
+
+        for fam, fit_key, base_key in ((False, "full", "none"), (True, "gis-h_v3_n1_duplex", "gis-h_v3_none")):
+            if fit_key in results and base_key in results and "_trace" in results[fit_key]:
+                base_s = {k: v / 1e3 for k, v in results[base_key]["pass_ms"].items()}
+                insitu[fam] = (fit_key, fit_dma_slowdown(results[fit_key]["_trace"], 0, base_s,
+                                                         DmaSlowdown.from_calibration(cal, split=fam)))
         base_cache = {}
         for label, rk, sv, pv, sm, base_key in checks:
             if rk not in results or base_key not in results or pv is None:
@@ -715,6 +726,12 @@ def run_b200(args, rank, world, local_rank):
             entry = {"policy": label, "measured_pct": round(measured, 2), "modelled_pct": round(100 * mo["model"], 2),
                      "modelled_dma_pct": round(100 * mo["model_dma"], 2),
                      "dma_error_pts": round(100 * mo["model_dma"] - measured, 2)}
+            if split in insitu:
+                fit_key, fit = insitu[split]
+                mi = modelled_overheads(sv, pv, 0, fit, sm, base=base_cache[key])
+                entry.update(modelled_insitu_pct=round(100 * mi["model_dma"], 2),
+                             insitu_error_pts=round(100 * mi["model_dma"] - measured, 2),
+                             insitu_fitted_on=fit_key)
             results[rk].update(modelled_pct=entry["modelled_pct"], modelled_dma_pct=entry["modelled_dma_pct"])
             dma_check.append(entry)
     except Exception as e:  # noqa: BLE001
@@ -814,6 +831,8 @@ def run_b200(args, rank, world, local_rank):
             "schedules": {k: results[k] for k in sched_variants if k in results},
             "gis-h_closed_loop_trials": gish_trials,
             "dma_model_check": dma_check,
+            "dma_insitu_fit": {("split" if k else "unsplit"): {"fitted_on": v[0], "F": v[1].f, "B": v[1].b, "W": v[1].w}
+                               for k, v in insitu.items()},
             "memory_method": ("peak_act_gb = torch allocator peak over the run minus the persistent training "
                               "state (bf16 weights, fp32 grads and masters): slab arenas, W-pass buffers, "
                               "workspaces, boundary rings, graph pools, library temporaries (PAPER.md:265 "
@@ -822,10 +841,10 @@ def run_b200(args, rank, world, local_rank):
         "roundtrip_check": roundtrip,
         "errors": errors,
     }
-    for r in [full, auto, single, duplex] + line["offload"]["partial_candidates"] + \
-            list(line["offload"]["schedules"].values()) + [none, results.get("none"), none_cublas]:
+    for r in list(results.values()) + [full, auto, single, duplex, none, none_cublas]:
         if isinstance(r, dict):
             r.pop("_offload_fraction", None)
+            r.pop("_trace", None)
     # k-aware partial offload: the least-memory measured candidate within 5% of no offload
     ok = [r for r in line["offload"]["partial_candidates"] if r["tokens_per_s"] >= none["tokens_per_s"] / 1.05]
     if ok:

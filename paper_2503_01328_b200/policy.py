@@ -76,6 +76,46 @@ def _overlaps(a: float, b: float, transfers) -> tuple[float, float, float]:
     return d_only, h_only, both
 
 
+def fit_dma_slowdown(trace, device: int, base_seconds: dict, fallback: DmaSlowdown | None = None) -> DmaSlowdown:
+    """In-situ DMA slowdown from a MEASURED run: every compute pass of ``device`` gives
+    duration / base - 1 = s_d2h * f_d2h + s_h2d * f_h2d + s_duplex * f_both, with f the
+    fractions of the pass overlapping D2H only, H2D only and both directions
+    (``_overlaps`` on the measured trace) and ``base_seconds[kind]`` the same pass kind's
+    mean duration without offload.  Least squares per pass kind (F, B, W), clipped at 0;
+    a kind without passes that overlap copies keeps ``fallback``'s values."""
+    import numpy as np
+
+    xfer = [(float(p.start), float(p.end), p.kind) for p in trace.transfer_passes() if p.device == device]
+    rows: dict = {}
+    for p in trace.compute_passes():
+        if p.device != device or str(p.kind) not in base_seconds:
+            continue
+        a, b = float(p.start), float(p.end)
+        if b <= a:
+            continue
+        od, oh, ox = _overlaps(a, b, xfer)
+        rows.setdefault(p.kind, []).append(((od / (b - a), oh / (b - a), ox / (b - a)),
+                                            (b - a) / base_seconds[str(p.kind)] - 1))
+    fb = fallback or DmaSlowdown()
+    fitted = {}
+    for kind in (PassKind.F, PassKind.B, PassKind.W):
+        data = rows.get(kind, [])
+        X = np.array([x for x, _ in data], dtype=float).reshape(-1, 3)
+        y = np.array([v for _, v in data], dtype=float)
+        if len(data) < 3 or X.sum() == 0:
+            fitted[kind] = fb.of(kind)
+            continue
+        coef = []
+        for j in range(3):  # columns without any overlap keep the fallback value
+            coef.append(None if X[:, j].sum() < 1e-9 else 0.0)
+        cols = [j for j in range(3) if coef[j] is not None]
+        sol, *_ = np.linalg.lstsq(X[:, cols], y, rcond=None)
+        for j, v in zip(cols, sol):
+            coef[j] = max(0.0, float(v))
+        fitted[kind] = tuple(fb.of(kind)[j] if coef[j] is None else coef[j] for j in range(3))
+    return DmaSlowdown(fitted[PassKind.F], fitted[PassKind.B], fitted[PassKind.W])
+
+
 def dma_adjusted_end(trace, device: int, dma: DmaSlowdown | None) -> float:
     """End of ``device``'s last compute pass with every pass stretched by the measured
     slowdown for the copy traffic it overlaps (first order: a device that computes

@@ -111,3 +111,31 @@ def test_choose_offload_respects_dma_model():
                            dma=DmaSlowdown(f=(0.5, 0.5, 0.9), b=(0.5, 0.5, 0.9), w=(0.5, 0.5, 0.9)))
     assert plain.plan is not None
     assert heavy.offloaded_pairs <= plain.offloaded_pairs
+
+
+def test_fit_dma_slowdown_recovers_synthetic_stretch():
+    """Passes that run entirely under D2H only / H2D only / both directions, stretched by
+    known factors: the in-situ least-squares fit recovers the factors per pass kind."""
+    from fractions import Fraction as Fr
+
+    from paper_2503_01328_b200.policy import fit_dma_slowdown
+    from paper_2503_01328_b200.schedule_types import Pass, PassKind
+
+    OFF, REL = PassKind.OFFLOAD, PassKind.RELOAD
+    xfers = [Pass(OFF, 0, 0, 0, Fr(0), Fr(100)), Pass(REL, 0, 0, 1, Fr(200), Fr(100)),
+             Pass(OFF, 0, 0, 2, Fr(400), Fr(100)), Pass(REL, 0, 0, 3, Fr(400), Fr(100))]
+    want = {PassKind.F: (0.2, 0.05, 0.3), PassKind.B: (0.25, 0.1, 0.4)}
+    base = {"F": 1.0, "B": 2.0}
+    comp = []
+    for kind, factors in want.items():
+        for region, f in zip((0, 200, 400), factors):
+            for i in range(4):
+                start = Fr(region + 10 + 20 * i + (5 if kind == PassKind.B else 0))
+                comp.append(Pass(kind, 0, 0, i, start, Fr(base[str(kind)] * (1 + f)).limit_denominator(10**6)))
+        comp.append(Pass(kind, 0, 0, 9, Fr(700), Fr(base[str(kind)])))  # no copies in flight
+    trace = type("T", (), {"compute_passes": lambda self: comp, "transfer_passes": lambda self: xfers})()
+    fit = fit_dma_slowdown(trace, 0, base)
+    for kind, factors in want.items():
+        for got, w in zip(fit.of(kind), factors):
+            assert abs(got - w) < 1e-6, (kind, fit)
+    assert fit.w == (0.0, 0.0, 0.0)  # no W passes: the fallback
