@@ -76,13 +76,15 @@ def _overlaps(a: float, b: float, transfers) -> tuple[float, float, float]:
     return d_only, h_only, both
 
 
-def fit_dma_slowdown(trace, device: int, base_seconds: dict, fallback: DmaSlowdown | None = None) -> DmaSlowdown:
+def fit_dma_slowdown(trace, device: int, base_seconds: dict, fallback: DmaSlowdown | None = None,
+                     min_mass: float = 2.0) -> DmaSlowdown:
     """In-situ DMA slowdown from a MEASURED run: every compute pass of ``device`` gives
     duration / base - 1 = s_d2h * f_d2h + s_h2d * f_h2d + s_duplex * f_both, with f the
     fractions of the pass overlapping D2H only, H2D only and both directions
     (``_overlaps`` on the measured trace) and ``base_seconds[kind]`` the same pass kind's
-    mean duration without offload.  Least squares per pass kind (F, B, W), clipped at 0;
-    a kind without passes that overlap copies keeps ``fallback``'s values."""
+    mean duration without offload.  Least squares per pass kind (F, B, W), clipped to
+    [0, 1]; a direction whose overlap sums to fewer than ``min_mass`` whole passes (too
+    little signal against run-to-run noise) keeps ``fallback``'s value."""
     import numpy as np
 
     xfer = [(float(p.start), float(p.end), p.kind) for p in trace.transfer_passes() if p.device == device]
@@ -106,12 +108,13 @@ def fit_dma_slowdown(trace, device: int, base_seconds: dict, fallback: DmaSlowdo
             fitted[kind] = fb.of(kind)
             continue
         coef = []
-        for j in range(3):  # columns without any overlap keep the fallback value
-            coef.append(None if X[:, j].sum() < 1e-9 else 0.0)
+        for j in range(3):  # a direction overlapped by < min_mass pass-equivalents keeps the fallback
+            coef.append(None if X[:, j].sum() < min_mass else 0.0)
         cols = [j for j in range(3) if coef[j] is not None]
-        sol, *_ = np.linalg.lstsq(X[:, cols], y, rcond=None)
-        for j, v in zip(cols, sol):
-            coef[j] = max(0.0, float(v))
+        if cols:
+            sol, *_ = np.linalg.lstsq(X[:, cols], y, rcond=None)
+            for j, v in zip(cols, sol):
+                coef[j] = min(1.0, max(0.0, float(v)))
         fitted[kind] = tuple(fb.of(kind)[j] if coef[j] is None else coef[j] for j in range(3))
     return DmaSlowdown(fitted[PassKind.F], fitted[PassKind.B], fitted[PassKind.W])
 

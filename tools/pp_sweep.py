@@ -135,7 +135,9 @@ def main():
             prog = res.programs[0]
             row = dict(head, plan=name, schedule=sv.kind, stream_mode=sm, tensors=tensors and len(tensors),
                        tokens_per_s=a.m * s / it, ms_per_step=it * 1e3,
-                       peak_act_gb=res.act_bytes[0] / 1e9, slab_gb=res.slab_bytes / 1e9,
+                       peak_act_gb=res.mem["alloc_peak_bytes"] / 1e9,  # measured: peak minus training state
+                       device_act_gb=res.mem["device_bytes"] / 1e9, arena_gb=res.act_bytes[0] / 1e9,
+                       wbuf_gb=res.mem["wbuf_bytes"] / 1e9, slab_gb=res.slab_bytes / 1e9,
                        offload_fraction=round(res.offload_fraction, 4),
                        host_pinned_gb=prog.n_host_slots * res.slab_bytes * res.offload_fraction / 1e9,
                        offloaded=len(prog.offloaded), late=len(plan.late_list()) if plan is not None else 0,
