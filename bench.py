@@ -703,13 +703,15 @@ def run_b200(args, rank, world, local_rank):
                 checks.append((name, name, sv, pv, kw["stream_mode"], f"{sv.kind}_v{sv.local_stages}_none"))
         # in-situ slowdowns: fitted on one measured run per schedule family (the heaviest
         # duplex traffic), then used to predict every other plan (out of sample)
-        from paper_2503_01328_b200.policy import fit_dma_slowdown
+        from paper_2503_01328_b200.policy import fit_dma_slowdown, link_factors
 
         for fam, fit_key, base_key in ((False, "full", "none"), (True, "gis-h_v3_n1_duplex", "gis-h_v3_none")):
             if fit_key in results and base_key in results and "_trace" in results[fit_key]:
                 base_s = {k: v / 1e3 for k, v in results[base_key]["pass_ms"].items()}
+                fit_plan = plans["full"] if not fam else variant_kw[fit_key][1]
                 insitu[fam] = (fit_key, fit_dma_slowdown(results[fit_key]["_trace"], 0, base_s,
-                                                         DmaSlowdown.from_calibration(cal, split=fam)))
+                                                         DmaSlowdown.from_calibration(cal, split=fam)),
+                               link_factors(results[fit_key]["_trace"], fit_plan, 0))
         base_cache = {}
         for label, rk, sv, pv, sm, base_key in checks:
             if rk not in results or base_key not in results or pv is None:
@@ -727,8 +729,8 @@ def run_b200(args, rank, world, local_rank):
                      "modelled_dma_pct": round(100 * mo["model_dma"], 2),
                      "dma_error_pts": round(100 * mo["model_dma"] - measured, 2)}
             if split in insitu:
-                fit_key, fit = insitu[split]
-                mi = modelled_overheads(sv, pv, 0, fit, sm, base=base_cache[key])
+                fit_key, fit, link = insitu[split]
+                mi = modelled_overheads(sv, pv, 0, fit, sm, base=base_cache[key], link=link)
                 entry.update(modelled_insitu_pct=round(100 * mi["model_dma"], 2),
                              insitu_error_pts=round(100 * mi["model_dma"] - measured, 2),
                              insitu_fitted_on=fit_key)
@@ -831,7 +833,8 @@ def run_b200(args, rank, world, local_rank):
             "schedules": {k: results[k] for k in sched_variants if k in results},
             "gis-h_closed_loop_trials": gish_trials,
             "dma_model_check": dma_check,
-            "dma_insitu_fit": {("split" if k else "unsplit"): {"fitted_on": v[0], "F": v[1].f, "B": v[1].b, "W": v[1].w}
+            "dma_insitu_fit": {("split" if k else "unsplit"): {"fitted_on": v[0], "F": v[1].f, "B": v[1].b, "W": v[1].w,
+                                                                 "link_factor_d2h_h2d": v[2]}
                                for k, v in insitu.items()},
             "memory_method": ("peak_act_gb = torch allocator peak over the run minus the persistent training "
                               "state (bf16 weights, fp32 grads and masters): slab arenas, W-pass buffers, "

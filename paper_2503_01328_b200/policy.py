@@ -119,6 +119,35 @@ def fit_dma_slowdown(trace, device: int, base_seconds: dict, fallback: DmaSlowdo
     return DmaSlowdown(fitted[PassKind.F], fitted[PassKind.B], fitted[PassKind.W])
 
 
+def link_factors(trace, plan: OffloadPlan, device: int) -> tuple[float, float]:
+    """Measured / planned duration of the D2H and H2D transfers of ``device`` in a
+    measured run of ``plan`` (1.0 where the device moved nothing): how much slower the
+    host link ran in situ -- under duplex load and beside compute -- than the calibrated
+    copy the plan's slots were sized with."""
+    planned = {(t.direction, t.stage, t.microbatch): float(t.duration)
+               for stm in plan.streams for t in stm.transfers if t.device == device}
+    out = []
+    for kind in (PassKind.OFFLOAD, PassKind.RELOAD):
+        got = [(float(p.duration), planned[(kind, p.stage, p.microbatch)]) for p in trace.transfer_passes()
+               if p.device == device and p.kind == kind and (kind, p.stage, p.microbatch) in planned]
+        out.append(sum(g for g, _ in got) / sum(w for _, w in got) if got else 1.0)
+    return out[0], out[1]
+
+
+def scale_transfers(plan: OffloadPlan, f_d2h: float, f_h2d: float) -> OffloadPlan:
+    """The same plan (slots, order, floors) with every transfer's duration scaled by the
+    measured link factor of its direction: what the runner model needs to price stalls
+    when the link runs slower than planned."""
+    from dataclasses import replace
+
+    def scaled(t):
+        f = f_d2h if t.direction == PassKind.OFFLOAD else f_h2d
+        return replace(t, duration=Fraction(t.duration * Fraction(f).limit_denominator(10**6)))
+
+    return replace(plan, streams=tuple(replace(stm, transfers=tuple(scaled(t) for t in stm.transfers))
+                                       for stm in plan.streams))
+
+
 def dma_adjusted_end(trace, device: int, dma: DmaSlowdown | None) -> float:
     """End of ``device``'s last compute pass with every pass stretched by the measured
     slowdown for the copy traffic it overlaps (first order: a device that computes
@@ -139,10 +168,13 @@ def dma_adjusted_end(trace, device: int, dma: DmaSlowdown | None) -> float:
 
 
 def modelled_overheads(sched: Schedule, plan, device: int, dma: DmaSlowdown | None = None,
-                       stream_mode: str = "single", base=None) -> dict:
+                       stream_mode: str = "single", base=None, link: tuple | None = None) -> dict:
     """Modelled overhead of ``plan`` at ``device`` versus no offload: the reference runner
-    model alone, and with the measured DMA slowdown (``dma_adjusted_end``)."""
+    model alone, and with the measured DMA slowdown (``dma_adjusted_end``); ``link`` =
+    (D2H, H2D) measured link factors (``link_factors``) stretch the plan's transfers."""
     base = base or simulate(sched, stream_mode=stream_mode)
+    if link is not None:
+        plan = scale_transfers(plan, *link)
     tr = simulate(sched, plan, stream_mode=stream_mode)
     b = dma_adjusted_end(base, device, None)
     return {"model": dma_adjusted_end(tr, device, None) / b - 1,

@@ -139,3 +139,22 @@ def test_fit_dma_slowdown_recovers_synthetic_stretch():
         for got, w in zip(fit.of(kind), factors):
             assert abs(got - w) < 1e-6, (kind, fit)
     assert fit.w == (0.0, 0.0, 0.0)  # no W passes: the fallback
+
+
+def test_scaled_transfers_price_stalls():
+    """A link running 4x slower than planned: the same plan, transfers stretched, makes
+    the runner model predict the stall (reloads floor later, B waits)."""
+    from fractions import Fraction
+
+    import paper_2503_01328_b200 as po
+    from paper_2503_01328_b200.policy import modelled_overheads, scale_transfers
+
+    U = po.PassCosts.unit()
+    sched, plan = po.build_1f1b_full_offload(4, 8, U, Fraction(3, 2))
+    slow = scale_transfers(plan, 2.0, 2.0)
+    assert [t.slot for s in slow.streams for t in s.transfers] == [t.slot for s in plan.streams for t in s.transfers]
+    assert all(b.duration == 2 * a.duration for sa, sb in zip(plan.streams, slow.streams)
+               for a, b in zip(sa.transfers, sb.transfers))
+    m1 = modelled_overheads(sched, plan, 0)
+    m2 = modelled_overheads(sched, plan, 0, link=(4.0, 4.0))  # k = 1/2: 2x still fits the window
+    assert m2["model"] > m1["model"]
