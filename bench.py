@@ -656,8 +656,10 @@ def run_b200(args, rank, world, local_rank):
                                          dict(stream_mode=c.stream_mode, offload_tensors=c.tensors, gemm=backend))
     for name, spec in variant_kw.items():
         cand_pool[name] = (name, spec[0], spec[1], spec[2])
+    # single runs are noisy (+-2-5% between runs and boxes, profiles/r2_gish_m_probe.jsonl): every
+    # memory-lowering policy within 10% in its single run is a candidate for the 3-run gate
     single_ok = sorted((results[rk]["peak_act_gb"], key) for key, (rk, *_x) in cand_pool.items()
-                       if rk in results and results[rk]["tokens_per_s"] >= none["tokens_per_s"] / 1.05
+                       if rk in results and results[rk]["tokens_per_s"] >= none["tokens_per_s"] / 1.10
                        and results[rk]["peak_act_gb"] < none["peak_act_gb"])
     confirm = {"runs_per_policy": 3, "tried": []}
     none_kw = dict(stream_mode="single", gemm=backend)
@@ -855,7 +857,7 @@ def run_b200(args, rank, world, local_rank):
         line["offload"]["partial"] = best
         line["offload"]["overhead_partial_pct"] = pct(best)
         line["offload"]["partial_peak_reduction_pct"] = 100 * (1 - best["peak_act_gb"] / none["peak_act_gb"])
-    line["offload"]["least_memory_within_5pct_single_run"] = [
+    line["offload"]["confirm_candidates_within_10pct_single_run"] = [
         {"policy": key, "peak_act_gb": gb} for gb, key in single_ok]
     # the north-star answer: confirmed over 3 alternating runs (median gate), else none
     line["offload"]["least_memory_within_5pct"] = confirm.get("chosen") or {
@@ -907,7 +909,7 @@ def main():
     ap.add_argument("--no-schedules", dest="schedules", action="store_false",
                     help="skip the GIS-H / PO split-backward schedule variants")
     ap.add_argument("--partial-top", type=int, default=3, help="partial-offload plans to measure (0: none)")
-    ap.add_argument("--confirm-top", type=int, default=2,
+    ap.add_argument("--confirm-top", type=int, default=3,
                     help="least-memory policies within 5%% re-measured 3x against the baseline (north-star gate)")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)

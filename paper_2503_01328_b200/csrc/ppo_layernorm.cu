@@ -77,8 +77,8 @@ __device__ __forceinline__ void load8f(const float* p, float (&o)[8]) {
 // kDual (no residual): two independent LayerNorms in one launch -- rows [0, rows_a) are
 // LN(src) * gamma + beta -> ln, rows [rows_a, rows) are LN(resid) * gamma_b + beta_b -> out
 // (the W pass's LN1 and LN2 recompute: one 4E launch instead of two 2E launches).
-template <bool kResidual, int W, int kVecPerLane, int G, bool kDual = false>
-__global__ void __launch_bounds__(32 * W * G) ln_fwd_kernel(
+template <bool kResidual, int W, int kVecPerLane, int G, bool kDual = false, int kMinBlocks = 1>
+__global__ void __launch_bounds__(32 * W * G, kMinBlocks > 1 ? kMinBlocks : 0) ln_fwd_kernel(
     const __nv_bfloat16* __restrict__ resid, const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
     const float* __restrict__ gamma, const float* __restrict__ beta, __nv_bfloat16* __restrict__ ln, int64_t rows,
     int hidden, float eps, uint32_t threshold, float scale, uint64_t seed, uint64_t offset_add,
@@ -337,6 +337,17 @@ static int vpl_choice(int64_t hidden, int dflt) {
   return v;
 }
 
+// PPO_LN_FWD_MINB=4: forward LayerNorm kernels compiled for >= 4 resident CTAs per SM
+// (register cap 64 at 256 threads) -- an occupancy A/B for the latency-bound C2 shapes.
+static bool ln_fwd_min4() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PPO_LN_FWD_MINB");
+    v = (e && atoi(e) == 4) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static int warps_per_row(int64_t hidden, int vpl) { return (int)((hidden + 256 * vpl - 1) / (256 * vpl)); }
 
 struct RowLaunch {
@@ -403,11 +414,15 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
   RowLaunch l;
   int rc = PPO_OK;
   const int vpl = vpl_choice(hidden, 4);
-#define PPO_LN_FWD_W(W, V)                                                                                    \
-  if ((rc = row_launch(ln_fwd_kernel<false, W, V, fwd_groups_for(W)>, rows, hidden, W, 0, &l, fwd_groups_for(W)))) return rc; \
-  launch_pdl(ln_fwd_kernel<false, W, V, fwd_groups_for(W)>, l.grid, l.block, l.smem, as_stream(stream),                                  \
-      nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta, static_cast<__nv_bfloat16*>(y), rows, \
-      (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0, nullptr, nullptr, (int64_t)0);
+#define PPO_LN_FWD_K(W, V, MB)                                                                                \
+  if ((rc = row_launch(ln_fwd_kernel<false, W, V, fwd_groups_for(W), false, MB>, rows, hidden, W, 0, &l,      \
+                       fwd_groups_for(W)))) return rc;                                                         \
+  launch_pdl(ln_fwd_kernel<false, W, V, fwd_groups_for(W), false, MB>, l.grid, l.block, l.smem,                \
+      as_stream(stream), nullptr, static_cast<const __nv_bfloat16*>(x), nullptr, gamma, beta,                  \
+      static_cast<__nv_bfloat16*>(y), rows, (int)hidden, eps, 0u, 1.f, 0, 0, nullptr, 0, nullptr, nullptr,      \
+      (int64_t)0);
+#define PPO_LN_FWD_W(W, V)                                \
+  if (ln_fwd_min4()) { PPO_LN_FWD_K(W, V, 4) } else { PPO_LN_FWD_K(W, V, 1) }
 #define PPO_LN_FWD_V(V)                                               \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \
@@ -424,6 +439,7 @@ int ppo_layernorm_fwd(const void* x, const float* gamma, const float* beta, void
   PPO_VPL_DISPATCH(vpl, PPO_LN_FWD_V)
 #undef PPO_LN_FWD_V
 #undef PPO_LN_FWD_W
+#undef PPO_LN_FWD_K
   PPO_LAUNCHED("ln_fwd_kernel");
   return PPO_OK;
 }
@@ -439,13 +455,16 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   RowLaunch l;
   int rc = PPO_OK;
   const int vpl = vpl_choice(hidden, 4);
-#define PPO_RES_W(W, V)                                                                                      \
-  if ((rc = row_launch(ln_fwd_kernel<true, W, V, fwd_groups_for(W)>, rows, hidden, W, 0, &l, fwd_groups_for(W)))) return rc; \
-  launch_pdl(ln_fwd_kernel<true, W, V, fwd_groups_for(W)>, l.grid, l.block, l.smem, as_stream(stream),                                  \
-      static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),                   \
-      static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps, \
+#define PPO_RES_K(W, V, MB)                                                                                   \
+  if ((rc = row_launch(ln_fwd_kernel<true, W, V, fwd_groups_for(W), false, MB>, rows, hidden, W, 0, &l,       \
+                       fwd_groups_for(W)))) return rc;                                                         \
+  launch_pdl(ln_fwd_kernel<true, W, V, fwd_groups_for(W), false, MB>, l.grid, l.block, l.smem,                 \
+      as_stream(stream), static_cast<const __nv_bfloat16*>(resid), static_cast<const __nv_bfloat16*>(branch),  \
+      static_cast<__nv_bfloat16*>(out), gamma, beta, static_cast<__nv_bfloat16*>(ln), rows, (int)hidden, eps,   \
       dropout_threshold(p), 1.f / (1.f - p), seed, offset, offset_base, p > 0.f ? 1 : 0, nullptr, nullptr,      \
       (int64_t)0);
+#define PPO_RES_W(W, V)                                   \
+  if (ln_fwd_min4()) { PPO_RES_K(W, V, 4) } else { PPO_RES_K(W, V, 1) }
 #define PPO_RES_V(V)                                                  \
   {                                                                   \
     switch (warps_per_row(hidden, V)) {                               \
@@ -462,6 +481,7 @@ int ppo_residual_dropout_ln_fwd(const void* resid, const void* branch, void* out
   PPO_VPL_DISPATCH(vpl, PPO_RES_V)
 #undef PPO_RES_V
 #undef PPO_RES_W
+#undef PPO_RES_K
   PPO_LAUNCHED("ln_fwd_kernel<residual>");
   return PPO_OK;
 }

@@ -95,7 +95,8 @@ def test_row_kernels_do_not_spill(lib):
     assert len(bwd_ln) >= 10
     for f, u in bwd_ln.items():
         assert int(re.search(r"STACK:(\d+)", u).group(1)) <= 8, (f, u)
-    fwd4 = {f: u for f, u in usage.items() if re.search(r"ln_fwd_kernelILb[01]ELi\d+ELi4E", f)}
+    # default build of the forward kernels (kMinBlocks = 1; the PPO_LN_FWD_MINB=4 A/B variants may spill)
+    fwd4 = {f: u for f, u in usage.items() if re.search(r"ln_fwd_kernelILb[01]ELi\d+ELi4ELi\d+ELb[01]ELi1EE", f)}
     assert fwd4
     for f, u in fwd4.items():
         assert int(re.search(r"STACK:(\d+)", u).group(1)) <= 8, (f, u)
