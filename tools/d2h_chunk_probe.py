@@ -1,8 +1,7 @@
 """D2H interference vs issue granularity: the HBM-bound compute loop (LayerNorm + GeLU at
 C2) beside back-to-back D2H of 504 MB issued as one cudaMemcpyAsync or as chunks of
-64 / 16 / 4 MB on the same copy stream, or through cudaMemcpyBatchAsync without / with
-the cudaMemcpyFlagPreferOverlapWithCompute hint (tools/probes/batchcopy.cu); link GB/s
-of each issue pattern alone."""
+64 / 16 / 4 MB on the same copy stream; link GB/s of each issue pattern alone.  (The
+batched-copy driver call measured in round 1 is closed on this GPU pool and was removed.)"""
 import json
 import os
 import sys
@@ -22,17 +21,9 @@ N = 504_102_912
 hd = torch.empty(N, dtype=torch.uint8, pin_memory=True)
 dd = torch.empty(N, dtype=torch.uint8, device=dev)
 cs, s1 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-import ctypes  # noqa: E402
-
-_bc = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "probes", "libbatchcopy.so"))
-_bc.batch_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint, ctypes.c_void_p]
 
 
 def d2h(chunk):
-    if isinstance(chunk, str):  # "batch0" / "batch1": cudaMemcpyBatchAsync with flags 0 / PreferOverlapWithCompute
-        rc = _bc.batch_copy(hd.data_ptr(), dd.data_ptr(), N, int(chunk[-1]), s1.cuda_stream)
-        assert rc == 0, rc
-        return
     with torch.cuda.stream(s1):
         if chunk is None:
             hd.copy_(dd, non_blocking=True)
@@ -70,7 +61,7 @@ def compute(bg_chunk="none", n=100):
 
 compute()
 out = {"alone_us": compute()}
-for c in (None, 64 << 20, 16 << 20, 4 << 20, "batch0", "batch1"):
-    key = "whole" if c is None else (c if isinstance(c, str) else f"{c >> 20}MB")
+for c in (None, 64 << 20, 16 << 20, 4 << 20):
+    key = "whole" if c is None else f"{c >> 20}MB"
     out[key] = {"link_gbs": link(c), "compute_us": compute(c)}
 print(json.dumps(out))
