@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PPO_ABI_VERSION 8
+#define PPO_ABI_VERSION 9
 
 #define PPO_OK 0
 #define PPO_EINVAL (-1)   /* bad argument (null pointer, misaligned, bad size)      */
@@ -245,6 +245,20 @@ int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
  * causal tile scheduler; the first call per seq must not be inside a stream capture. */
 int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t heads, int64_t head_dim, float scale,
                  void* stream);
+
+/* ----------------------------------------------- K7b: causal attention backward */
+/* The backward of the attention core priced by costs.py:144-161 (backward = 2x the
+ * forward's 4bs^2h).  From qkv[s, 3h], the saved o[s, h] and lse[heads, s] (natural log,
+ * as ppo_attn_fwd writes them into the slab) and the output gradient dout[s, h], writes
+ * dqkv[s, 3h] = [dq | dk | dv] (bf16), the single operand of the QKV projection's dgrad
+ * and wgrad GEMMs.  head_dim 128, seq a multiple of 128.  Hand-written tcgen05 kernel:
+ * one CTA per (128-row kv block, head), five 128^3 UMMAs per tile with S, dP, dK, dV in
+ * TMEM, dQ through TMA bulk reduce-add into the fp32 workspace
+ * (ppo_attn_bwd_workspace_bytes: dq accumulator s*h + row statistics heads*s, fp32).
+ * dq is accumulated in an unspecified order (fp32 reduce-add), dk and dv are not. */
+int64_t ppo_attn_bwd_workspace_bytes(int64_t seq, int64_t heads, int64_t head_dim);
+int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv, void* workspace,
+                 int64_t seq, int64_t heads, int64_t head_dim, float scale, void* stream);
 
 /* ----------------------------------------------- K8: stage-boundary send/recv */
 /* NCCL communicator of the pipeline (one rank per GPU).  The 128-byte unique id is

@@ -1,0 +1,599 @@
+// libppo_b200.so -- K7b causal attention backward on tcgen05 (sm_100a), hand-written.
+//
+//   ppo_attn_bwd   dqkv[s, 3h] (bf16: dq | dk | dv, the layout the QKV projection's
+//                  dgrad and wgrad GEMMs consume as one operand) from qkv[s, 3h], the
+//                  saved o[s, h] and lse[heads, s] (both reloaded from the activation
+//                  slab), and the output gradient do[s, h].
+//
+// The reference prices attention only through its FLOP model (pkg/src/ppoff/costs.py:
+// 144-161: the s-term of 12bsh(6h+s), backward = 2x forward) and keeps o and the softmax
+// statistics in the saved set (costs.py:99-105), so the backward needs no recompute of
+// the forward statistics: P = exp(scale * Q K^T - lse).
+//
+// One CTA per (kv block j of 128 rows, head); it walks the q blocks i >= j (causal) and
+// keeps dK_j, dV_j in TMEM for the whole walk.  Per (i, j) tile, five 128x128x128 UMMAs
+// (tcgen05.mma.cta_group::1.kind::f16, fp32 accumulators in TMEM):
+//
+//   S^T  = K_j Q_i^T           A = K  smem K-major   B = Q  smem K-major   -> TMEM S
+//   dP^T = V_j dO_i^T          A = V  smem K-major   B = dO smem K-major   -> TMEM dP
+//   dV  += P^T dO_i            A = P^T TMEM (bf16)   B = dO smem MN-major  -> TMEM dV
+//   dK  += dS^T Q_i            A = dS^T smem K-major B = Q  smem MN-major  -> TMEM dK
+//   dQ_i = dS K_j              A = dS smem MN-major  B = K  smem MN-major  -> TMEM dQ (= dP cols)
+//
+// Every operand tile is loaded once by TMA in the 128-byte-swizzled layout and read by
+// the tensor core both K-major and MN-major (the swizzle atom of 8 rows x 128 B is the
+// same physical arrangement for both), so Q, dO and K feed two UMMAs each without a
+// transpose.  dQ partials leave through TMA bulk reduce-add (cp.reduce.async.bulk.tensor
+// .add.f32) into an fp32 accumulator; a small kernel scales and casts it into dqkv.
+//
+// Warp roles (448 threads): warps 0-3 drain dQ from TMEM into the reduce-add, warps 4-11
+// (two warpgroups, q columns 0-63 / 64-127) compute P = exp2(S*scale*log2e - lse*log2e)
+// and dS = P (dP - delta) and write P^T to TMEM and dS^T to shared memory, warp 12 issues
+// the UMMAs (one thread) and owns the TMEM allocation, warp 13 issues the TMA loads.
+// TMEM (512 columns x 128 lanes): dK [0,128), dV [128,256), dP / dQ [256,384),
+// S [384,512) with P^T (bf16 pairs) over S's first 64 columns.
+#include <cuda.h>  // CUtensorMap; the encoder comes from cudaGetDriverEntryPoint
+
+#include <mutex>
+
+#include "ppo_common.cuh"
+
+namespace ppo {
+namespace attnb {
+
+constexpr int kTile = 128;           // kv rows per CTA, q rows per step, head_dim
+constexpr int kHalf = 128 * 64 * 2;  // one 128-row x 64-column bf16 TMA box (16 KB)
+constexpr int kTileBytes = 2 * kHalf;
+
+// shared memory map (bytes from the 1024-aligned dynamic base)
+constexpr int kOffK = 0;
+constexpr int kOffV = kOffK + kTileBytes;
+constexpr int kOffQ = kOffV + kTileBytes;   // 2 stages
+constexpr int kOffDO = kOffQ + 2 * kTileBytes;  // 1 stage
+constexpr int kOffDS = kOffDO + kTileBytes;
+constexpr int kOffStg = kOffDS + kTileBytes;  // dQ staging: 4 warps x 2 x 4 KB
+constexpr int kStgBytes = 32 * 32 * 4;
+constexpr int kOffLse = kOffStg + 4 * 2 * kStgBytes;  // 2 stages x 128 fp32
+constexpr int kOffDelta = kOffLse + 2 * 512;
+constexpr int kOffBar = kOffDelta + 2 * 512;
+constexpr int kNumBars = 16;
+constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
+constexpr int kSmemBytes = kOffTmemPtr + 16;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+// barrier indices
+enum : int {
+  B_KV = 0,
+  B_QF0 = 1,  // q_full[2]
+  B_QE0 = 3,  // q_empty[2]
+  B_DOF = 5,
+  B_DOE = 6,
+  B_SF = 7,
+  B_PF = 8,
+  B_DPF = 9,
+  B_DSF = 10,
+  B_DSE = 11,
+  B_DQF = 12,
+  B_DQE = 13,
+  B_DKV = 14,
+};
+
+constexpr uint32_t kColDK = 0, kColDV = 128, kColDP = 256, kColS = 384;
+constexpr int kThreads = 448;
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]
+__device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns; thread t gets lane (base lane + t).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return reinterpret_cast<uint32_t&>(v);
+}
+
+// UMMA shared-memory descriptors for a 128 x 128 bf16 tile stored as two 64-column halves
+// (16 KB apart), 128 B per row, 128-byte swizzle (the TMA SWIZZLE_128B box layout).
+//   K-major (rows = M/N, columns = K):  SBO = 1024 B between 8-row groups; the k-th
+//     16-element step starts 32 B further inside the swizzle atom (next half at k = 4).
+//   MN-major (rows = K, columns = M/N): LBO = 16 KB between the 64-wide M/N halves,
+//     SBO = 1024 B between 8-row K groups; the k-th 16-row step starts 2 KB further.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int k) {
+  return sdesc(tile + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int k) { return sdesc(tile + k * 2048, kHalf, 1024); }
+
+// instruction descriptor: bf16 x bf16 -> f32, M = N = 128
+__host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((128u >> 3) << 17) |
+         ((128u >> 4) << 24);
+}
+
+struct Params {
+  __nv_bfloat16* dqkv;
+  const float* lse;  // [H, s] natural log
+  const float* delta;  // [H, s]
+  int s, H;
+  float scale;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_dq, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hd = blockIdx.x, jb = blockIdx.y;
+  const int n_q = p.s / kTile;
+  const int n_it = n_q - jb;  // q blocks jb .. n_q-1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmemPtr);
+  float* s_lse = reinterpret_cast<float*>(smem + kOffLse);
+  float* s_delta = reinterpret_cast<float*>(smem + kOffDelta);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[B_KV], 1);
+    mbar_init(&bars[B_QF0], 1);
+    mbar_init(&bars[B_QF0 + 1], 1);
+    mbar_init(&bars[B_QE0], 1);
+    mbar_init(&bars[B_QE0 + 1], 1);
+    mbar_init(&bars[B_DOF], 1);
+    mbar_init(&bars[B_DOE], 1);
+    mbar_init(&bars[B_SF], 1);
+    mbar_init(&bars[B_PF], 8);
+    mbar_init(&bars[B_DPF], 1);
+    mbar_init(&bars[B_DSF], 8);
+    mbar_init(&bars[B_DSE], 1);
+    mbar_init(&bars[B_DQF], 1);
+    mbar_init(&bars[B_DQE], 4);
+    mbar_init(&bars[B_DKV], 1);
+    mbar_fence_init();
+  }
+  if (warp == 12) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_ptr))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 13 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_qkv)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_do)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dq)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp == 13) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      const int H = p.H;
+      mbar_expect_tx(&bars[B_KV], 2 * kTileBytes);
+      for (int half = 0; half < 2; ++half) {
+        tma_load_3d(smem + kOffK + half * kHalf, &tm_qkv, half * 64, H + hd, jb * kTile, &bars[B_KV]);
+        tma_load_3d(smem + kOffV + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, jb * kTile, &bars[B_KV]);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int qb = jb + it, st = it & 1;
+        mbar_wait(&bars[B_QE0 + st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&bars[B_QF0 + st], kTileBytes + 1024);
+        for (int half = 0; half < 2; ++half)
+          tma_load_3d(smem + kOffQ + st * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd, qb * kTile,
+                      &bars[B_QF0 + st]);
+        tma_load_1d(s_lse + st * 128, p.lse + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
+        tma_load_1d(s_delta + st * 128, p.delta + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
+        mbar_wait(&bars[B_DOE], (it & 1) ^ 1);
+        mbar_expect_tx(&bars[B_DOF], kTileBytes);
+        for (int half = 0; half < 2; ++half)
+          tma_load_3d(smem + kOffDO + half * kHalf, &tm_do, half * 64, hd, qb * kTile, &bars[B_DOF]);
+      }
+    }
+  } else if (warp == 12) {
+    // ===================================================== UMMA issuer
+    if (lane == 0) {
+      const uint32_t sK = sbase + kOffK, sV = sbase + kOffV, sDO = sbase + kOffDO, sDS = sbase + kOffDS;
+      const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tDV = tmem + kColDV, tDK = tmem + kColDK;
+      constexpr uint32_t I_KK = idesc(0, 0), I_KM = idesc(0, 1), I_MM = idesc(1, 1);
+      mbar_wait(&bars[B_KV], 0);
+      tc_fence_after();
+      for (int it = 0; it <= n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t sQ = sbase + kOffQ + st * kTileBytes;
+        if (it < n_it) {
+          mbar_wait(&bars[B_QF0 + st], (it >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) umma_ss(tS, desc_k(sK, k), desc_k(sQ, k), I_KK, k > 0);
+          tc_commit(&bars[B_SF]);
+        }
+        if (it > 0) {
+          // dQ(it-1), dK(it-1): dS(it-1) is in shared memory
+          const int pt = it - 1;
+          const uint32_t sQp = sbase + kOffQ + (pt & 1) * kTileBytes;
+          mbar_wait(&bars[B_DSF], pt & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) umma_ss(tDP, desc_mn(sDS, k), desc_mn(sK, k), I_MM, k > 0);
+          tc_commit(&bars[B_DQF]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) umma_ss(tDK, desc_k(sDS, k), desc_mn(sQp, k), I_KM, (pt > 0 || k > 0));
+          tc_commit(&bars[B_QE0 + (pt & 1)]);
+          tc_commit(&bars[B_DSE]);
+          if (it == n_it) tc_commit(&bars[B_DKV]);
+        }
+        if (it < n_it) {
+          mbar_wait(&bars[B_DOF], it & 1);
+          if (it > 0) mbar_wait(&bars[B_DQE], (it - 1) & 1);  // dQ(it-1) drained: dP reuses its columns
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) umma_ss(tDP, desc_k(sV, k), desc_k(sDO, k), I_KK, k > 0);
+          tc_commit(&bars[B_DPF]);
+          mbar_wait(&bars[B_PF], it & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) umma_ts(tDV, tS + k * 8, desc_mn(sDO, k), I_KM, (it > 0 || k > 0));
+          tc_commit(&bars[B_DOE]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================================================== softmax-gradient warpgroups
+    const int wg = (warp - 4) >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // kv row within the tile (TMEM lane)
+    const int c0 = wg * 64;               // q columns of this warpgroup
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const float sl2 = p.scale * 1.4426950408889634f;
+    uint8_t* ds_row = smem + kOffDS + wg * kHalf + row * 128;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const float* lse = s_lse + st * 128 + c0;
+      const float* dlt = s_delta + st * 128 + c0;
+      mbar_wait(&bars[B_QF0 + st], (it >> 1) & 1);
+      mbar_wait(&bars[B_SF], it & 1);
+      tc_fence_after();
+      float pr[64];
+      {
+        uint32_t r[32];
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          tmem_ld32(tmem + lane_off + kColS + c0 + ch * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) pr[ch * 32 + c] = __uint_as_float(r[c]);
+        }
+      }
+      const bool diag = it == 0;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        float v = ex2(fmaf(pr[c], sl2, -lse[c] * 1.4426950408889634f));
+        pr[c] = (diag && c0 + c < row) ? 0.f : v;
+      }
+      // every S column of this tile has been read before P^T overwrites the first 64
+      tc_fence_before();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      tc_fence_after();
+      {
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = pack_bf16(pr[2 * c], pr[2 * c + 1]);
+        tmem_st32(tmem + lane_off + kColS + wg * 32, r);
+        tmem_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_PF]);
+
+      mbar_wait(&bars[B_DPF], it & 1);
+      tc_fence_after();
+      mbar_wait(&bars[B_DSE], (it & 1) ^ 1);  // dQ/dK of the previous step have read dS
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + kColDP + c0 + ch * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v8 = 0; v8 < 4; ++v8) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = ch * 32 + v8 * 8 + 2 * e;
+            const float d0 = pr[c] * (__uint_as_float(r[v8 * 8 + 2 * e]) - dlt[c]);
+            const float d1 = pr[c + 1] * (__uint_as_float(r[v8 * 8 + 2 * e + 1]) - dlt[c + 1]);
+            w[e] = pack_bf16(d0, d1);
+          }
+          const int chunk = ch * 4 + v8;  // 16-byte chunk within the 128-byte row
+          *reinterpret_cast<uint4*>(ds_row + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy dS writes -> tensor-core reads
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_DSF]);
+    }
+    // ---- epilogue: dV and scale * dK rows of this kv block into dqkv
+    mbar_wait(&bars[B_DKV], 0);
+    tc_fence_after();
+    const size_t h = size_t(p.H) * kTile;
+    __nv_bfloat16* out = p.dqkv + (size_t(jb) * kTile + row) * 3 * h + size_t(hd) * kTile + c0;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {  // 0: dK (scaled), 1: dV
+      const uint32_t col = m == 0 ? kColDK : kColDV;
+      const float f = m == 0 ? p.scale : 1.f;
+      __nv_bfloat16* dst = out + (m == 0 ? h : 2 * h);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + col + c0 + ch * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v8 = 0; v8 < 4; ++v8) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(r[v8 * 8 + 0]) * f, __uint_as_float(r[v8 * 8 + 1]) * f);
+          w.y = pack_bf16(__uint_as_float(r[v8 * 8 + 2]) * f, __uint_as_float(r[v8 * 8 + 3]) * f);
+          w.z = pack_bf16(__uint_as_float(r[v8 * 8 + 4]) * f, __uint_as_float(r[v8 * 8 + 5]) * f);
+          w.w = pack_bf16(__uint_as_float(r[v8 * 8 + 6]) * f, __uint_as_float(r[v8 * 8 + 7]) * f);
+          *reinterpret_cast<uint4*>(dst + ch * 32 + v8 * 8) = w;
+        }
+      }
+    }
+  } else {
+    // ===================================================== dQ drain: TMEM -> smem -> TMA reduce-add
+    const int quarter = warp;  // TMEM lanes 32*warp .. +31 = q rows of the tile
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    uint8_t* stg = smem + kOffStg + warp * 2 * kStgBytes;
+    int buf = 0;
+    for (int it = 0; it < n_it; ++it) {
+      const int qb = jb + it;
+      mbar_wait(&bars[B_DQF], it & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + kColDP + ch * 32, r);
+        tmem_wait_ld();
+        if (ch == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[B_DQE]);
+        }
+        // the reduce that last read this staging buffer has finished reading it
+        if (lane == 0) tma_store_wait_read<1>();
+        __syncwarp();
+        uint8_t* row_p = stg + buf * kStgBytes + lane * 128;
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<uint4*>(row_p + ((v ^ (lane & 7)) << 4)) =
+              make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_3d(&tm_dq, stg + buf * kStgBytes, ch * 32, hd, qb * kTile + quarter * 32);
+          tma_store_commit();
+        }
+        buf ^= 1;
+      }
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// delta[hd, i] = sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), and the fp32 dQ
+// accumulator row i zeroed.  One block per row; 16 lanes per head of 128.
+__global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                                            const __nv_bfloat16* __restrict__ dout,
+                                                            float* __restrict__ delta, float* __restrict__ dq_acc,
+                                                            int s, int H) {
+  pdl_wait();
+  const int i = blockIdx.x;
+  const int h = H * kTile;
+  for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
+    const int e = e0 + threadIdx.x * 8;
+    const bool ok = e < h;
+    float acc = 0.f;
+    if (ok) {
+      float a[8], b[8];
+      unpack8(*reinterpret_cast<const uint4*>(o + size_t(i) * h + e), a);
+      unpack8(*reinterpret_cast<const uint4*>(dout + size_t(i) * h + e), b);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = fmaf(a[k], b[k], acc);
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (ok) {
+      if ((threadIdx.x & 15) == 0) delta[size_t(e / kTile) * s + i] = acc;
+      float4* z = reinterpret_cast<float4*>(dq_acc + size_t(i) * h + e);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+// dqkv[:, 0:h] = bf16(scale * dq_acc)
+__global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const float* __restrict__ dq_acc,
+                                                          __nv_bfloat16* __restrict__ dqkv, int s, int h, float scale) {
+  pdl_wait();
+  const size_t n8 = size_t(s) * h / 8;
+  for (size_t v = blockIdx.x * size_t(blockDim.x) + threadIdx.x; v < n8; v += size_t(gridDim.x) * blockDim.x) {
+    const size_t e = v * 8;
+    const size_t row = e / h, col = e % h;
+    const float4 a = reinterpret_cast<const float4*>(dq_acc)[2 * v];
+    const float4 b = reinterpret_cast<const float4*>(dq_acc)[2 * v + 1];
+    float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale, b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+    *reinterpret_cast<uint4*>(dqkv + row * 3 * h + col) = pack8(f);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder(int* rc) {
+  static std::once_flag once;
+  static EncodeTiled fn = nullptr;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(f);
+  });
+  *rc = fn ? PPO_OK : set_error(PPO_ENOTSUP, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 3-D map over a row-major [rows][heads][D] view: dims (D, heads, rows), 128-byte swizzle.
+static int make_map(EncodeTiled enc, CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+                    uint64_t heads, uint64_t rows, uint64_t row_stride_bytes, uint32_t box_d, uint32_t box_rows) {
+  cuuint64_t dims[3] = {kTile, heads, rows};
+  cuuint64_t strides[2] = {uint64_t(kTile) * esize, row_stride_bytes};
+  cuuint32_t box[3] = {box_d, 1, box_rows};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PPO_EINVAL, "ppo_attn_bwd: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PPO_OK;
+}
+
+}  // namespace attnb
+}  // namespace ppo
+
+using namespace ppo;
+using namespace ppo::attnb;
+
+extern "C" {
+
+int64_t ppo_attn_bwd_workspace_bytes(int64_t seq, int64_t heads, int64_t head_dim) {
+  return (seq * heads * head_dim + heads * seq) * int64_t(sizeof(float));
+}
+
+int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv, void* workspace,
+                 int64_t seq, int64_t heads, int64_t head_dim, float scale, void* stream) {
+  if (!qkv || !o || !dout || !lse || !dqkv || !workspace || seq <= 0 || heads <= 0)
+    return set_error(PPO_EINVAL, "ppo_attn_bwd: bad arguments");
+  if (head_dim != kTile) return set_error(PPO_ESHAPE, "ppo_attn_bwd: head_dim %lld (compiled for 128)", (long long)head_dim);
+  if (seq % kTile != 0 || seq >= (1ll << 30) || heads * head_dim * 3 >= (1ll << 31))
+    return set_error(PPO_ESHAPE, "ppo_attn_bwd: seq %lld must be a multiple of 128", (long long)seq);
+  if (!aligned16(qkv) || !aligned16(o) || !aligned16(dout) || !aligned16(lse) || !aligned16(dqkv) ||
+      !aligned16(workspace))
+    return set_error(PPO_EINVAL, "ppo_attn_bwd: misaligned");
+  const int s = int(seq), H = int(heads);
+  const int64_t h = heads * head_dim;
+  cudaStream_t st = as_stream(stream);
+  int rc = PPO_OK;
+  EncodeTiled enc = encoder(&rc);
+  if (rc) return rc;
+  float* dq_acc = static_cast<float*>(workspace);
+  float* delta = dq_acc + size_t(s) * h;
+
+  CUtensorMap tm_qkv, tm_do, tm_dq;
+  if ((rc = make_map(enc, &tm_qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, 3 * heads, seq, 3 * h * 2, 64, kTile)))
+    return rc;
+  if ((rc = make_map(enc, &tm_do, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, heads, seq, h * 2, 64, kTile))) return rc;
+  if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, heads, seq, h * 4, 32, 32))) return rc;
+
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return cuda_error(attr_err, "ppo_attn_bwd: smem attribute");
+
+  launch_pdl(attn_bwd_prep_kernel, dim3(s), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
+             static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, s, H);
+  PPO_LAUNCHED("attn_bwd_prep_kernel");
+  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse, delta, s, H, scale};
+  attn_bwd_kernel<<<dim3(H, s / kTile), kThreads, kSmemBytes, st>>>(tm_qkv, tm_do, tm_dq, prm);
+  PPO_LAUNCHED("attn_bwd_kernel");
+  const int sms = sm_count_current();
+  launch_pdl(attn_bwd_dq_kernel, dim3(sms * 4), dim3(256), 0, st, static_cast<const float*>(dq_acc),
+             static_cast<__nv_bfloat16*>(dqkv), s, int(h), scale);
+  PPO_LAUNCHED("attn_bwd_dq_kernel");
+  return PPO_OK;
+}
+
+}  // extern "C"

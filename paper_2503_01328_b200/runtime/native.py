@@ -52,7 +52,7 @@ class P2POp(ctypes.Structure):
 
 
 _VP, _U64, _I64, _F32, _I32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_float, ctypes.c_int
-ABI_VERSION = 8  # include/ppo_b200.h PPO_ABI_VERSION
+ABI_VERSION = 9  # include/ppo_b200.h PPO_ABI_VERSION
 _FP = ctypes.POINTER(ctypes.c_float)
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -92,6 +92,8 @@ SIGNATURES = {
     "ppo_gemm_nn_dgelu": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_wgrad": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_attn_fwd": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
+    "ppo_attn_bwd_workspace_bytes": [_I64, _I64, _I64],
+    "ppo_attn_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
     "ppo_comm_init": [ctypes.POINTER(ctypes.c_uint8), _I32, _I32, _I32, ctypes.POINTER(_VP)],
     "ppo_comm_destroy": [_VP],
@@ -102,6 +104,7 @@ _RESTYPES = {
     "ppo_kernel_launches": ctypes.c_uint64,
     "ppo_pool_base": ctypes.c_void_p,
     "ppo_pool_bytes": ctypes.c_uint64,
+    "ppo_attn_bwd_workspace_bytes": ctypes.c_int64,
 }
 
 _lock = threading.Lock()
@@ -291,6 +294,34 @@ def attn_fwd(qkv, o, lse, heads, scale=None, stream=None):
     scale = D ** -0.5 if scale is None else scale
     SHAPES[("ppo_attn_fwd", s, heads, D)] += 1
     call("ppo_attn_fwd", _ptr(qkv), _ptr(o), _ptr(lse), s, heads, D, scale, _stream(stream))
+
+
+def attn_bwd_workspace_bytes(seq, heads, head_dim=128):
+    return int(load().ppo_attn_bwd_workspace_bytes(seq, heads, head_dim))
+
+
+def attn_bwd(qkv, o, do, lse, dqkv, heads, workspace, scale=None, stream=None):
+    """Causal attention backward on tcgen05 (K7b): dqkv[s, 3h] = [dq | dk | dv] (bf16) from
+    qkv[s, 3h], the saved o[s, h] and lse[heads, s] and the output gradient do[s, h].
+    ``workspace``: a CUDA buffer of at least ``attn_bwd_workspace_bytes`` (fp32 dq
+    accumulator + row statistics)."""
+    _check_bf16(qkv, o, do, dqkv)
+    s, h3 = qkv.shape
+    h = h3 // 3
+    D = h // heads
+    if (h3 != 3 * h or tuple(o.shape) != (s, h) or tuple(do.shape) != (s, h) or tuple(dqkv.shape) != (s, h3)
+            or lse.dtype != _torch().float32 or not lse.is_cuda or lse.numel() != heads * s):
+        raise ValueError(f"attn_bwd shapes: qkv {tuple(qkv.shape)} o {tuple(o.shape)} do {tuple(do.shape)} "
+                         f"dqkv {tuple(dqkv.shape)} lse {tuple(lse.shape)}")
+    if not all(t.is_contiguous() for t in (qkv, o, do, lse, dqkv)):
+        raise ValueError("attn_bwd: operands must be contiguous")
+    need = attn_bwd_workspace_bytes(s, heads, D)
+    if not workspace.is_cuda or workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"attn_bwd: workspace needs {need} bytes")
+    scale = D ** -0.5 if scale is None else scale
+    SHAPES[("ppo_attn_bwd", s, heads, D)] += 1
+    call("ppo_attn_bwd", _ptr(qkv), _ptr(o), _ptr(do), _ptr(lse), _ptr(dqkv), _ptr(workspace), s, heads, D, scale,
+         _stream(stream))
 
 
 def gemm_nn(a, b, d, beta=0.0, stream=None):

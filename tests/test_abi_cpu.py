@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "ppo_b200.h")
 def declared():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return set(re.findall(r"^\s*(?:int|const char\*|uint64_t|void\*)\s+(ppo_\w+)\s*\(", text, flags=re.M))
+    return set(re.findall(r"^\s*(?:int|int64_t|const char\*|uint64_t|void\*)\s+(ppo_\w+)\s*\(", text, flags=re.M))
 
 
 def macro(name):
