@@ -26,7 +26,7 @@
 // transpose.  dQ partials leave through TMA bulk reduce-add (cp.reduce.async.bulk.tensor
 // .add.f32) into an fp32 accumulator; a small kernel scales and casts it into dqkv.
 //
-// Warp roles (448 threads): warps 0-3 drain dQ from TMEM into the reduce-add, warps 4-11
+// Warp roles (512 threads): warps 0-3 drain dQ from TMEM into the reduce-add, warps 4-11
 // (two warpgroups, q columns 0-63 / 64-127) compute P = exp2(S*scale*log2e - lse*log2e)
 // and dS = P (dP - delta) and write P^T to TMEM and dS^T to shared memory, warp 12 issues
 // the UMMAs (one thread) and owns the TMEM allocation, warp 13 issues the TMA loads.
@@ -34,6 +34,7 @@
 // S [384,512) with P^T (bf16 pairs) over S's first 64 columns.
 #include <cuda.h>  // CUtensorMap; the encoder comes from cudaGetDriverEntryPoint
 
+#include <cstdlib>
 #include <mutex>
 
 #include "ppo_common.cuh"
@@ -76,10 +77,11 @@ enum : int {
   B_DQF = 12,
   B_DQE = 13,
   B_DKV = 14,
+  B_DBG = 15,  // diagnostics: per-GEMM completion (PPO_ATB_EXP bit 2)
 };
 
 constexpr uint32_t kColDK = 0, kColDV = 128, kColDP = 256, kColS = 384;
-constexpr int kThreads = 448;
+constexpr int kThreads = 512;  // warps 14, 15 idle: setmaxnreg works per warpgroup
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -89,13 +91,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// one lane of a converged warp (the UMMA warp runs converged so its operands stay uniform)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, 0xffffffff;\n@px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  if (elect_one())
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
 
 // D[tmem] (+)= A[smem] * B[smem]
 __device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (elect_one())
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
@@ -105,6 +118,7 @@ __device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint
 
 // D[tmem] (+)= A[tmem] * B[smem]
 __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (elect_one())
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
@@ -159,6 +173,17 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// (2^a, 2^b) through one ex2.approx.f16x2 (inputs rounded to f16, results widened to fp32)
+__device__ __forceinline__ float2 ex2_pair(float a, float b) {
+  uint32_t h;
+  asm("{\n.reg .b32 t;\ncvt.rn.f16x2.f32 t, %2, %1;\nex2.approx.f16x2 %0, t;\n}\n" : "=r"(h) : "f"(a), "f"(b));
+  float2 r;
+  asm("{\n.reg .f16 lo, hi;\nmov.b32 {lo, hi}, %2;\ncvt.f32.f16 %0, lo;\ncvt.f32.f16 %1, hi;\n}\n"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(h));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return reinterpret_cast<uint32_t&>(v);
@@ -174,10 +199,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
          (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
+// (the k-th step adds a constant to the start-address field: no carry, addresses < 2^18)
 __device__ __forceinline__ uint64_t desc_k(uint32_t tile, int k) {
-  return sdesc(tile + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
+  return sdesc(tile, 16, 1024) + uint64_t(((k >> 2) * kHalf + (k & 3) * 32) >> 4);
 }
-__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int k) { return sdesc(tile + k * 2048, kHalf, 1024); }
+__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int k) {
+  return sdesc(tile, kHalf, 1024) + uint64_t((k * 2048) >> 4);
+}
 
 // instruction descriptor: bf16 x bf16 -> f32, M = N = 128
 __host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn) {
@@ -185,13 +213,57 @@ __host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn) {
          ((128u >> 4) << 24);
 }
 
+// One 128 x 128 x 128 GEMM = 8 UMMAs of K = 16, issued by one elected lane of the
+// converged UMMA warp.  a4 / b4: shared-memory tile start >> 4 (descriptor address field),
+// or for kATmem the TMEM address of A (K = 16 per 8 columns of bf16 pairs).  Descriptor low
+// words are a4/b4 + compile-time constants (no carry: addresses < 2^18); the high word is
+// SBO = 1024 B, version 1, SWIZZLE_128B for both majors.
+template <bool kAMn, bool kBMn, bool kATmem>
+__device__ __forceinline__ void gemm128(uint32_t d, uint32_t a4, uint32_t b4, uint32_t idesc, bool acc) {
+  asm volatile("" : "+r"(a4), "+r"(b4));  // keep the per-k descriptors out of the loop-invariant pool
+  constexpr uint64_t kHi = uint64_t(0x40004040u) << 32;
+  if (elect_one()) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t boff = kBMn ? (k * 2048) >> 4 : (((k >> 2) * kHalf + (k & 3) * 32) >> 4);
+      const uint64_t bd = kHi | (b4 + boff + (kBMn ? (uint32_t(kHalf) >> 4) << 16 : 1u << 16));
+      const uint32_t en = (acc || k > 0) ? 1u : 0u;
+      if constexpr (kATmem) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+            "r"(a4 + k * 8), "l"(bd), "r"(idesc), "r"(en)
+            : "memory");
+      } else {
+        const uint32_t aoff = kAMn ? (k * 2048) >> 4 : (((k >> 2) * kHalf + (k & 3) * 32) >> 4);
+        const uint64_t ad = kHi | (a4 + aoff + (kAMn ? (uint32_t(kHalf) >> 4) << 16 : 1u << 16));
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(en)
+            : "memory");
+      }
+    }
+  }
+  __syncwarp();
+}
+
 struct Params {
   __nv_bfloat16* dqkv;
   const float* lse;  // [H, s] natural log
   const float* delta;  // [H, s]
+  float* dq_acc;       // [s, h] fp32
   int s, H;
   float scale;
+  long long* trace;  // diagnostics: per-event SM clocks of CTA (0, 0), or null
+  int exp_mode;      // diagnostics (PPO_ATB_EXP): bit 0 no dQ reduce (wrong dq), bit 2 timed GEMMs, bit 3 GEMM forms
 };
+
+// diagnostics (ppo_attn_bwd_trace): event e of step `it` at trace[e * 256 + it]
+#define ATB_TRACE(e, it)                                                                      \
+  do {                                                                                        \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (it) < 256) p.trace[(e) * 256 + (it)] = clock64(); \
+  } while (0)
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -222,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars[B_DQF], 1);
     mbar_init(&bars[B_DQE], 4);
     mbar_init(&bars[B_DKV], 1);
+    mbar_init(&bars[B_DBG], 1);
     mbar_fence_init();
   }
   if (warp == 12) {
@@ -239,6 +312,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
   const uint32_t sbase = smem_u32(smem);
+  // register budget per warpgroup (64K registers / 512 threads = 128 at launch): the
+  // issue warpgroup (12-15) gives 72 per thread to the dQ drain and softmax-gradient
+  // warpgroups (152 each).  Each side's roles branch below without re-merging, so the
+  // allocator sees one budget per path.
+  if (warp >= 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
 
   if (warp == 13) {
     // ===================================================== TMA producer
@@ -252,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int it = 0; it < n_it; ++it) {
         const int qb = jb + it, st = it & 1;
         mbar_wait(&bars[B_QE0 + st], ((it >> 1) & 1) ^ 1);
+        ATB_TRACE(28, it);
         mbar_expect_tx(&bars[B_QF0 + st], kTileBytes + 1024);
         for (int half = 0; half < 2; ++half)
           tma_load_3d(smem + kOffQ + st * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd, qb * kTile,
@@ -259,60 +339,114 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_1d(s_lse + st * 128, p.lse + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
         tma_load_1d(s_delta + st * 128, p.delta + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
         mbar_wait(&bars[B_DOE], (it & 1) ^ 1);
+        ATB_TRACE(29, it);
         mbar_expect_tx(&bars[B_DOF], kTileBytes);
         for (int half = 0; half < 2; ++half)
           tma_load_3d(smem + kOffDO + half * kHalf, &tm_do, half * 64, hd, qb * kTile, &bars[B_DOF]);
       }
     }
   } else if (warp == 12) {
-    // ===================================================== UMMA issuer
-    if (lane == 0) {
-      const uint32_t sK = sbase + kOffK, sV = sbase + kOffV, sDO = sbase + kOffDO, sDS = sbase + kOffDS;
+    // ===================================================== UMMA issuer (converged warp, one lane issues)
+    {
+      const uint32_t sb4 = sbase >> 4;
+      const uint32_t aK = sb4 + (kOffK >> 4), aV = sb4 + (kOffV >> 4), aDO = sb4 + (kOffDO >> 4),
+                     aDS = sb4 + (kOffDS >> 4);
       const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tDV = tmem + kColDV, tDK = tmem + kColDK;
       constexpr uint32_t I_KK = idesc(0, 0), I_KM = idesc(0, 1), I_MM = idesc(1, 1);
       mbar_wait(&bars[B_KV], 0);
       tc_fence_after();
+      uint32_t dbg_ph = 0;
+      // diagnostics: serialise one GEMM and time it (events 16.. start, 17.. done)
+      auto dbg_start = [&](int ev, int i) {
+        if (p.exp_mode & 4) ATB_TRACE(ev, i);
+      };
+      auto dbg_done = [&](int ev, int i) {
+        if (p.exp_mode & 4) {
+          tc_commit(&bars[B_DBG]);
+          mbar_wait(&bars[B_DBG], dbg_ph);
+          dbg_ph ^= 1;
+          ATB_TRACE(ev, i);
+        }
+      };
+      if ((p.exp_mode & 8) && blockIdx.x == 0 && blockIdx.y == 0 && p.trace) {
+        // diagnostics: clocks per GEMM form, 16 back to back on resident operands
+        mbar_wait(&bars[B_QF0], 0);
+        mbar_wait(&bars[B_DOF], 0);
+        tc_fence_after();
+        const uint32_t aQ = sb4 + (kOffQ >> 4);
+        for (int form = 0; form < 6; ++form) {
+          const long long t0 = clock64();
+          for (int r = 0; r < 16; ++r) {
+            if (form == 0) gemm128<false, false, false>(tS, aK, aQ, I_KK, false);
+            else if (form == 1) gemm128<true, true, false>(tDP, aDS, aK, I_MM, false);
+            else if (form == 2) gemm128<false, true, false>(tDK, aDS, aQ, I_KM, true);
+            else if (form == 3) gemm128<false, true, true>(tDV, tS, aDO, I_KM, true);
+            else if (form == 4) gemm128<false, false, true>(tDV, tS, aDO, I_KK, true);
+            else gemm128<false, false, false>(tDK, aDS, aQ, I_KK, true);
+          }
+          tc_commit(&bars[B_DBG]);
+          mbar_wait(&bars[B_DBG], dbg_ph);
+          dbg_ph ^= 1;
+          if (lane == 0) p.trace[30 * 256 + form] = (clock64() - t0) / 16;
+        }
+      }
       for (int it = 0; it <= n_it; ++it) {
         const int st = it & 1;
-        const uint32_t sQ = sbase + kOffQ + st * kTileBytes;
+        const uint32_t aQ = sb4 + ((kOffQ + st * kTileBytes) >> 4);
         if (it < n_it) {
           mbar_wait(&bars[B_QF0 + st], (it >> 1) & 1);
+          ATB_TRACE(0, it);
           tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < 8; ++k) umma_ss(tS, desc_k(sK, k), desc_k(sQ, k), I_KK, k > 0);
+          dbg_start(16, it);
+          gemm128<false, false, false>(tS, aK, aQ, I_KK, false);  // S^T = K Q^T
+          dbg_done(17, it);
           tc_commit(&bars[B_SF]);
+          ATB_TRACE(1, it);
         }
         if (it > 0) {
           // dQ(it-1), dK(it-1): dS(it-1) is in shared memory
           const int pt = it - 1;
-          const uint32_t sQp = sbase + kOffQ + (pt & 1) * kTileBytes;
+          const uint32_t aQp = sb4 + ((kOffQ + (pt & 1) * kTileBytes) >> 4);
           mbar_wait(&bars[B_DSF], pt & 1);
+          ATB_TRACE(2, pt);
           tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < 8; ++k) umma_ss(tDP, desc_mn(sDS, k), desc_mn(sK, k), I_MM, k > 0);
+          dbg_start(18, pt);
+          gemm128<true, true, false>(tDP, aDS, aK, I_MM, false);  // dQ = dS K
+          dbg_done(19, pt);
           tc_commit(&bars[B_DQF]);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) umma_ss(tDK, desc_k(sDS, k), desc_mn(sQp, k), I_KM, (pt > 0 || k > 0));
+          gemm128<false, true, false>(tDK, aDS, aQp, I_KM, pt > 0);  // dK += dS^T Q
+          dbg_done(23, pt);
           tc_commit(&bars[B_QE0 + (pt & 1)]);
           tc_commit(&bars[B_DSE]);
+          ATB_TRACE(3, pt);
           if (it == n_it) tc_commit(&bars[B_DKV]);
         }
         if (it < n_it) {
           mbar_wait(&bars[B_DOF], it & 1);
+          ATB_TRACE(4, it);
           if (it > 0) mbar_wait(&bars[B_DQE], (it - 1) & 1);  // dQ(it-1) drained: dP reuses its columns
+          ATB_TRACE(5, it);
           tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < 8; ++k) umma_ss(tDP, desc_k(sV, k), desc_k(sDO, k), I_KK, k > 0);
+          dbg_start(24, it);
+          gemm128<false, false, false>(tDP, aV, aDO, I_KK, false);  // dP^T = V dO^T
+          dbg_done(25, it);
           tc_commit(&bars[B_DPF]);
+          ATB_TRACE(6, it);
           mbar_wait(&bars[B_PF], it & 1);
+          ATB_TRACE(7, it);
           tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < 8; ++k) umma_ts(tDV, tS + k * 8, desc_mn(sDO, k), I_KM, (it > 0 || k > 0));
+          dbg_start(26, it);
+          gemm128<false, true, true>(tDV, tS, aDO, I_KM, it > 0);  // dV += P^T dO
+          dbg_done(27, it);
           tc_commit(&bars[B_DOE]);
+          ATB_TRACE(8, it);
         }
       }
     }
-  } else if (warp >= 4) {
+  }  // warps 14, 15: idle register donors
+  } else {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
+  if (warp >= 4) {
     // ===================================================== softmax-gradient warpgroups
     const int wg = (warp - 4) >> 2, quarter = warp & 3;
     const int row = quarter * 32 + lane;  // kv row within the tile (TMEM lane)
@@ -326,28 +460,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* dlt = s_delta + st * 128 + c0;
       mbar_wait(&bars[B_QF0 + st], (it >> 1) & 1);
       mbar_wait(&bars[B_SF], it & 1);
+      if (warp == 4 && lane == 0) ATB_TRACE(10, it);
       tc_fence_after();
       float pr[64];
       {
-        uint32_t r[32];
+        uint32_t r[2][32];
+        tmem_ld32(tmem + lane_off + kColS + c0, r[0]);
+        tmem_ld32(tmem + lane_off + kColS + c0 + 32, r[1]);
+        tmem_wait_ld();
+        if (warp == 4 && lane == 0) ATB_TRACE(40, it);
+        float4 l4[16];
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          tmem_ld32(tmem + lane_off + kColS + c0 + ch * 32, r);
-          tmem_wait_ld();
+        for (int v = 0; v < 16; ++v) l4[v] = reinterpret_cast<const float4*>(lse)[v];
+        // exp2 on packed halves: one MUFU op per two elements (the SFU is the bound of this
+        // phase); |x| < 16 carries >= 7 fractional bits, below the bf16 rounding P gets for
+        // the tensor core anyway
 #pragma unroll
-          for (int c = 0; c < 32; ++c) pr[ch * 32 + c] = __uint_as_float(r[c]);
+        for (int c = 0; c < 64; c += 2) {
+          const float* l = reinterpret_cast<const float*>(l4);
+          const float x0 = fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l[c] * 1.4426950408889634f);
+          const float x1 = fmaf(__uint_as_float(r[c >> 5][(c + 1) & 31]), sl2, -l[c + 1] * 1.4426950408889634f);
+          const float2 e = ex2_pair(x0, x1);
+          pr[c] = e.x;
+          pr[c + 1] = e.y;
         }
       }
-      const bool diag = it == 0;
+      if (it == 0) {  // the diagonal tile: q < kv is masked
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        float v = ex2(fmaf(pr[c], sl2, -lse[c] * 1.4426950408889634f));
-        pr[c] = (diag && c0 + c < row) ? 0.f : v;
+        for (int c = 0; c < 64; ++c) pr[c] = c0 + c < row ? 0.f : pr[c];
       }
+      if (warp == 4 && lane == 0) ATB_TRACE(41, it);
       // every S column of this tile has been read before P^T overwrites the first 64
       tc_fence_before();
       asm volatile("bar.sync 1, 256;" ::: "memory");
       tc_fence_after();
+      if (warp == 4 && lane == 0) ATB_TRACE(42, it);
       {
         uint32_t r[32];
 #pragma unroll
@@ -355,36 +502,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st32(tmem + lane_off + kColS + wg * 32, r);
         tmem_wait_st();
       }
+      if (warp == 4 && lane == 0) ATB_TRACE(43, it);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_PF]);
+      if (warp == 4 && lane == 0) ATB_TRACE(11, it);
 
       mbar_wait(&bars[B_DPF], it & 1);
+      if (warp == 4 && lane == 0) ATB_TRACE(12, it);
       tc_fence_after();
       mbar_wait(&bars[B_DSE], (it & 1) ^ 1);  // dQ/dK of the previous step have read dS
-#pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_off + kColDP + c0 + ch * 32, r);
+      if (warp == 4 && lane == 0) ATB_TRACE(13, it);
+      {
+        uint32_t r[2][32];
+        tmem_ld32(tmem + lane_off + kColDP + c0, r[0]);
+        tmem_ld32(tmem + lane_off + kColDP + c0 + 32, r[1]);
         tmem_wait_ld();
+        if (warp == 4 && lane == 0) ATB_TRACE(44, it);
 #pragma unroll
-        for (int v8 = 0; v8 < 4; ++v8) {
+        for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk (8 q columns) of the 128-byte row
+          const float4 d0 = reinterpret_cast<const float4*>(dlt)[2 * chunk];
+          const float4 d1 = reinterpret_cast<const float4*>(dlt)[2 * chunk + 1];
+          const float dl[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int c = ch * 32 + v8 * 8 + 2 * e;
-            const float d0 = pr[c] * (__uint_as_float(r[v8 * 8 + 2 * e]) - dlt[c]);
-            const float d1 = pr[c + 1] * (__uint_as_float(r[v8 * 8 + 2 * e + 1]) - dlt[c + 1]);
-            w[e] = pack_bf16(d0, d1);
+            const int c = chunk * 8 + 2 * e;
+            const float a0 = pr[c] * (__uint_as_float(r[c >> 5][c & 31]) - dl[2 * e]);
+            const float a1 = pr[c + 1] * (__uint_as_float(r[(c + 1) >> 5][(c + 1) & 31]) - dl[2 * e + 1]);
+            w[e] = pack_bf16(a0, a1);
           }
-          const int chunk = ch * 4 + v8;  // 16-byte chunk within the 128-byte row
           *reinterpret_cast<uint4*>(ds_row + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
+        if (warp == 4 && lane == 0) ATB_TRACE(45, it);
       }
       fence_proxy_async_smem();  // generic-proxy dS writes -> tensor-core reads
+      if (warp == 4 && lane == 0) ATB_TRACE(46, it);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_DSF]);
+      if (warp == 4 && lane == 0) ATB_TRACE(14, it);
     }
     // ---- epilogue: dV and scale * dK rows of this kv block into dqkv
     mbar_wait(&bars[B_DKV], 0);
@@ -421,17 +578,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; it < n_it; ++it) {
       const int qb = jb + it;
       mbar_wait(&bars[B_DQF], it & 1);
+      if (warp == 0 && lane == 0) ATB_TRACE(20, it);
       tc_fence_after();
-#pragma unroll 1
+      // all 128 columns in registers first: the dQ columns are dP's, and the next dP
+      // UMMA waits for this release (B_DQE) on the tensor core's critical path
+      uint32_t r[4][32];
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) tmem_ld32(tmem + lane_off + kColDP + ch * 32, r[ch]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_DQE]);
+      if (warp == 0 && lane == 0) ATB_TRACE(21, it);
+#pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_off + kColDP + ch * 32, r);
-        tmem_wait_ld();
-        if (ch == 3) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[B_DQE]);
-        }
+        if (p.exp_mode & 1) break;
         // the reduce that last read this staging buffer has finished reading it
         if (lane == 0) tma_store_wait_read<1>();
         __syncwarp();
@@ -439,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int v = 0; v < 8; ++v)
           *reinterpret_cast<uint4*>(row_p + ((v ^ (lane & 7)) << 4)) =
-              make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+              make_uint4(r[ch][4 * v], r[ch][4 * v + 1], r[ch][4 * v + 2], r[ch][4 * v + 3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -450,6 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) tma_store_wait_all();
+  }
   }
 
   tc_fence_before();
@@ -539,6 +701,8 @@ static int make_map(EncodeTiled enc, CUtensorMap* m, CUtensorMapDataType dt, int
   return PPO_OK;
 }
 
+static long long* g_trace = nullptr;
+
 }  // namespace attnb
 }  // namespace ppo
 
@@ -546,6 +710,11 @@ using namespace ppo;
 using namespace ppo::attnb;
 
 extern "C" {
+
+int ppo_attn_bwd_trace(void* trace) {
+  g_trace = static_cast<long long*>(trace);
+  return PPO_OK;
+}
 
 int64_t ppo_attn_bwd_workspace_bytes(int64_t seq, int64_t heads, int64_t head_dim) {
   return (seq * heads * head_dim + heads * seq) * int64_t(sizeof(float));
@@ -586,7 +755,11 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   launch_pdl(attn_bwd_prep_kernel, dim3(s), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
              static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, s, H);
   PPO_LAUNCHED("attn_bwd_prep_kernel");
-  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse, delta, s, H, scale};
+  static const int exp_mode = [] {
+    const char* e = std::getenv("PPO_ATB_EXP");
+    return e ? std::atoi(e) : 0;
+  }();
+  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse, delta, dq_acc, s, H, scale, g_trace, exp_mode};
   attn_bwd_kernel<<<dim3(H, s / kTile), kThreads, kSmemBytes, st>>>(tm_qkv, tm_do, tm_dq, prm);
   PPO_LAUNCHED("attn_bwd_kernel");
   const int sms = sm_count_current();

@@ -93,6 +93,7 @@ SIGNATURES = {
     "ppo_gemm_wgrad": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_attn_fwd": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_attn_bwd_workspace_bytes": [_I64, _I64, _I64],
+    "ppo_attn_bwd_trace": [_VP],
     "ppo_attn_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
     "ppo_comm_init": [ctypes.POINTER(ctypes.c_uint8), _I32, _I32, _I32, ctypes.POINTER(_VP)],

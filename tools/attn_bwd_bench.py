@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run_one(s, H, D=128):
+def run_one(s, H, D=128, eager=0):
     import torch
 
     from bench import _graph_time_us
@@ -45,6 +45,11 @@ def run_one(s, H, D=128):
         torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
             t["do4"], t["q"], t["k"], t["v"], r[0], r[1], r[6], r[7], None, r[2], r[3], r[4], r[5], 0.0, True)
 
+    if eager:  # for ncu: plain launches of ours only
+        for i in range(eager):
+            ours(sets[i % 2])
+        torch.cuda.synchronize()
+        return {"s": s, "heads": H, "eager_launches": eager}
     flops = 5 * s * s * h
     out = {"s": s, "heads": H, "head_dim": D}
     for name, fn in (("ours", ours), ("cudnn", cudnn)):
@@ -56,10 +61,11 @@ def run_one(s, H, D=128):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="4096x16,8192x32,16384x40")
+    ap.add_argument("--eager", type=int, default=0, help="only launch ours N times (for ncu)")
     a = ap.parse_args()
     for shp in a.shapes.split(","):
         s, H = map(int, shp.split("x"))
-        print(json.dumps(run_one(s, H)), flush=True)
+        print(json.dumps(run_one(s, H, eager=a.eager)), flush=True)
 
 
 if __name__ == "__main__":
