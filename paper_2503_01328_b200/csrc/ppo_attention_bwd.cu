@@ -42,25 +42,33 @@
 namespace ppo {
 namespace attnb {
 
-constexpr int kTile = 128;           // kv rows per CTA, q rows per step, head_dim
+constexpr int kTile = 128;           // kv rows per CTA, q rows per step
 constexpr int kHalf = 128 * 64 * 2;  // one 128-row x 64-column bf16 TMA box (16 KB)
-constexpr int kTileBytes = 2 * kHalf;
-
-// shared memory map (bytes from the 1024-aligned dynamic base)
-constexpr int kOffK = 0;
-constexpr int kOffV = kOffK + kTileBytes;
-constexpr int kOffQ = kOffV + kTileBytes;   // 2 stages
-constexpr int kOffDO = kOffQ + 2 * kTileBytes;  // 1 stage
-constexpr int kOffDS = kOffDO + kTileBytes;
-constexpr int kOffStg = kOffDS + kTileBytes;  // dQ staging: 4 warps x 2 x 4 KB
 constexpr int kStgBytes = 32 * 32 * 4;
-constexpr int kOffLse = kOffStg + 4 * 2 * kStgBytes;  // 2 stages x 128 fp32
-constexpr int kOffDelta = kOffLse + 2 * 512;
-constexpr int kOffBar = kOffDelta + 2 * 512;
-constexpr int kNumBars = 16;
-constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
-constexpr int kSmemBytes = kOffTmemPtr + 16;
-static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+// Per head_dim D (64 or 128): tiles of 128 rows x D are D/64 boxes of 64 columns.
+// Shared memory map (bytes from the 1024-aligned dynamic base) and TMEM columns:
+// dK [0, D), dV [D, 2D), dP / dQ [2D, 2D + 128), S [2D + 128, 2D + 256) (P^T over its
+// first 64 columns).
+template <int D>
+struct Cfg {
+  static constexpr int kHalves = D / 64;
+  static constexpr int kTileBytes = kHalves * kHalf;
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kTileBytes;
+  static constexpr int kOffQ = kOffV + kTileBytes;       // 2 stages
+  static constexpr int kOffDO = kOffQ + 2 * kTileBytes;  // 1 stage
+  static constexpr int kOffDS = kOffDO + kTileBytes;     // 128 x 128 bf16
+  static constexpr int kOffStg = kOffDS + 2 * kHalf;     // dQ staging: 4 warps x 2 x 4 KB
+  static constexpr int kOffLse = kOffStg + 4 * 2 * kStgBytes;  // 2 stages x 128 fp32
+  static constexpr int kOffDelta = kOffLse + 2 * 512;
+  static constexpr int kOffBar = kOffDelta + 2 * 512;
+  static constexpr int kNumBars = 16;
+  static constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
+  static constexpr int kSmemBytes = kOffTmemPtr + 16;
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
+  static constexpr uint32_t kColDK = 0, kColDV = D, kColDP = 2 * D, kColS = 2 * D + 128;
+};
 
 // barrier indices
 enum : int {
@@ -80,7 +88,6 @@ enum : int {
   B_DBG = 15,  // diagnostics: per-GEMM completion (PPO_ATB_EXP bit 2)
 };
 
-constexpr uint32_t kColDK = 0, kColDV = 128, kColDP = 256, kColS = 384;
 constexpr int kThreads = 512;  // warps 14, 15 idle: setmaxnreg works per warpgroup
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -173,17 +180,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// (2^a, 2^b) through one ex2.approx.f16x2 (inputs rounded to f16, results widened to fp32)
-__device__ __forceinline__ float2 ex2_pair(float a, float b) {
-  uint32_t h;
-  asm("{\n.reg .b32 t;\ncvt.rn.f16x2.f32 t, %2, %1;\nex2.approx.f16x2 %0, t;\n}\n" : "=r"(h) : "f"(a), "f"(b));
-  float2 r;
-  asm("{\n.reg .f16 lo, hi;\nmov.b32 {lo, hi}, %2;\ncvt.f32.f16 %0, lo;\ncvt.f32.f16 %1, hi;\n}\n"
-      : "=f"(r.x), "=f"(r.y)
-      : "r"(h));
-  return r;
-}
-
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return reinterpret_cast<uint32_t&>(v);
@@ -199,32 +195,23 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
          (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-// (the k-th step adds a constant to the start-address field: no carry, addresses < 2^18)
-__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int k) {
-  return sdesc(tile, 16, 1024) + uint64_t(((k >> 2) * kHalf + (k & 3) * 32) >> 4);
-}
-__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int k) {
-  return sdesc(tile, kHalf, 1024) + uint64_t((k * 2048) >> 4);
+// instruction descriptor: bf16 x bf16 -> f32, M = 128
+__host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn, uint32_t n = 128) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
-// instruction descriptor: bf16 x bf16 -> f32, M = N = 128
-__host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((128u >> 3) << 17) |
-         ((128u >> 4) << 24);
-}
-
-// One 128 x 128 x 128 GEMM = 8 UMMAs of K = 16, issued by one elected lane of the
+// One 128 x N x (16 kSteps) GEMM = kSteps UMMAs of K = 16, issued by one elected lane of the
 // converged UMMA warp.  a4 / b4: shared-memory tile start >> 4 (descriptor address field),
 // or for kATmem the TMEM address of A (K = 16 per 8 columns of bf16 pairs).  Descriptor low
 // words are a4/b4 + compile-time constants (no carry: addresses < 2^18); the high word is
 // SBO = 1024 B, version 1, SWIZZLE_128B for both majors.
-template <bool kAMn, bool kBMn, bool kATmem>
+template <int kSteps, bool kAMn, bool kBMn, bool kATmem>
 __device__ __forceinline__ void gemm128(uint32_t d, uint32_t a4, uint32_t b4, uint32_t idesc, bool acc) {
   asm volatile("" : "+r"(a4), "+r"(b4));  // keep the per-k descriptors out of the loop-invariant pool
   constexpr uint64_t kHi = uint64_t(0x40004040u) << 32;
   if (elect_one()) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kSteps; ++k) {
       const uint32_t boff = kBMn ? (k * 2048) >> 4 : (((k >> 2) * kHalf + (k & 3) * 32) >> 4);
       const uint64_t bd = kHi | (b4 + boff + (kBMn ? (uint32_t(kHalf) >> 4) << 16 : 1u << 16));
       const uint32_t en = (acc || k > 0) ? 1u : 0u;
@@ -265,9 +252,16 @@ struct Params {
     if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (it) < 256) p.trace[(e) * 256 + (it)] = clock64(); \
   } while (0)
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, const Params p) {
+  using C = Cfg<D>;
+  constexpr int kTileBytes = C::kTileBytes, kOffK = C::kOffK, kOffV = C::kOffV, kOffQ = C::kOffQ, kOffDO = C::kOffDO,
+                kOffDS = C::kOffDS, kOffStg = C::kOffStg, kOffLse = C::kOffLse, kOffDelta = C::kOffDelta,
+                kOffBar = C::kOffBar, kOffTmemPtr = C::kOffTmemPtr;
+  constexpr uint32_t kColDK = C::kColDK, kColDV = C::kColDV, kColDP = C::kColDP, kColS = C::kColS;
+  constexpr int kDK = D / 16;  // UMMA K-steps over the head dimension
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hd = blockIdx.x, jb = blockIdx.y;
@@ -324,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const int H = p.H;
       mbar_expect_tx(&bars[B_KV], 2 * kTileBytes);
-      for (int half = 0; half < 2; ++half) {
+      for (int half = 0; half < C::kHalves; ++half) {
         tma_load_3d(smem + kOffK + half * kHalf, &tm_qkv, half * 64, H + hd, jb * kTile, &bars[B_KV]);
         tma_load_3d(smem + kOffV + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, jb * kTile, &bars[B_KV]);
       }
@@ -333,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars[B_QE0 + st], ((it >> 1) & 1) ^ 1);
         ATB_TRACE(28, it);
         mbar_expect_tx(&bars[B_QF0 + st], kTileBytes + 1024);
-        for (int half = 0; half < 2; ++half)
+        for (int half = 0; half < C::kHalves; ++half)
           tma_load_3d(smem + kOffQ + st * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd, qb * kTile,
                       &bars[B_QF0 + st]);
         tma_load_1d(s_lse + st * 128, p.lse + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
@@ -341,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars[B_DOE], (it & 1) ^ 1);
         ATB_TRACE(29, it);
         mbar_expect_tx(&bars[B_DOF], kTileBytes);
-        for (int half = 0; half < 2; ++half)
+        for (int half = 0; half < C::kHalves; ++half)
           tma_load_3d(smem + kOffDO + half * kHalf, &tm_do, half * 64, hd, qb * kTile, &bars[B_DOF]);
       }
     }
@@ -352,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t aK = sb4 + (kOffK >> 4), aV = sb4 + (kOffV >> 4), aDO = sb4 + (kOffDO >> 4),
                      aDS = sb4 + (kOffDS >> 4);
       const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tDV = tmem + kColDV, tDK = tmem + kColDK;
-      constexpr uint32_t I_KK = idesc(0, 0), I_KM = idesc(0, 1), I_MM = idesc(1, 1);
+      constexpr uint32_t I_KK = idesc(0, 0), I_KMd = idesc(0, 1, D), I_MMd = idesc(1, 1, D);
       mbar_wait(&bars[B_KV], 0);
       tc_fence_after();
       uint32_t dbg_ph = 0;
@@ -377,12 +371,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int form = 0; form < 6; ++form) {
           const long long t0 = clock64();
           for (int r = 0; r < 16; ++r) {
-            if (form == 0) gemm128<false, false, false>(tS, aK, aQ, I_KK, false);
-            else if (form == 1) gemm128<true, true, false>(tDP, aDS, aK, I_MM, false);
-            else if (form == 2) gemm128<false, true, false>(tDK, aDS, aQ, I_KM, true);
-            else if (form == 3) gemm128<false, true, true>(tDV, tS, aDO, I_KM, true);
-            else if (form == 4) gemm128<false, false, true>(tDV, tS, aDO, I_KK, true);
-            else gemm128<false, false, false>(tDK, aDS, aQ, I_KK, true);
+            if (form == 0) gemm128<kDK, false, false, false>(tS, aK, aQ, I_KK, false);
+            else if (form == 1) gemm128<8, true, true, false>(tDP, aDS, aK, I_MMd, false);
+            else if (form == 2) gemm128<8, false, true, false>(tDK, aDS, aQ, I_KMd, true);
+            else if (form == 3) gemm128<8, false, true, true>(tDV, tS, aDO, I_KMd, true);
+            else if (form == 4) gemm128<kDK, false, false, true>(tDV, tS, aDO, idesc(0, 0, D), true);
+            else gemm128<kDK, false, false, false>(tDK, aDS, aQ, idesc(0, 0, D), true);
           }
           tc_commit(&bars[B_DBG]);
           mbar_wait(&bars[B_DBG], dbg_ph);
@@ -398,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ATB_TRACE(0, it);
           tc_fence_after();
           dbg_start(16, it);
-          gemm128<false, false, false>(tS, aK, aQ, I_KK, false);  // S^T = K Q^T
+          gemm128<kDK, false, false, false>(tS, aK, aQ, I_KK, false);  // S^T = K Q^T
           dbg_done(17, it);
           tc_commit(&bars[B_SF]);
           ATB_TRACE(1, it);
@@ -411,10 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           ATB_TRACE(2, pt);
           tc_fence_after();
           dbg_start(18, pt);
-          gemm128<true, true, false>(tDP, aDS, aK, I_MM, false);  // dQ = dS K
+          gemm128<8, true, true, false>(tDP, aDS, aK, I_MMd, false);  // dQ = dS K
           dbg_done(19, pt);
           tc_commit(&bars[B_DQF]);
-          gemm128<false, true, false>(tDK, aDS, aQp, I_KM, pt > 0);  // dK += dS^T Q
+          gemm128<8, false, true, false>(tDK, aDS, aQp, I_KMd, pt > 0);  // dK += dS^T Q
           dbg_done(23, pt);
           tc_commit(&bars[B_QE0 + (pt & 1)]);
           tc_commit(&bars[B_DSE]);
@@ -428,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ATB_TRACE(5, it);
           tc_fence_after();
           dbg_start(24, it);
-          gemm128<false, false, false>(tDP, aV, aDO, I_KK, false);  // dP^T = V dO^T
+          gemm128<kDK, false, false, false>(tDP, aV, aDO, I_KK, false);  // dP^T = V dO^T
           dbg_done(25, it);
           tc_commit(&bars[B_DPF]);
           ATB_TRACE(6, it);
@@ -436,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ATB_TRACE(7, it);
           tc_fence_after();
           dbg_start(26, it);
-          gemm128<false, true, true>(tDV, tS, aDO, I_KM, it > 0);  // dV += P^T dO
+          gemm128<8, false, true, true>(tDV, tS, aDO, I_KMd, it > 0);  // dV += P^T dO
           dbg_done(27, it);
           tc_commit(&bars[B_DOE]);
           ATB_TRACE(8, it);
@@ -472,17 +466,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float4 l4[16];
 #pragma unroll
         for (int v = 0; v < 16; ++v) l4[v] = reinterpret_cast<const float4*>(lse)[v];
-        // exp2 on packed halves: one MUFU op per two elements (the SFU is the bound of this
-        // phase); |x| < 16 carries >= 7 fractional bits, below the bf16 rounding P gets for
-        // the tensor core anyway
+        // (ex2.approx.f16x2 was measured: sm_100 issues it as two MUFU ops, no gain)
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float* l = reinterpret_cast<const float*>(l4);
-          const float x0 = fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l[c] * 1.4426950408889634f);
-          const float x1 = fmaf(__uint_as_float(r[c >> 5][(c + 1) & 31]), sl2, -l[c + 1] * 1.4426950408889634f);
-          const float2 e = ex2_pair(x0, x1);
-          pr[c] = e.x;
-          pr[c + 1] = e.y;
+        for (int c = 0; c < 64; ++c) {
+          const float l = reinterpret_cast<const float*>(l4)[c];
+          pr[c] = ex2(fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l * 1.4426950408889634f));
         }
       }
       if (it == 0) {  // the diagonal tile: q < kv is masked
@@ -546,17 +534,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- epilogue: dV and scale * dK rows of this kv block into dqkv
     mbar_wait(&bars[B_DKV], 0);
     tc_fence_after();
-    const size_t h = size_t(p.H) * kTile;
-    __nv_bfloat16* out = p.dqkv + (size_t(jb) * kTile + row) * 3 * h + size_t(hd) * kTile + c0;
+    const size_t h = size_t(p.H) * D;
+    constexpr int kHalfD = D / 2;  // columns of dK / dV per warpgroup
+    __nv_bfloat16* out = p.dqkv + (size_t(jb) * kTile + row) * 3 * h + size_t(hd) * D + wg * kHalfD;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {  // 0: dK (scaled), 1: dV
       const uint32_t col = m == 0 ? kColDK : kColDV;
       const float f = m == 0 ? p.scale : 1.f;
       __nv_bfloat16* dst = out + (m == 0 ? h : 2 * h);
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
+      for (int ch = 0; ch < kHalfD / 32; ++ch) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_off + col + c0 + ch * 32, r);
+        tmem_ld32(tmem + lane_off + col + wg * kHalfD + ch * 32, r);
         tmem_wait_ld();
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8) {
@@ -582,16 +571,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       // all 128 columns in registers first: the dQ columns are dP's, and the next dP
       // UMMA waits for this release (B_DQE) on the tensor core's critical path
-      uint32_t r[4][32];
+      constexpr int kCh = D / 32;  // 32-column chunks of the dQ tile
+      uint32_t r[kCh][32];
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) tmem_ld32(tmem + lane_off + kColDP + ch * 32, r[ch]);
+      for (int ch = 0; ch < kCh; ++ch) tmem_ld32(tmem + lane_off + kColDP + ch * 32, r[ch]);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_DQE]);
       if (warp == 0 && lane == 0) ATB_TRACE(21, it);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 0; ch < kCh; ++ch) {
         if (p.exp_mode & 1) break;
         // the reduce that last read this staging buffer has finished reading it
         if (lane == 0) tma_store_wait_read<1>();
@@ -624,14 +614,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // delta[hd, i] = sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), and the fp32 dQ
-// accumulator row i zeroed.  One block per row; 16 lanes per head of 128.
+// accumulator row i zeroed.  One block per row; D/8 lanes per head.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                             const __nv_bfloat16* __restrict__ dout,
                                                             float* __restrict__ delta, float* __restrict__ dq_acc,
-                                                            int s, int H) {
+                                                            int s, int H, int D) {
   pdl_wait();
   const int i = blockIdx.x;
-  const int h = H * kTile;
+  const int h = H * D;
   for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
     const int e = e0 + threadIdx.x * 8;
     const bool ok = e < h;
@@ -643,10 +633,9 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16*
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc = fmaf(a[k], b[k], acc);
     }
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = D / 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (ok) {
-      if ((threadIdx.x & 15) == 0) delta[size_t(e / kTile) * s + i] = acc;
+      if ((threadIdx.x & (D / 8 - 1)) == 0) delta[size_t(e / D) * s + i] = acc;
       float4* z = reinterpret_cast<float4*>(dq_acc + size_t(i) * h + e);
       z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
       z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -689,10 +678,10 @@ static EncodeTiled encoder(int* rc) {
 }
 
 // 3-D map over a row-major [rows][heads][D] view: dims (D, heads, rows), 128-byte swizzle.
-static int make_map(EncodeTiled enc, CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+static int make_map(EncodeTiled enc, CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base, int D,
                     uint64_t heads, uint64_t rows, uint64_t row_stride_bytes, uint32_t box_d, uint32_t box_rows) {
-  cuuint64_t dims[3] = {kTile, heads, rows};
-  cuuint64_t strides[2] = {uint64_t(kTile) * esize, row_stride_bytes};
+  cuuint64_t dims[3] = {uint64_t(D), heads, rows};
+  cuuint64_t strides[2] = {uint64_t(D) * esize, row_stride_bytes};
   cuuint32_t box[3] = {box_d, 1, box_rows};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -702,6 +691,29 @@ static int make_map(EncodeTiled enc, CUtensorMap* m, CUtensorMapDataType dt, int
 }
 
 static long long* g_trace = nullptr;
+
+// The kernel's shared-memory opt-in, once per (device, head_dim).
+template <int D>
+static int smem_optin() {
+  static std::mutex mu;
+  static unsigned done = 0;  // bit per device
+  int dev = 0;
+  PPO_TRY_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 32 && (done >> dev) & 1u) return PPO_OK;
+  PPO_TRY_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes));
+  if (dev < 32) done |= 1u << dev;
+  return PPO_OK;
+}
+
+template <int D>
+static int launch_main(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const Params& prm,
+                       cudaStream_t st) {
+  if (int rc = smem_optin<D>()) return rc;
+  attn_bwd_kernel<D><<<dim3(prm.H, prm.s / kTile), kThreads, Cfg<D>::kSmemBytes, st>>>(a, b, c, prm);
+  PPO_LAUNCHED("attn_bwd_kernel");
+  return PPO_OK;
+}
 
 }  // namespace attnb
 }  // namespace ppo
@@ -724,7 +736,8 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
                  int64_t seq, int64_t heads, int64_t head_dim, float scale, void* stream) {
   if (!qkv || !o || !dout || !lse || !dqkv || !workspace || seq <= 0 || heads <= 0)
     return set_error(PPO_EINVAL, "ppo_attn_bwd: bad arguments");
-  if (head_dim != kTile) return set_error(PPO_ESHAPE, "ppo_attn_bwd: head_dim %lld (compiled for 128)", (long long)head_dim);
+  if (head_dim != 64 && head_dim != 128)
+    return set_error(PPO_ESHAPE, "ppo_attn_bwd: head_dim %lld (compiled for 64, 128)", (long long)head_dim);
   if (seq % kTile != 0 || seq >= (1ll << 30) || heads * head_dim * 3 >= (1ll << 31))
     return set_error(PPO_ESHAPE, "ppo_attn_bwd: seq %lld must be a multiple of 128", (long long)seq);
   if (!aligned16(qkv) || !aligned16(o) || !aligned16(dout) || !aligned16(lse) || !aligned16(dqkv) ||
@@ -739,29 +752,24 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   float* dq_acc = static_cast<float*>(workspace);
   float* delta = dq_acc + size_t(s) * h;
 
+  const int D = int(head_dim);
   CUtensorMap tm_qkv, tm_do, tm_dq;
-  if ((rc = make_map(enc, &tm_qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, 3 * heads, seq, 3 * h * 2, 64, kTile)))
+  if ((rc = make_map(enc, &tm_qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * heads, seq, 3 * h * 2, 64, kTile)))
     return rc;
-  if ((rc = make_map(enc, &tm_do, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, heads, seq, h * 2, 64, kTile))) return rc;
-  if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, heads, seq, h * 4, 32, 32))) return rc;
-
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return cuda_error(attr_err, "ppo_attn_bwd: smem attribute");
+  if ((rc = make_map(enc, &tm_do, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, D, heads, seq, h * 2, 64, kTile)))
+    return rc;
+  if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, D, heads, seq, h * 4, 32, 32))) return rc;
 
   launch_pdl(attn_bwd_prep_kernel, dim3(s), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
-             static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, s, H);
+             static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, s, H, D);
   PPO_LAUNCHED("attn_bwd_prep_kernel");
   static const int exp_mode = [] {
     const char* e = std::getenv("PPO_ATB_EXP");
     return e ? std::atoi(e) : 0;
   }();
   Params prm{static_cast<__nv_bfloat16*>(dqkv), lse, delta, dq_acc, s, H, scale, g_trace, exp_mode};
-  attn_bwd_kernel<<<dim3(H, s / kTile), kThreads, kSmemBytes, st>>>(tm_qkv, tm_do, tm_dq, prm);
-  PPO_LAUNCHED("attn_bwd_kernel");
+  rc = D == 64 ? launch_main<64>(tm_qkv, tm_do, tm_dq, prm, st) : launch_main<128>(tm_qkv, tm_do, tm_dq, prm, st);
+  if (rc) return rc;
   const int sms = sm_count_current();
   launch_pdl(attn_bwd_dq_kernel, dim3(sms * 4), dim3(256), 0, st, static_cast<const float*>(dq_acc),
              static_cast<__nv_bfloat16*>(dqkv), s, int(h), scale);

@@ -48,9 +48,9 @@ def _run_ours(qkv, o, do, lse, heads):
     return dqkv
 
 
-@pytest.mark.parametrize("s,heads", [(128, 1), (256, 2), (512, 4), (1024, 2), (2048, 3)])
-def test_attn_bwd_matches_fp32(s, heads):
-    D = 128
+@pytest.mark.parametrize("s,heads,D", [(128, 1, 128), (256, 2, 128), (512, 4, 128), (1024, 2, 128), (2048, 3, 128),
+                                       (128, 2, 64), (256, 4, 64), (512, 4, 64), (1024, 3, 64)])
+def test_attn_bwd_matches_fp32(s, heads, D):
     h = heads * D
     g = torch.Generator(device=DEV).manual_seed(11 * s + heads)
     qkv = torch.randn(s, 3 * h, device=DEV, generator=g).bfloat16()
@@ -101,7 +101,7 @@ def test_attn_bwd_rejects_bad_shapes():
     ws = torch.empty(native.attn_bwd_workspace_bytes(256, heads, 128), device=DEV, dtype=torch.uint8)
     with pytest.raises(native.PpoError):
         native.attn_bwd(qkv, o, o, torch.zeros(heads, 200, device=DEV), torch.empty_like(qkv), heads, ws)
-    qkv = torch.zeros(256, 3 * 128, device=DEV, dtype=torch.bfloat16)  # head_dim 64
-    o = torch.zeros(256, 128, device=DEV, dtype=torch.bfloat16)
+    qkv = torch.zeros(256, 3 * 192, device=DEV, dtype=torch.bfloat16)  # head_dim 96
+    o = torch.zeros(256, 192, device=DEV, dtype=torch.bfloat16)
     with pytest.raises(native.PpoError):
         native.attn_bwd(qkv, o, o, torch.zeros(heads, 256, device=DEV), torch.empty_like(qkv), heads, ws)
