@@ -286,13 +286,15 @@ def _graph_time_us(fn_sets, dev, torch, launches=16):
 
 
 GEMM_NAMES = {"ppo_gemm_tn": "gemm_tn", "ppo_gemm_tn_gelu": "gemm_tn_gelu", "ppo_gemm_nn": "gemm_nn",
-              "ppo_gemm_nn_dgelu": "gemm_nn_dgelu", "ppo_gemm_wgrad": "gemm_wgrad", "ppo_attn_fwd": "attn_fwd"}
+              "ppo_gemm_nn_dgelu": "gemm_nn_dgelu", "ppo_gemm_wgrad": "gemm_wgrad", "ppo_attn_fwd": "attn_fwd",
+              "ppo_attn_bwd": "attn_bwd"}
 
 
 def measure_gemms(shapes, dev, torch, native, sets=2):
     """Device time per launch of each tcgen05 GEMM (entry, M, N, K) and attention forward
-    (entry, s, heads, head_dim) the step ran.  Attention FLOPs are causal-effective:
-    QK^T and PV over the lower triangle, 2 * 2 * s^2/2 * head_dim per head = 2 s^2 h."""
+    and backward (entry, s, heads, head_dim) the step ran.  Attention FLOPs are
+    causal-effective: forward QK^T and PV over the lower triangle, 2 * 2 * s^2/2 * head_dim
+    per head = 2 s^2 h; backward (K7b) five such GEMMs (S, dP, dV, dK, dQ) = 5 s^2 h."""
     bf = dict(device=dev, dtype=torch.bfloat16)
     out = {}
     for (entry, M, N, K) in sorted(shapes):
@@ -318,10 +320,18 @@ def measure_gemms(shapes, dev, torch, native, sets=2):
                 qkv, o = torch.randn(M, 3 * N * K, **bf), torch.empty(M, N * K, **bf)
                 lse = torch.empty(N, M, device=dev)
                 fns.append(lambda qkv=qkv, o=o, lse=lse, H=N: native.attn_fwd(qkv, o, lse, H))
+            elif entry == "ppo_attn_bwd":  # (s, heads, head_dim): saved o / lse from the forward
+                qkv, o, do = torch.randn(M, 3 * N * K, **bf), torch.empty(M, N * K, **bf), torch.randn(M, N * K, **bf)
+                lse, dqkv = torch.empty(N, M, device=dev), torch.empty(M, 3 * N * K, **bf)
+                wsb = torch.empty(native.attn_bwd_workspace_bytes(M, N, K), device=dev, dtype=torch.uint8)
+                native.attn_fwd(qkv, o, lse, N)
+                fns.append(lambda qkv=qkv, o=o, do=do, lse=lse, dqkv=dqkv, wsb=wsb, H=N:
+                           native.attn_bwd(qkv, o, do, lse, dqkv, H, wsb))
         if not fns:
             continue
         name = f"{GEMM_NAMES[entry]}_{M}x{N}x{K}"
-        flops = 2 * M * M * N * K if entry == "ppo_attn_fwd" else 2 * M * N * K
+        flops = (2 * M * M * N * K if entry == "ppo_attn_fwd" else 5 * M * M * N * K if entry == "ppo_attn_bwd"
+                 else 2 * M * N * K)
         out[name] = {"entry": entry, "shape": (M, N, K), "flops_per_launch": flops,
                      "avg_us": _graph_time_us(fns, dev, torch)}
         del fns
@@ -803,8 +813,9 @@ def run_b200(args, rank, world, local_rank):
                          else "cuBLAS (faster end to end than gemm=auto by > 1% in this run)",
                          "per_shape": gemm_decisions(),
                          "table_digest_per_rank": table_digests, "misses": sorted(gemm_tune.MISSES)},
-        "attn_backend": {"policies": "attention forward: tcgen05 (ours) or cuDNN + K1 pack, measured per shape "
-                                     "(attn=auto); backward: cuDNN", "per_shape": attn_decisions()},
+        "attn_backend": {"policies": "attention forward: tcgen05 (ours) or cuDNN + K1 pack; backward: tcgen05 "
+                                     "K7b (ours) or cuDNN + K1 gather; each measured per shape (attn=auto)",
+                         "per_shape": attn_decisions()},
         "clocks": clocks,
         "roofline": roofline,
         "kernels": {k: {"bound": v["bound"], "avg_us": round(v["avg_us"], 2), "achieved": round(v["achieved"], 1),
@@ -822,7 +833,7 @@ def run_b200(args, rank, world, local_rank):
             "dma_slowdown": cal.get("dma_slowdown"),
             "slab_bytes": slab_bytes,
             "no_offload": none, "no_offload_auto_gemms": results["none"], "no_offload_cublas_gemms": none_cublas,
-            "no_offload_tcgen05_attention_fwd": results.get("none_tcgen05_attn"),
+            "no_offload_tcgen05_attention": results.get("none_tcgen05_attn"),
             "full": full, "auto": auto,
             "full_single_stream": single, "full_duplex_plan": duplex,
             "auto_stride": choice.stride, "auto_modelled_overhead": choice.overhead,
@@ -875,7 +886,7 @@ def run_b200(args, rank, world, local_rank):
 def attn_decisions():
     from paper_2503_01328_b200.runtime import gemm_tune
 
-    return {k: v for k, v in gemm_tune.decisions().items() if k.startswith("attn_fwd")}
+    return {k: v for k, v in gemm_tune.decisions().items() if k.startswith("attn_")}
 
 
 def gemm_decisions():
@@ -883,7 +894,7 @@ def gemm_decisions():
     the gemm="auto" tuner (runtime/gemm_tune.py), and the backend it picked."""
     from paper_2503_01328_b200.runtime import gemm_tune
 
-    return {k: v for k, v in gemm_tune.decisions().items() if not k.startswith("attn_fwd")}
+    return {k: v for k, v in gemm_tune.decisions().items() if not k.startswith("attn_")}
 
 
 def cpu_baseline(args):

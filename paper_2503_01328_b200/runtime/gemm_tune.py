@@ -5,7 +5,9 @@ Each layer GEMM of a stage has two implementations: libppo_b200's tcgen05 kernel
 fp32-accumulate epilogues) and cuBLAS (nvjet) plus, where ours fuses an epilogue,
 the separate libppo_b200 GeLU kernel.  Which is faster depends on the shape
 (profiles/r1_gemm_tuning.txt).  The attention forward has libppo_b200's tcgen05
-kernel (o and lse straight into the slab) and cuDNN's fused kernel + K1 pack.
+kernel (o and lse straight into the slab) and cuDNN's fused kernel + K1 pack; the
+attention backward has libppo_b200's K7b (dqkv [s, 3h] directly) and cuDNN's fused
+backward + the K1 gather into dqkv.
 
 Numerics follow the backend, so the choice must be the same in every process that
 is compared or pipelined together.  The contract:
@@ -51,6 +53,10 @@ def gemm_key(kind: str, shape) -> str:
 
 def attn_key(seq: int, heads: int, head_dim: int) -> str:
     return f"attn_fwd {seq}x{heads}x{head_dim}"
+
+
+def attn_bwd_key(seq: int, heads: int, head_dim: int) -> str:
+    return f"attn_bwd {seq}x{heads}x{head_dim}"
 
 
 def layer_gemm_shapes(seq: int, hidden: int) -> list[tuple]:
@@ -103,6 +109,16 @@ def attn_choice(seq: int, heads: int, head_dim: int) -> bool:
     d = TABLE.get(attn_key(seq, heads, head_dim))
     if d is None:
         MISSES.add(attn_key(seq, heads, head_dim))
+        return False
+    return d["backend"] == "tcgen05"
+
+
+def attn_bwd_choice(seq: int, heads: int, head_dim: int) -> bool:
+    """True if libppo_b200's attention backward (K7b) runs this shape under ``attn="auto"``."""
+    _env_table()
+    d = TABLE.get(attn_bwd_key(seq, heads, head_dim))
+    if d is None:
+        MISSES.add(attn_bwd_key(seq, heads, head_dim))
         return False
     return d["backend"] == "tcgen05"
 
@@ -193,6 +209,33 @@ def attn_candidates(seq: int, heads: int, head_dim: int, device):
     return (lambda: native.attn_fwd(qkv, o, lse, heads)), cudnn
 
 
+def attn_bwd_candidates(seq: int, heads: int, head_dim: int, device):
+    """(run_ours, run_cudnn_plus_gather): the backward of one layer's attention into the
+    packed dqkv [s, 3h] both ways (cuDNN's three gradients gathered by one K1 launch, as
+    the split backward does), from the same saved o / lse."""
+    from . import native
+
+    h = heads * head_dim
+    qkv, do = _rand(device, seq, 3 * h), _rand(device, seq, h)
+    qv = qkv.view(1, seq, 3, heads, head_dim)
+    q, k, v = (qv[:, :, i].transpose(1, 2) for i in range(3))
+    r = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+    o4, lse4 = r[0], r[1]
+    o = o4.transpose(1, 2).reshape(seq, h).contiguous()
+    lse = lse4.reshape(heads, seq).contiguous()
+    do4 = do.view(1, seq, heads, head_dim).transpose(1, 2)
+    dqkv = torch.empty_like(qkv)
+    ws = torch.empty(native.attn_bwd_workspace_bytes(seq, heads, head_dim), device=device, dtype=torch.uint8)
+
+    def cudnn():
+        g = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
+            do4, q, k, v, o4, lse4, r[6], r[7], None, r[2], r[3], r[4], r[5], 0.0, True)
+        parts = [t.transpose(1, 2) for t in g]
+        native.pack([(p_, 2 * h * j, seq, 2 * h, 2 * h, 6 * h) for j, p_ in enumerate(parts)], dqkv)
+
+    return (lambda: native.attn_bwd(qkv, o, do, lse, dqkv, heads, ws)), cudnn
+
+
 def _duel(ours, lib, stream) -> tuple[float, float]:
     est = max(_time_us(ours, stream), _time_us(lib, stream))
     n = int(min(50, max(3, 10_000 / max(est, 1.0))))
@@ -222,8 +265,8 @@ def tune_gemm(kind: str, shape, device, stream) -> dict:
             "ours_us": round(t_ours, 2), "lib_us": round(t_lib, 2)}
 
 
-def tune_attn(seq, heads, head_dim, device, stream) -> dict:
-    ours, lib = attn_candidates(seq, heads, head_dim, device)
+def tune_attn(seq, heads, head_dim, device, stream, backward: bool = False) -> dict:
+    ours, lib = (attn_bwd_candidates if backward else attn_candidates)(seq, heads, head_dim, device)
     t_ours, t_lib = _duel(ours, lib, stream)
     return {"backend": "tcgen05" if t_ours <= t_lib else "cudnn", "ours_us": round(t_ours, 2),
             "lib_us": round(t_lib, 2)}
@@ -239,6 +282,8 @@ def needed_keys(cfg, gemm: str = "auto", attn: str = "auto") -> list[tuple[str, 
         out += [(gemm_key(k, sh), ("gemm", k, sh)) for (k, *sh) in layer_gemm_shapes(cfg.seq, cfg.hidden)]
     if attn == "auto" and cfg.head_dim in (64, 128) and cfg.seq % 256 == 0:
         out.append((attn_key(cfg.seq, cfg.heads, cfg.head_dim), ("attn", cfg.seq, cfg.heads, cfg.head_dim)))
+    if attn == "auto" and cfg.head_dim in (64, 128) and cfg.seq % 128 == 0:
+        out.append((attn_bwd_key(cfg.seq, cfg.heads, cfg.head_dim), ("attn_bwd", cfg.seq, cfg.heads, cfg.head_dim)))
     return out
 
 
@@ -249,7 +294,7 @@ def install(entries: dict) -> None:
     for key, d in entries.items():
         TABLE[key] = dict(d)
         kind, shape = key.split(" ", 1)
-        if kind != "attn_fwd" and d.get("swizzle"):
+        if not kind.startswith("attn") and d.get("swizzle"):
             M, N, K = (int(x) for x in shape.split("x"))
             native.gemm_set_swizzle(kind, M, N, K, int(d["swizzle"]))
 
@@ -286,7 +331,7 @@ def ensure(cfg, device, gemm: str = "auto", attn: str = "auto") -> dict:
             with torch.cuda.device(dev), torch.cuda.stream(stream):
                 for k, spec in missing:
                     TABLE[k] = (tune_gemm(spec[1], spec[2], dev, stream) if spec[0] == "gemm"
-                                else tune_attn(*spec[1:], dev, stream))
+                                else tune_attn(*spec[1:], dev, stream, backward=spec[0] == "attn_bwd"))
             stream.synchronize()
             torch.cuda.empty_cache()
     mine = {k: TABLE[k] for k, _ in keys if k in TABLE}

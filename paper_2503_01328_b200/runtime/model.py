@@ -144,16 +144,19 @@ class Stage:
             raise ValueError(f"gemm backend {gemm!r}")
         if attn not in ("auto", "tcgen05", "cudnn"):
             raise ValueError(f"attention backend {attn!r}")
-        # attention forward: "tcgen05" = libppo_b200's kernel writing o and lse straight into
-        # the slab (head_dim 64/128, seq % 256 == 0); "cudnn" = cuDNN's fused kernel + K1 pack
-        # (the library baseline); "auto" = whichever measured faster at this shape
-        # (gemm_tune.prefer_ours_attn, decided in _attn_init).  The backward is cuDNN's fused
-        # kernel in every case, fed the saved o and lse.
+        # attention: "tcgen05" = libppo_b200's kernels -- the forward writing o and lse straight
+        # into the slab (head_dim 64/128, seq % 256 == 0) and the backward (K7b) writing
+        # dqkv [s, 3h] for one dgrad and one wgrad GEMM; "cudnn" = cuDNN's fused kernels + K1
+        # pack / gather (the library baseline); "auto" = per direction, whichever measured
+        # faster at this shape (gemm_tune decision table, looked up in _attn_init).  Both
+        # backward kernels consume the same saved o and natural-log lse.
         self.attn_supported = cfg.head_dim in (64, 128) and cfg.seq % 256 == 0
+        self.attn_bwd_supported = cfg.head_dim in (64, 128) and cfg.seq % 128 == 0
         if attn == "tcgen05" and not self.attn_supported:
             raise ValueError(f"tcgen05 attention needs head_dim 64/128 and seq % 256 == 0 (got {cfg.head_dim}, {cfg.seq})")
         self.attn_mode = attn
         self.attn_ours = attn == "tcgen05"
+        self.attn_bwd_ours = attn == "tcgen05"
         # "tcgen05": every GEMM on libppo_b200's kernels (fused GeLU epilogues); "cublas": the
         # library baseline; "best": ours except narrow-N / deep-K shapes (N <= 2048, K >= 3N)
         # where cuBLAS nvjet measured ~7% faster (profiles/r1_gemm_tuning.txt).
@@ -235,6 +238,11 @@ class Stage:
             native.attn_fwd(qkv, ws["a"], lse, cfg.heads)  # creates the library's per-seq constants
             if self.attn_mode == "auto":
                 self.attn_ours = gemm_tune.attn_choice(s, cfg.heads, cfg.head_dim)
+        if self.attn_mode == "auto" and self.attn_bwd_supported:
+            self.attn_bwd_ours = gemm_tune.attn_bwd_choice(s, cfg.heads, cfg.head_dim)
+        if self.attn_bwd_ours and "attn" not in ws:  # fp32 dq accumulator + row statistics
+            ws["attn"] = torch.empty(native.attn_bwd_workspace_bytes(s, cfg.heads, cfg.head_dim), device=self.device,
+                                     dtype=torch.uint8)
         del res
 
     def _k(self, name: str, nbytes: int, fn, *args, **kw):
@@ -497,22 +505,28 @@ class Stage:
             if not split:
                 self.wgrad(self.gp(l, "w_proj"), da, o)
             self.mm_dgrad(da, self.p(l, "w_proj"), ws["t"])
-            q, k, v = self._qkv_views(qkv)
-            o4 = o.view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
-            do4 = ws["t"].view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
-            lse3 = lse.view(self._lse_shape)
-            cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
-            dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
-                do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
             grads = None
-            if split:
-                self._gather_dqkv(dq, dk, dv, dqkv)  # the W pass needs them after cuDNN's buffers are reused
+            if self.attn_bwd_ours:  # K7b: dqkv [s, 3h] straight from the saved o and lse
+                native.attn_bwd(qkv, o, ws["t"], lse, dqkv, cfg.heads, ws["attn"])
                 self.mm_dgrad(dqkv, self.p(l, "w_qkv"), ws["t"])
+                if not split:
+                    grads = [dqkv]
             else:
-                grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
-                w_qkv = self.p(l, "w_qkv")
-                for j, gj in enumerate(grads):
-                    self.mm_dgrad(gj, w_qkv[j * h:(j + 1) * h], ws["t"], accumulate=j > 0)
+                q, k, v = self._qkv_views(qkv)
+                o4 = o.view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
+                do4 = ws["t"].view(1, s, cfg.heads, cfg.head_dim).transpose(1, 2)
+                lse3 = lse.view(self._lse_shape)
+                cq, ck, mq, mk, ps, po = self._attn_meta[0], self._attn_meta[1], self._attn_meta[2], self._attn_meta[3], self._attn_meta[4], self._attn_meta[5]
+                dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
+                    do4, q, k, v, o4, lse3, ps, po, None, cq, ck, mq, mk, 0.0, True)
+                if split:
+                    self._gather_dqkv(dq, dk, dv, dqkv)  # the W pass needs them after cuDNN's buffers are reused
+                    self.mm_dgrad(dqkv, self.p(l, "w_qkv"), ws["t"])
+                else:
+                    grads = [t.transpose(1, 2).reshape(s, h) for t in (dq, dk, dv)]
+                    w_qkv = self.p(l, "w_qkv")
+                    for j, gj in enumerate(grads):
+                        self.mm_dgrad(gj, w_qkv[j * h:(j + 1) * h], ws["t"], accumulate=j > 0)
             # dx = dh1 + LN1_bwd(dln1); also the next-lower layer's MLP-branch dropout replay;
             # unsplit: the same kernel emits the LN1 recompute ln = LN1(x) for dWqkv
             below = i > 0
@@ -525,8 +539,11 @@ class Stage:
                                  beta=None if split else self.p(l, "ln1_b"), ln_out=None if split else ws["ln"])
             if grads is not None:
                 g_qkv = self.gp(l, "w_qkv")
-                for j, gj in enumerate(grads):
-                    self.wgrad(g_qkv[j * h:(j + 1) * h], gj, ws["ln"])
+                if len(grads) == 1:  # packed dqkv: one weight-gradient GEMM (3h x h)
+                    self.wgrad(g_qkv, grads[0], ws["ln"])
+                else:
+                    for j, gj in enumerate(grads):
+                        self.wgrad(g_qkv[j * h:(j + 1) * h], gj, ws["ln"])
             dy_cur = dx_target
         if self.first:
             native.embed_bwd(self.tok[:-1], dy_cur, self.g["wte"], self.g["wpe"])
