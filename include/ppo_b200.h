@@ -254,7 +254,7 @@ int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t head
  * and wgrad GEMMs.  head_dim 128, seq a multiple of 128.  Hand-written tcgen05 kernel:
  * one CTA per (128-row kv block, head), five 128^3 UMMAs per tile with S, dP, dK, dV in
  * TMEM, dQ through TMA bulk reduce-add into the fp32 workspace
- * (ppo_attn_bwd_workspace_bytes: dq accumulator s*h + row statistics heads*s, fp32).
+ * (ppo_attn_bwd_workspace_bytes: dq accumulator s*h + two row statistics heads*s, fp32).
  * dq is accumulated in an unspecified order (fp32 reduce-add), dk and dv are not. */
 int64_t ppo_attn_bwd_workspace_bytes(int64_t seq, int64_t heads, int64_t head_dim);
 int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv, void* workspace,

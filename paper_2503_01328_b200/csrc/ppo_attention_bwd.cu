@@ -20,6 +20,10 @@
 //   dK  += dS^T Q_i            A = dS^T smem K-major B = Q  smem MN-major  -> TMEM dK
 //   dQ_i = dS K_j              A = dS smem MN-major  B = K  smem MN-major  -> TMEM dQ (= dP cols)
 //
+// Issue order per step i (one thread): S(i); dK(i-1), dQ(i-1) once dS(i-1) is in shared
+// memory; dP(i) once the drain warps hold dQ(i-1); dV(i) once P(i) is in TMEM.  The
+// softmax-gradient warps of step i overlap the tensor core's dK/dQ of step i-1.
+//
 // Every operand tile is loaded once by TMA in the 128-byte-swizzled layout and read by
 // the tensor core both K-major and MN-major (the swizzle atom of 8 rows x 128 B is the
 // same physical arrangement for both), so Q, dO and K feed two UMMAs each without a
@@ -237,7 +241,7 @@ __device__ __forceinline__ void gemm128(uint32_t d, uint32_t a4, uint32_t b4, ui
 
 struct Params {
   __nv_bfloat16* dqkv;
-  const float* lse;  // [H, s] natural log
+  const float* lse2;   // [H, s] log2(e) * logsumexp
   const float* delta;  // [H, s]
   float* dq_acc;       // [s, h] fp32
   int s, H;
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int half = 0; half < C::kHalves; ++half)
           tma_load_3d(smem + kOffQ + st * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd, qb * kTile,
                       &bars[B_QF0 + st]);
-        tma_load_1d(s_lse + st * 128, p.lse + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
+        tma_load_1d(s_lse + st * 128, p.lse2 + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
         tma_load_1d(s_delta + st * 128, p.delta + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
         mbar_wait(&bars[B_DOE], (it & 1) ^ 1);
         ATB_TRACE(29, it);
@@ -404,13 +408,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars[B_DSF], pt & 1);
           ATB_TRACE(2, pt);
           tc_fence_after();
+          // dK first: its Q stage goes back to the producer one GEMM earlier (measured:
+          // period 3839 vs 4128 clocks per step at C2, the Q load latency is ~2000 clocks)
           dbg_start(18, pt);
-          gemm128<8, true, true, false>(tDP, aDS, aK, I_MMd, false);  // dQ = dS K
-          dbg_done(19, pt);
-          tc_commit(&bars[B_DQF]);
           gemm128<8, false, true, false>(tDK, aDS, aQp, I_KMd, pt > 0);  // dK += dS^T Q
-          dbg_done(23, pt);
+          dbg_done(19, pt);
           tc_commit(&bars[B_QE0 + (pt & 1)]);
+          gemm128<8, true, true, false>(tDP, aDS, aK, I_MMd, false);  // dQ = dS K
+          dbg_done(23, pt);
+          tc_commit(&bars[B_DQF]);
           tc_commit(&bars[B_DSE]);
           ATB_TRACE(3, pt);
           if (it == n_it) tc_commit(&bars[B_DKV]);
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           const float l = reinterpret_cast<const float*>(l4)[c];
-          pr[c] = ex2(fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l * 1.4426950408889634f));
+          pr[c] = ex2(fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l));  // s_lse holds log2(e) * lse
         }
       }
       if (it == 0) {  // the diagonal tile: q < kv is masked
@@ -613,15 +619,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// delta[hd, i] = sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), and the fp32 dQ
-// accumulator row i zeroed.  One block per row; D/8 lanes per head.
+// delta[hd, i] = sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), lse2 = log2(e) * lse,
+// and the fp32 dQ accumulator row i zeroed.  One block per row; D/8 lanes per head.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                             const __nv_bfloat16* __restrict__ dout,
+                                                            const float* __restrict__ lse, float* __restrict__ lse2,
                                                             float* __restrict__ delta, float* __restrict__ dq_acc,
                                                             int s, int H, int D) {
   pdl_wait();
   const int i = blockIdx.x;
   const int h = H * D;
+  for (int t = threadIdx.x; t < H; t += blockDim.x) lse2[size_t(t) * s + i] = lse[size_t(t) * s + i] * 1.4426950408889634f;
   for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
     const int e = e0 + threadIdx.x * 8;
     const bool ok = e < h;
@@ -729,7 +737,7 @@ int ppo_attn_bwd_trace(void* trace) {
 }
 
 int64_t ppo_attn_bwd_workspace_bytes(int64_t seq, int64_t heads, int64_t head_dim) {
-  return (seq * heads * head_dim + heads * seq) * int64_t(sizeof(float));
+  return (seq * heads * head_dim + 2 * heads * seq) * int64_t(sizeof(float));
 }
 
 int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv, void* workspace,
@@ -751,6 +759,7 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   if (rc) return rc;
   float* dq_acc = static_cast<float*>(workspace);
   float* delta = dq_acc + size_t(s) * h;
+  float* lse2 = delta + size_t(H) * s;
 
   const int D = int(head_dim);
   CUtensorMap tm_qkv, tm_do, tm_dq;
@@ -761,13 +770,13 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, D, heads, seq, h * 4, 32, 32))) return rc;
 
   launch_pdl(attn_bwd_prep_kernel, dim3(s), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
-             static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, s, H, D);
+             static_cast<const __nv_bfloat16*>(dout), lse, lse2, delta, dq_acc, s, H, D);
   PPO_LAUNCHED("attn_bwd_prep_kernel");
   static const int exp_mode = [] {
     const char* e = std::getenv("PPO_ATB_EXP");
     return e ? std::atoi(e) : 0;
   }();
-  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse, delta, dq_acc, s, H, scale, g_trace, exp_mode};
+  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse2, delta, dq_acc, s, H, scale, g_trace, exp_mode};
   rc = D == 64 ? launch_main<64>(tm_qkv, tm_do, tm_dq, prm, st) : launch_main<128>(tm_qkv, tm_do, tm_dq, prm, st);
   if (rc) return rc;
   const int sms = sm_count_current();

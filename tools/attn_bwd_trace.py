@@ -66,7 +66,7 @@ def main():
         waits["q_tma_latency"].append(ev["m_qf"][i] - ev["p_qe"][i])
         waits["do_tma_latency"].append(ev["m_dof"][i] - ev["p_doe"][i])
     if "g_S1" in ev and ev["g_S1"][1] > 0:  # PPO_ATB_EXP bit 2: each GEMM serialised and timed
-        for name, a0, a1 in (("S", "g_S0", "g_S1"), ("dQ", "g_dQ0", "g_dQ1"), ("dK", "g_dQ1", "g_dK1"),
+        for name, a0, a1 in (("S", "g_S0", "g_S1"), ("dK", "g_dQ0", "g_dQ1"), ("dQ", "g_dQ1", "g_dK1"),
                              ("dP", "g_dP0", "g_dP1"), ("dV", "g_dV0", "g_dV1")):
             d = [ev[a1][i] - ev[a0][i] for i in range(1, n - 1)]
             waits["gemm_" + name] = d
