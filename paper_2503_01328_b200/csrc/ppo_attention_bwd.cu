@@ -184,6 +184,19 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (x <= 0): round-to-nearest split through the 1.5 * 2^23 shifter,
+// degree-3 fit of 2^f on [-1/2, 1/2] (max relative error 1.4e-4, far below the bf16
+// rounding P gets for the tensor core), exponent added as an integer.  A share of the
+// softmax exponentials runs here so the SFU (16 results per clock per SM) stops being
+// the bound of the P phase.
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float j = x + 12582912.f;
+  const float f = x - (j - 12582912.f);
+  const float q = fmaf(fmaf(fmaf(0.0550292665f, f, 0.242256982f), f, 0.693253055f), f, 0.999951339f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(j) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return reinterpret_cast<uint32_t&>(v);
@@ -266,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 kOffBar = C::kOffBar, kOffTmemPtr = C::kOffTmemPtr;
   constexpr uint32_t kColDK = C::kColDK, kColDV = C::kColDV, kColDP = C::kColDP, kColS = C::kColS;
   constexpr int kDK = D / 16;  // UMMA K-steps over the head dimension
+  constexpr int kPolyPer8 = 3;  // exponentials per 8 on the FMA pipe (ex2_fma), the rest on the SFU
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hd = blockIdx.x, jb = blockIdx.y;
@@ -476,7 +490,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           const float l = reinterpret_cast<const float*>(l4)[c];
-          pr[c] = ex2(fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l));  // s_lse holds log2(e) * lse
+          const float x = fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l);  // s_lse holds log2(e) * lse
+          pr[c] = (c & 7) < kPolyPer8 ? ex2_fma(x) : ex2(x);
         }
       }
       if (it == 0) {  // the diagonal tile: q < kv is masked
