@@ -22,7 +22,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libppo_b200.so")
 SOURCES = ["ppo_runtime.cu", "ppo_kernels.cu", "ppo_layernorm.cu", "ppo_comm.cu", "ppo_gemm_fwd.cu", "ppo_gemm_bwd.cu", "ppo_gemm_wgrad.cu",
-           "ppo_attention.cu", "ppo_attention_bwd.cu"]
+           "ppo_attention.cu", "ppo_attention_bwd.cu", "ppo_attention_fwd.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -21,6 +21,7 @@
 
 #include <cute/tensor.hpp>
 #include <cstdlib>
+#include <string>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -192,6 +193,19 @@ __global__ void __launch_bounds__(256) lse_log2_to_ln_kernel(float* __restrict__
 }
 
 }  // namespace attn
+
+int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, float scale, cudaStream_t st);
+
+// PPO_ATTN_FWD=cutlass selects the CUTLASS-collective kernel above (A/B experiments);
+// default: the hand-written kernel of ppo_attention_fwd.cu.
+static bool use_cutlass_fwd() {
+  static const bool v = [] {
+    const char* e = std::getenv("PPO_ATTN_FWD");
+    return e && std::string(e) == "cutlass";
+  }();
+  return v;
+}
+
 }  // namespace ppo
 
 using namespace ppo;
@@ -210,6 +224,7 @@ int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t head
   cudaStream_t st = as_stream(stream);
   int rc = PPO_OK;
   int s = int(seq), H = int(heads), D = int(head_dim);
+  if (!use_cutlass_fwd()) return attn_fwd_tcgen05(qkv, o, lse, s, H, D, scale, st);
   int* offs = segment_offsets(s, st, &rc);
   if (rc) return rc;
 

@@ -28,7 +28,9 @@
 // the tensor core both K-major and MN-major (the swizzle atom of 8 rows x 128 B is the
 // same physical arrangement for both), so Q, dO and K feed two UMMAs each without a
 // transpose.  dQ partials leave through TMA bulk reduce-add (cp.reduce.async.bulk.tensor
-// .add.f32) into an fp32 accumulator; a small kernel scales and casts it into dqkv.
+// .add.f32) into an fp32 accumulator; a small kernel scales and casts it into dqkv (a
+// fused cast by the last contributor per block was measured: waiting for the reduce-adds
+// to complete takes ~20000 clocks, the cast stays a kernel of its own).
 //
 // Warp roles (512 threads): warps 0-3 drain dQ from TMEM into the reduce-add, warps 4-11
 // (two warpgroups, q columns 0-63 / 64-127) compute P = exp2(S*scale*log2e - lse*log2e)
@@ -42,12 +44,14 @@
 #include <mutex>
 
 #include "ppo_common.cuh"
+#include "ppo_tcgen05.cuh"
 
 namespace ppo {
 namespace attnb {
 
+using namespace ppo::tc;
+
 constexpr int kTile = 128;           // kv rows per CTA, q rows per step
-constexpr int kHalf = 128 * 64 * 2;  // one 128-row x 64-column bf16 TMA box (16 KB)
 constexpr int kStgBytes = 32 * 32 * 4;
 
 // Per head_dim D (64 or 128): tiles of 128 rows x D are D/64 boxes of 64 columns.
@@ -93,164 +97,6 @@ enum : int {
 };
 
 constexpr int kThreads = 512;  // warps 14, 15 idle: setmaxnreg works per warpgroup
-
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// one lane of a converged warp (the UMMA warp runs converged so its operands stay uniform)
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, 0xffffffff;\n@px mov.s32 %0, 1;\n}\n"
-      : "+r"(pred));
-  return pred != 0;
-}
-
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  if (elect_one())
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-// D[tmem] (+)= A[smem] * B[smem]
-__device__ __forceinline__ void umma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  if (elect_one())
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-// D[tmem] (+)= A[tmem] * B[smem]
-__device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  if (elect_one())
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
-      "r"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-// 32 lanes x 32 consecutive 32-bit columns; thread t gets lane (base lane + t).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
-  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// 2^x on the FMA pipe (x <= 0): round-to-nearest split through the 1.5 * 2^23 shifter,
-// degree-3 fit of 2^f on [-1/2, 1/2] (max relative error 1.4e-4, far below the bf16
-// rounding P gets for the tensor core), exponent added as an integer.  A share of the
-// softmax exponentials runs here so the SFU (16 results per clock per SM) stops being
-// the bound of the P phase.
-__device__ __forceinline__ float ex2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float j = x + 12582912.f;
-  const float f = x - (j - 12582912.f);
-  const float q = fmaf(fmaf(fmaf(0.0550292665f, f, 0.242256982f), f, 0.693253055f), f, 0.999951339f);
-  return __int_as_float(__float_as_int(q) + (__float_as_int(j) << 23));
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return reinterpret_cast<uint32_t&>(v);
-}
-
-// UMMA shared-memory descriptors for a 128 x 128 bf16 tile stored as two 64-column halves
-// (16 KB apart), 128 B per row, 128-byte swizzle (the TMA SWIZZLE_128B box layout).
-//   K-major (rows = M/N, columns = K):  SBO = 1024 B between 8-row groups; the k-th
-//     16-element step starts 32 B further inside the swizzle atom (next half at k = 4).
-//   MN-major (rows = K, columns = M/N): LBO = 16 KB between the 64-wide M/N halves,
-//     SBO = 1024 B between 8-row K groups; the k-th 16-row step starts 2 KB further.
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
-         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
-}
-// instruction descriptor: bf16 x bf16 -> f32, M = 128
-__host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn, uint32_t n = 128) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
-}
-
-// One 128 x N x (16 kSteps) GEMM = kSteps UMMAs of K = 16, issued by one elected lane of the
-// converged UMMA warp.  a4 / b4: shared-memory tile start >> 4 (descriptor address field),
-// or for kATmem the TMEM address of A (K = 16 per 8 columns of bf16 pairs).  Descriptor low
-// words are a4/b4 + compile-time constants (no carry: addresses < 2^18); the high word is
-// SBO = 1024 B, version 1, SWIZZLE_128B for both majors.
-template <int kSteps, bool kAMn, bool kBMn, bool kATmem>
-__device__ __forceinline__ void gemm128(uint32_t d, uint32_t a4, uint32_t b4, uint32_t idesc, bool acc) {
-  asm volatile("" : "+r"(a4), "+r"(b4));  // keep the per-k descriptors out of the loop-invariant pool
-  constexpr uint64_t kHi = uint64_t(0x40004040u) << 32;
-  if (elect_one()) {
-#pragma unroll
-    for (int k = 0; k < kSteps; ++k) {
-      const uint32_t boff = kBMn ? (k * 2048) >> 4 : (((k >> 2) * kHalf + (k & 3) * 32) >> 4);
-      const uint64_t bd = kHi | (b4 + boff + (kBMn ? (uint32_t(kHalf) >> 4) << 16 : 1u << 16));
-      const uint32_t en = (acc || k > 0) ? 1u : 0u;
-      if constexpr (kATmem) {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
-            "r"(a4 + k * 8), "l"(bd), "r"(idesc), "r"(en)
-            : "memory");
-      } else {
-        const uint32_t aoff = kAMn ? (k * 2048) >> 4 : (((k >> 2) * kHalf + (k & 3) * 32) >> 4);
-        const uint64_t ad = kHi | (a4 + aoff + (kAMn ? (uint32_t(kHalf) >> 4) << 16 : 1u << 16));
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(en)
-            : "memory");
-      }
-    }
-  }
-  __syncwarp();
-}
 
 struct Params {
   __nv_bfloat16* dqkv;
@@ -679,38 +525,6 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const float* __restric
     float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale, b.x * scale, b.y * scale, b.z * scale, b.w * scale};
     *reinterpret_cast<uint4*>(dqkv + row * 3 * h + col) = pack8(f);
   }
-}
-
-// ------------------------------------------------------------------ host side
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiled encoder(int* rc) {
-  static std::once_flag once;
-  static EncodeTiled fn = nullptr;
-  std::call_once(once, [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiled>(f);
-  });
-  *rc = fn ? PPO_OK : set_error(PPO_ENOTSUP, "cuTensorMapEncodeTiled unavailable");
-  return fn;
-}
-
-// 3-D map over a row-major [rows][heads][D] view: dims (D, heads, rows), 128-byte swizzle.
-static int make_map(EncodeTiled enc, CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base, int D,
-                    uint64_t heads, uint64_t rows, uint64_t row_stride_bytes, uint32_t box_d, uint32_t box_rows) {
-  cuuint64_t dims[3] = {uint64_t(D), heads, rows};
-  cuuint64_t strides[2] = {uint64_t(D) * esize, row_stride_bytes};
-  cuuint32_t box[3] = {box_d, 1, box_rows};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_error(PPO_EINVAL, "ppo_attn_bwd: cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return PPO_OK;
 }
 
 static long long* g_trace = nullptr;

@@ -1,0 +1,310 @@
+// libppo_b200.so -- K7 causal attention forward, hand-written on tcgen05 (sm_100a).
+//
+// o[s, h] (bf16, written straight into the activation slab) and lse[heads, s] (fp32,
+// natural log -- the statistics K7b and cuDNN's backward consume) from the fused
+// qkv[s, 3h] of one microbatch.  The reference holds only the FLOP model of this op
+// (pkg/src/ppoff/costs.py:144-161: 12bs^2h of the 12bsh(6h+s) per layer) and keeps o and
+// the softmax statistics in the saved set it prices (costs.py:99-105).
+//
+// One CTA per (pair of adjacent 128-row q blocks i0 = 2t, i1 = 2t + 1, head): q block i0
+// walks kv blocks 0..i0, i1 walks 0..i1; every K/V tile is loaded once by TMA for both.
+// Per (q block, kv block): S = Q K^T (A = Q, B = K, both K-major shared memory) into
+// TMEM, the softmax warpgroup of that q block (one thread per q row, the row in
+// registers) turns S into P = exp2(S * scale * log2e - m) with a running row maximum m
+// that is only moved when it grows by more than 2^8 (O is rescaled in TMEM then, rarely
+// after the first kv blocks), writes P as bf16 over S's first 64 TMEM columns, and
+// O += P V runs with A = P from TMEM and B = V (MN-major shared memory).  The two q blocks
+// ping-pong: the tensor core runs S/PV of one while the other's warpgroup exponentiates.
+// TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+D), O1 [256+D, 256+2D).
+// Warps: 0-3 softmax of q block i0, 4-7 of i1, 8 UMMA issue (converged, one lane issues),
+// 9 TMA producer, 10-11 register donors (setmaxnreg).
+#include "ppo_common.cuh"
+#include "ppo_tcgen05.cuh"
+
+namespace ppo {
+namespace attnf {
+
+using namespace ppo::tc;
+
+constexpr int kTile = 128;
+constexpr int kThreads = 384;
+
+template <int D>
+struct Cfg {
+  static constexpr int kHalves = D / 64;
+  static constexpr int kTileBytes = kHalves * kHalf;
+  static constexpr int kOffQ = 0;                      // q0, q1
+  static constexpr int kOffKV = 2 * kTileBytes;        // 2 stages x (K, V)
+  static constexpr int kOffBar = kOffKV + 4 * kTileBytes;
+  static constexpr int kNumBars = 16;
+  static constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
+  static constexpr int kSmemBytes = kOffTmemPtr + 8;
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
+  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
+};
+
+enum : int {
+  B_Q = 0,
+  B_KVF0 = 1,  // kv full[2]
+  B_KVE0 = 3,  // kv empty[2]
+  B_SF0 = 5,   // S full[2] (q block 0 / 1)
+  B_PF0 = 7,   // P full[2]
+  B_OD0 = 9,   // O done[2]: the PV of the last issued step has completed
+};
+
+struct Params {
+  __nv_bfloat16* o;
+  float* lse;  // [H, s] natural log
+  int s, H;
+  float scale;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const Params p) {
+  using C = Cfg<D>;
+  constexpr int kTileBytes = C::kTileBytes;
+  constexpr int kDK = D / 16;  // UMMA K-steps over the head dimension (S)
+  constexpr int kPolyPer8 = 3;  // exponentials per 8 on the FMA pipe, the rest on the SFU
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hd = blockIdx.x;
+  const int n_pairs = p.s / (2 * kTile);
+  const int pair = n_pairs - 1 - int(blockIdx.y);  // heaviest pairs first (LPT through dispatch order)
+  const int i0 = 2 * pair;
+  const int n0 = i0 + 1, n1 = i0 + 2;  // kv blocks walked by q block i0 / i1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::kOffTmemPtr);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[B_Q], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars[B_KVF0 + i], 1);
+      mbar_init(&bars[B_KVE0 + i], 1);
+      mbar_init(&bars[B_SF0 + i], 1);
+      mbar_init(&bars[B_PF0 + i], 4);
+      mbar_init(&bars[B_OD0 + i], 1);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_ptr))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 9 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_qkv)) : "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    if (warp == 9) {
+      // ===================================================== TMA producer
+      if (lane == 0) {
+        const int H = p.H;
+        mbar_expect_tx(&bars[B_Q], 2 * kTileBytes);
+        for (int q = 0; q < 2; ++q)
+          for (int half = 0; half < C::kHalves; ++half)
+            tma_load_3d(smem + C::kOffQ + q * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd,
+                        (i0 + q) * kTile, &bars[B_Q]);
+        for (int j = 0; j < n1; ++j) {
+          const int st = j & 1;
+          mbar_wait(&bars[B_KVE0 + st], ((j >> 1) & 1) ^ 1);
+          mbar_expect_tx(&bars[B_KVF0 + st], 2 * kTileBytes);
+          uint8_t* kv = smem + C::kOffKV + st * 2 * kTileBytes;
+          for (int half = 0; half < C::kHalves; ++half) {
+            tma_load_3d(kv + half * kHalf, &tm_qkv, half * 64, H + hd, j * kTile, &bars[B_KVF0 + st]);
+            tma_load_3d(kv + kTileBytes + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, j * kTile,
+                        &bars[B_KVF0 + st]);
+          }
+        }
+      }
+    } else if (warp == 8) {
+      // ===================================================== UMMA issuer (converged warp)
+      const uint32_t sb4 = sbase >> 4;
+      const uint32_t aQ0 = sb4 + (C::kOffQ >> 4), aQ1 = sb4 + ((C::kOffQ + kTileBytes) >> 4);
+      const uint32_t tS0 = tmem + C::kColS0, tS1 = tmem + C::kColS1, tO0 = tmem + C::kColO0,
+                     tO1 = tmem + C::kColO1;
+      constexpr uint32_t I_S = idesc(0, 0, 128), I_PV = idesc(0, 1, D);
+      auto aK = [&](int j) { return sb4 + ((C::kOffKV + (j & 1) * 2 * kTileBytes) >> 4); };
+      auto aV = [&](int j) { return sb4 + ((C::kOffKV + (j & 1) * 2 * kTileBytes + kTileBytes) >> 4); };
+      auto kv_wait = [&](int j) { mbar_wait(&bars[B_KVF0 + (j & 1)], (j >> 1) & 1); };
+      mbar_wait(&bars[B_Q], 0);
+      kv_wait(0);
+      tc_fence_after();
+      gemm128<kDK, false, false, false>(tS0, aQ0, aK(0), I_S, false);  // S0(0)
+      tc_commit(&bars[B_SF0]);
+      gemm128<kDK, false, false, false>(tS1, aQ1, aK(0), I_S, false);  // S1(0)
+      tc_commit(&bars[B_SF0 + 1]);
+      for (int j = 0; j < n1; ++j) {
+        if (j < n0) {  // O0 += P0(j) V_j
+          mbar_wait(&bars[B_PF0], j & 1);
+          tc_fence_after();
+          gemm128<8, false, true, true>(tO0, tS0, aV(j), I_PV, j > 0);
+          tc_commit(&bars[B_OD0]);
+        }
+        if (j + 1 < n0) {  // S0(j+1): P0(j) in the same columns was read by the PV just issued
+          kv_wait(j + 1);
+          tc_fence_after();
+          gemm128<kDK, false, false, false>(tS0, aQ0, aK(j + 1), I_S, false);
+          tc_commit(&bars[B_SF0]);
+        }
+        mbar_wait(&bars[B_PF0 + 1], j & 1);  // O1 += P1(j) V_j
+        tc_fence_after();
+        gemm128<8, false, true, true>(tO1, tS1, aV(j), I_PV, j > 0);
+        tc_commit(&bars[B_OD0 + 1]);
+        tc_commit(&bars[B_KVE0 + (j & 1)]);  // K_j, V_j consumed
+        if (j + 1 < n1) {
+          kv_wait(j + 1);
+          tc_fence_after();
+          gemm128<kDK, false, false, false>(tS1, aQ1, aK(j + 1), I_S, false);
+          tc_commit(&bars[B_SF0 + 1]);
+        }
+      }
+    }
+    // warps 10, 11: idle register donors
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ===================================================== softmax warpgroups
+    const int wg = warp >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // q row within the block (TMEM lane)
+    const int qi = i0 + wg, nk = qi + 1;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_off + (wg ? C::kColS1 : C::kColS0);
+    const uint32_t tO = tmem + lane_off + (wg ? C::kColO1 : C::kColO0);
+    const float sl2 = p.scale * 1.4426950408889634f;
+    float m = -INFINITY, l = 0.f;  // running max (log2 domain, already scaled) and sum
+    for (int j = 0; j < nk; ++j) {
+      mbar_wait(&bars[B_SF0 + wg], j & 1);
+      tc_fence_after();
+      uint32_t r[4][32];
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) tmem_ld32(tS + ch * 32, r[ch]);
+      tmem_wait_ld();
+      if (j == qi) {  // the diagonal block: kv column c > q row is masked
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > row) r[c >> 5][c & 31] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(r[c >> 5][c & 31]));
+      const float m_new = fmaxf(m, mx * sl2);
+      // move the maximum only when it grows by more than 8 (P stays <= 2^8 otherwise)
+      const bool move = m_new > m + 8.f;
+      const float alpha = move ? ex2(m - m_new) : 1.f;
+      if (move) m = m_new;
+      float sum = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) {
+        const float x0 = fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -m);
+        const float x1 = fmaf(__uint_as_float(r[c >> 5][(c + 1) & 31]), sl2, -m);
+        const float e0 = (c & 7) < kPolyPer8 ? ex2_fma(x0) : ex2(x0);
+        const float e1 = ((c + 1) & 7) < kPolyPer8 ? ex2_fma(x1) : ex2(x1);
+        sum += e0 + e1;
+        pk[c >> 1] = pack_bf16(e0, e1);
+      }
+      l = l * alpha + sum;
+      // O rescale (rows whose maximum moved) once the previous PV of this block is done
+      if (j > 0 && __any_sync(0xffffffffu, move)) {
+        mbar_wait(&bars[B_OD0 + wg], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t o[32];
+          tmem_ld32(tO + ch * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          tmem_st32(tO + ch * 32, o);
+        }
+      }
+      {
+        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[0]);
+        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[32]);
+        tmem_st32(tS, p0);
+        tmem_st32(tS + 32, p1);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_PF0 + wg]);
+    }
+    // ---- epilogue: o = O / l (bf16) into the slab, lse = ln 2 * (m + log2 l)
+    mbar_wait(&bars[B_OD0 + wg], (nk - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const size_t h = size_t(p.H) * D;
+    const size_t q = size_t(qi) * kTile + row;
+    __nv_bfloat16* dst = p.o + q * h + size_t(hd) * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 32; ++ch) {
+      uint32_t o[32];
+      tmem_ld32(tO + ch * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+        w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+        w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+        w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+        *reinterpret_cast<uint4*>(dst + ch * 32 + v * 8) = w;
+      }
+    }
+    p.lse[size_t(hd) * p.s + q] = (m + __log2f(l)) * 0.69314718055994530942f;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int D>
+static int smem_optin() {
+  static std::mutex mu;
+  static unsigned done = 0;
+  int dev = 0;
+  PPO_TRY_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 32 && (done >> dev) & 1u) return PPO_OK;
+  PPO_TRY_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes));
+  if (dev < 32) done |= 1u << dev;
+  return PPO_OK;
+}
+
+}  // namespace attnf
+
+// Hand-written forward (used by ppo_attn_fwd, ppo_attention.cu).  seq % 256 == 0,
+// head_dim 64 / 128, arguments validated by the caller.
+int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, float scale, cudaStream_t st) {
+  using namespace attnf;
+  int rc = PPO_OK;
+  tc::EncodeTiled enc = tc::encoder(&rc);
+  if (rc) return rc;
+  const int64_t h = int64_t(H) * D;
+  CUtensorMap tm;
+  if ((rc = tc::make_map(enc, &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * H, s, 3 * h * 2, 64, kTile)))
+    return rc;
+  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale};
+  const dim3 grid(H, s / (2 * kTile));
+  if (D == 64) {
+    if ((rc = smem_optin<64>())) return rc;
+    attn_fwd_kernel<64><<<grid, kThreads, Cfg<64>::kSmemBytes, st>>>(tm, prm);
+  } else {
+    if ((rc = smem_optin<128>())) return rc;
+    attn_fwd_kernel<128><<<grid, kThreads, Cfg<128>::kSmemBytes, st>>>(tm, prm);
+  }
+  PPO_LAUNCHED("attn_fwd_kernel");
+  return PPO_OK;
+}
+
+}  // namespace ppo
