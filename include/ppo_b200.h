@@ -245,6 +245,9 @@ int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
  * causal tile scheduler; the first call per seq must not be inside a stream capture. */
 int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t heads, int64_t head_dim, float scale,
                  void* stream);
+/* Diagnostics: later ppo_attn_fwd launches record per-event SM clocks of the heaviest CTA of
+ * head 0 into trace (device, 32 x 256 int64; tools/attn_fwd_trace.py); NULL turns it off. */
+int ppo_attn_fwd_trace(void* trace);
 
 /* ----------------------------------------------- K7b: causal attention backward */
 /* The backward of the attention core priced by costs.py:144-161 (backward = 2x the

@@ -18,8 +18,14 @@
 // TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+D), O1 [256+D, 256+2D).
 // Warps: 0-3 softmax of q block i0, 4-7 of i1, 8 UMMA issue (converged, one lane issues),
 // 9 TMA producer, 10-11 register donors (setmaxnreg).
+#include <type_traits>
+
 #include "ppo_common.cuh"
 #include "ppo_tcgen05.cuh"
+
+#ifndef PPO_FWD_POLY
+#define PPO_FWD_POLY 1  // measured: 0 / 1 / 2 / 3 / 4 per 8 -> 68.8 / 65.7 / 66.9 / 67.0 / 70.4 us at C2
+#endif
 
 namespace ppo {
 namespace attnf {
@@ -57,7 +63,14 @@ struct Params {
   float* lse;  // [H, s] natural log
   int s, H;
   float scale;
+  long long* trace;  // diagnostics: per-event SM clocks of the heaviest CTA of head 0, or null
 };
+
+// diagnostics (ppo_attn_fwd_trace): event e of step j at trace[e * 256 + j]
+#define ATF_TRACE(e, j)                                                                          \
+  do {                                                                                           \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 256) p.trace[(e) * 256 + (j)] = clock64(); \
+  } while (0)
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -65,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<D>;
   constexpr int kTileBytes = C::kTileBytes;
   constexpr int kDK = D / 16;  // UMMA K-steps over the head dimension (S)
-  constexpr int kPolyPer8 = 3;  // exponentials per 8 on the FMA pipe, the rest on the SFU
+  constexpr int kPolyPer8 = PPO_FWD_POLY;  // exponentials per 8 on the FMA pipe, the rest on the SFU
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hd = blockIdx.x;
@@ -140,8 +153,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       gemm128<kDK, false, false, false>(tS1, aQ1, aK(0), I_S, false);  // S1(0)
       tc_commit(&bars[B_SF0 + 1]);
       for (int j = 0; j < n1; ++j) {
+        ATF_TRACE(0, j);
         if (j < n0) {  // O0 += P0(j) V_j
           mbar_wait(&bars[B_PF0], j & 1);
+          ATF_TRACE(1, j);
           tc_fence_after();
           gemm128<8, false, true, true>(tO0, tS0, aV(j), I_PV, j > 0);
           tc_commit(&bars[B_OD0]);
@@ -152,7 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           gemm128<kDK, false, false, false>(tS0, aQ0, aK(j + 1), I_S, false);
           tc_commit(&bars[B_SF0]);
         }
+        ATF_TRACE(2, j);
         mbar_wait(&bars[B_PF0 + 1], j & 1);  // O1 += P1(j) V_j
+        ATF_TRACE(3, j);
         tc_fence_after();
         gemm128<8, false, true, true>(tO1, tS1, aV(j), I_PV, j > 0);
         tc_commit(&bars[B_OD0 + 1]);
@@ -179,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m = -INFINITY, l = 0.f;  // running max (log2 domain, already scaled) and sum
     for (int j = 0; j < nk; ++j) {
       mbar_wait(&bars[B_SF0 + wg], j & 1);
+      if (quarter == 0 && lane == 0) ATF_TRACE(10 + 4 * wg, j);
       tc_fence_after();
       uint32_t r[4][32];
 #pragma unroll
@@ -189,26 +207,51 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 128; ++c)
           if (c > row) r[c >> 5][c & 31] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      float mx;
+      {
+        float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(r[c >> 5][c & 31]));
+        for (int c = 0; c < 128; c += 8) {
+          a0 = fmax3(a0, __uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31]));
+          a1 = fmax3(a1, __uint_as_float(r[c >> 5][(c + 2) & 31]), __uint_as_float(r[c >> 5][(c + 3) & 31]));
+          a2 = fmax3(a2, __uint_as_float(r[c >> 5][(c + 4) & 31]), __uint_as_float(r[c >> 5][(c + 5) & 31]));
+          a3 = fmax3(a3, __uint_as_float(r[c >> 5][(c + 6) & 31]), __uint_as_float(r[c >> 5][(c + 7) & 31]));
+        }
+        mx = fmax3(a0, a1, fmaxf(a2, a3));
+      }
       const float m_new = fmaxf(m, mx * sl2);
       // move the maximum only when it grows by more than 8 (P stays <= 2^8 otherwise)
       const bool move = m_new > m + 8.f;
       const float alpha = move ? ex2(m - m_new) : 1.f;
       if (move) m = m_new;
-      float sum = 0.f;
+      // x = s * scale * log2e - m on packed pairs; 3 of 8 exponentials on the FMA pipe
+      // (not in the diagonal step, whose masked -inf scores go through the SFU)
+      const uint64_t sl2x2 = f2(sl2, sl2), nm2 = f2(-m, -m);
+      uint64_t sum2 = f2(0.f, 0.f);
       uint32_t pk[64];
+      auto exps = [&](auto poly) {  // poly: std::true_type off the diagonal
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        const float x0 = fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -m);
-        const float x1 = fmaf(__uint_as_float(r[c >> 5][(c + 1) & 31]), sl2, -m);
-        const float e0 = (c & 7) < kPolyPer8 ? ex2_fma(x0) : ex2(x0);
-        const float e1 = ((c + 1) & 7) < kPolyPer8 ? ex2_fma(x1) : ex2(x1);
-        sum += e0 + e1;
-        pk[c >> 1] = pack_bf16(e0, e1);
-      }
+        for (int c = 0; c < 128; c += 2) {
+          const float2 x = f2u(ffma2(f2(__uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31])),
+                                     sl2x2, nm2));
+          float2 e;
+          if (decltype(poly)::value && (c & 7) < 2 * (kPolyPer8 / 2)) {
+            e = ex2_fma2(x.x, x.y);
+          } else if (decltype(poly)::value && (c & 7) == 2 * (kPolyPer8 / 2) && (kPolyPer8 & 1)) {
+            e = make_float2(ex2_fma(x.x), ex2(x.y));
+          } else {
+            e = make_float2(ex2(x.x), ex2(x.y));
+          }
+          sum2 = fadd2(sum2, f2(e.x, e.y));
+          pk[c >> 1] = pack_bf16(e.x, e.y);
+        }
+      };
+      if (j == qi) exps(std::false_type{});  // masked -inf scores go through the SFU
+      else exps(std::true_type{});
+      const float2 sp = f2u(sum2);
+      const float sum = sp.x + sp.y;
       l = l * alpha + sum;
+      if (quarter == 0 && lane == 0) ATF_TRACE(11 + 4 * wg, j);
       // O rescale (rows whose maximum moved) once the previous PV of this block is done
       if (j > 0 && __any_sync(0xffffffffu, move)) {
         mbar_wait(&bars[B_OD0 + wg], (j - 1) & 1);
@@ -233,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_PF0 + wg]);
+      if (quarter == 0 && lane == 0) ATF_TRACE(12 + 4 * wg, j);
     }
     // ---- epilogue: o = O / l (bf16) into the slab, lse = ln 2 * (m + log2 l)
     mbar_wait(&bars[B_OD0 + wg], (nk - 1) & 1);
@@ -268,6 +312,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+long long* g_trace = nullptr;
+
 template <int D>
 static int smem_optin() {
   static std::mutex mu;
@@ -294,7 +340,7 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, 
   CUtensorMap tm;
   if ((rc = tc::make_map(enc, &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * H, s, 3 * h * 2, 64, kTile)))
     return rc;
-  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale};
+  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale, attnf::g_trace};
   const dim3 grid(H, s / (2 * kTile));
   if (D == 64) {
     if ((rc = smem_optin<64>())) return rc;
@@ -308,3 +354,8 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, 
 }
 
 }  // namespace ppo
+
+extern "C" int ppo_attn_fwd_trace(void* trace) {
+  ppo::attnf::g_trace = static_cast<long long*>(trace);
+  return PPO_OK;
+}

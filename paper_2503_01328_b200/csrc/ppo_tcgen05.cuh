@@ -96,6 +96,47 @@ __device__ __forceinline__ float ex2_fma(float x) {
   return __int_as_float(__float_as_int(q) + (__float_as_int(j) << 23));
 }
 
+// ---- packed fp32 pairs (Blackwell FFMA2 / FADD2) and 3-input max
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2u(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// ex2_fma on a pair with the arithmetic in packed FFMA2 / FADD2 (x <= 0).
+__device__ __forceinline__ float2 ex2_fma2(float x0, float x1) {
+  const uint64_t x = f2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t j = fadd2(x, f2(12582912.f, 12582912.f));
+  const uint64_t t = fadd2(j, f2(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(t, f2(-1.f, -1.f), x);
+  uint64_t q = ffma2(f2(0.0550292665f, 0.0550292665f), f, f2(0.242256982f, 0.242256982f));
+  q = ffma2(q, f, f2(0.693253055f, 0.693253055f));
+  q = ffma2(q, f, f2(0.999951339f, 0.999951339f));
+  const float2 qq = f2u(q), jj = f2u(j);
+  return make_float2(__int_as_float(__float_as_int(qq.x) + (__float_as_int(jj.x) << 23)),
+                     __int_as_float(__float_as_int(qq.y) + (__float_as_int(jj.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return reinterpret_cast<uint32_t&>(v);

@@ -16,7 +16,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB_PATH = os.path.join(PKG, "libppo_b200.so")
+LIB_PATH = os.environ.get("PPO_LIB_PATH") or os.path.join(PKG, "libppo_b200.so")  # override: A/B builds only
 
 PPO_D2H, PPO_H2D = 0, 1
 PPO_NCCL_BASE = 10000
@@ -92,6 +92,7 @@ SIGNATURES = {
     "ppo_gemm_nn_dgelu": [_VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP],
     "ppo_gemm_wgrad": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
     "ppo_attn_fwd": [_VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
+    "ppo_attn_fwd_trace": [_VP],
     "ppo_attn_bwd_workspace_bytes": [_I64, _I64, _I64],
     "ppo_attn_bwd_trace": [_VP],
     "ppo_attn_bwd": [_VP, _VP, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _F32, _VP],
