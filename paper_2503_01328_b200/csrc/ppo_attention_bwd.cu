@@ -100,8 +100,8 @@ constexpr int kThreads = 512;  // warps 14, 15 idle: setmaxnreg works per warpgr
 
 struct Params {
   __nv_bfloat16* dqkv;
-  const float* lse2;   // [H, s] log2(e) * logsumexp
-  const float* delta;  // [H, s]
+  const float* lse2;   // [H, s] -log2(e) * logsumexp
+  const float* delta;  // [H, s] -rowsum(dO * O)
   float* dq_acc;       // [s, h] fp32
   int s, H;
   float scale;
@@ -125,7 +125,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 kOffBar = C::kOffBar, kOffTmemPtr = C::kOffTmemPtr;
   constexpr uint32_t kColDK = C::kColDK, kColDV = C::kColDV, kColDP = C::kColDP, kColS = C::kColS;
   constexpr int kDK = D / 16;  // UMMA K-steps over the head dimension
-  constexpr int kPolyPer8 = 3;  // exponentials per 8 on the FMA pipe (ex2_fma), the rest on the SFU
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hd = blockIdx.x, jb = blockIdx.y;
@@ -329,15 +328,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tmem + lane_off + kColS + c0 + 32, r[1]);
         tmem_wait_ld();
         if (warp == 4 && lane == 0) ATB_TRACE(40, it);
-        float4 l4[16];
+        // x = s * scale * log2e - log2e * lse on packed pairs (s_lse holds -log2e * lse);
+        // 1 of 8 exponentials on the FMA pipe (the forward's sweep, ppo_attention_fwd.cu)
+        const uint64_t sl2x2 = f2(sl2, sl2);
+        const uint64_t* nl = reinterpret_cast<const uint64_t*>(lse);
 #pragma unroll
-        for (int v = 0; v < 16; ++v) l4[v] = reinterpret_cast<const float4*>(lse)[v];
-        // (ex2.approx.f16x2 was measured: sm_100 issues it as two MUFU ops, no gain)
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float l = reinterpret_cast<const float*>(l4)[c];
-          const float x = fmaf(__uint_as_float(r[c >> 5][c & 31]), sl2, -l);  // s_lse holds log2(e) * lse
-          pr[c] = (c & 7) < kPolyPer8 ? ex2_fma(x) : ex2(x);
+        for (int c = 0; c < 64; c += 2) {
+          const float2 x = f2u(ffma2(f2(__uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31])),
+                                     sl2x2, nl[c >> 1]));
+          pr[c] = (c & 7) == 0 ? ex2_fma(x.x) : ex2(x.x);
+          pr[c + 1] = ex2(x.y);
         }
       }
       if (it == 0) {  // the diagonal tile: q < kv is masked
@@ -374,18 +374,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tmem + lane_off + kColDP + c0 + 32, r[1]);
         tmem_wait_ld();
         if (warp == 4 && lane == 0) ATB_TRACE(44, it);
+        const uint64_t* nd = reinterpret_cast<const uint64_t*>(dlt);  // -delta
 #pragma unroll
         for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk (8 q columns) of the 128-byte row
-          const float4 d0 = reinterpret_cast<const float4*>(dlt)[2 * chunk];
-          const float4 d1 = reinterpret_cast<const float4*>(dlt)[2 * chunk + 1];
-          const float dl[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int c = chunk * 8 + 2 * e;
-            const float a0 = pr[c] * (__uint_as_float(r[c >> 5][c & 31]) - dl[2 * e]);
-            const float a1 = pr[c + 1] * (__uint_as_float(r[(c + 1) >> 5][(c + 1) & 31]) - dl[2 * e + 1]);
-            w[e] = pack_bf16(a0, a1);
+            const int c = chunk * 8 + 2 * e;  // dS = P (dP - delta), packed pairs
+            const float2 a = f2u(fmul2(f2(pr[c], pr[c + 1]),
+                                       fadd2(f2(__uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31])),
+                                             nd[c >> 1])));
+            w[e] = pack_bf16(a.x, a.y);
           }
           *reinterpret_cast<uint4*>(ds_row + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
@@ -480,8 +479,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// delta[hd, i] = sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), lse2 = log2(e) * lse,
-// and the fp32 dQ accumulator row i zeroed.  One block per row; D/8 lanes per head.
+// delta[hd, i] = -sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), lse2 = -log2(e) * lse
+// (negated: the main kernel adds them in packed FFMA2 / FADD2), and the fp32 dQ
+// accumulator row i zeroed.  One block per row; D/8 lanes per head.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                             const __nv_bfloat16* __restrict__ dout,
                                                             const float* __restrict__ lse, float* __restrict__ lse2,
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16*
   pdl_wait();
   const int i = blockIdx.x;
   const int h = H * D;
-  for (int t = threadIdx.x; t < H; t += blockDim.x) lse2[size_t(t) * s + i] = lse[size_t(t) * s + i] * 1.4426950408889634f;
+  for (int t = threadIdx.x; t < H; t += blockDim.x) lse2[size_t(t) * s + i] = -lse[size_t(t) * s + i] * 1.4426950408889634f;
   for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
     const int e = e0 + threadIdx.x * 8;
     const bool ok = e < h;
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16*
     }
     for (int off = D / 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (ok) {
-      if ((threadIdx.x & (D / 8 - 1)) == 0) delta[size_t(e / D) * s + i] = acc;
+      if ((threadIdx.x & (D / 8 - 1)) == 0) delta[size_t(e / D) * s + i] = -acc;
       float4* z = reinterpret_cast<float4*>(dq_acc + size_t(i) * h + e);
       z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
       z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
