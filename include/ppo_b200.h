@@ -264,7 +264,8 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
                  int64_t seq, int64_t heads, int64_t head_dim, float scale, void* stream);
 /* Diagnostics: later ppo_attn_bwd launches record the SM clock of each pipeline event of
  * CTA (head 0, kv block 0) into trace (device, 64 x 256 int64: event e of step i at
- * e*256 + i; tools/attn_bwd_trace.py); NULL turns it off. */
+ * e*256 + i), followed by 4 int64 per CTA (globaltimer start, end, SM id;
+ * tools/attn_bwd_trace.py); NULL turns it off. */
 int ppo_attn_bwd_trace(void* trace);
 
 /* ----------------------------------------------- K8: stage-boundary send/recv */

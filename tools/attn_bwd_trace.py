@@ -39,13 +39,15 @@ def main():
     native.attn_fwd(qkv, o, lse, H)
     dqkv = torch.empty_like(qkv)
     ws = torch.empty(native.attn_bwd_workspace_bytes(s, H, D), device=dev, dtype=torch.uint8)
-    tr = torch.zeros(64 * 256, device=dev, dtype=torch.int64)
+    n_cta = H * (s // 128)
+    tr = torch.zeros(64 * 256 + 4 * n_cta, device=dev, dtype=torch.int64)
     native.attn_bwd(qkv, o, do, lse, dqkv, H, ws)  # warm
     native.load().ppo_attn_bwd_trace(tr.data_ptr())
     native.attn_bwd(qkv, o, do, lse, dqkv, H, ws)
     torch.cuda.synchronize()
     native.load().ppo_attn_bwd_trace(None)
-    t = tr.view(64, 256).cpu()
+    cta = tr[64 * 256:].view(n_cta, 4).cpu().tolist()
+    t = tr[:64 * 256].view(64, 256).cpu()
     n = s // 128
     t0 = int(t[0, 0])
     ev = {name: [int(t[e, i]) - t0 for i in range(n)] for e, name in EVENTS.items()}
@@ -79,6 +81,25 @@ def main():
                                          [int(t[30, i]) for i in range(6)]))
     summ["ideal_period_clk"] = 5 * 512
     summ["total_clk"] = ev["m_dk"][n - 1]
+    # CTA residency: busy time per SM vs the kernel's span, gaps between CTAs on an SM
+    t_lo = min(c[0] for c in cta)
+    t_hi = max(c[1] for c in cta)
+    per_sm = {}
+    for c in cta:
+        per_sm.setdefault(c[2], []).append((c[0] - t_lo, c[1] - t_lo))
+    busy = [sum(b - a for a, b in v) for v in per_sm.values()]
+    gaps = [b2[0] - a1[1] for v in per_sm.values() for a1, b2 in zip(sorted(v), sorted(v)[1:])]
+    ends = [max(b for _, b in v) for v in per_sm.values()]
+    import numpy as np
+    A = np.array([[1.0, c[3]] for c in cta])
+    y = np.array([(c[1] - c[0]) / 1e3 for c in cta])
+    fit = np.linalg.lstsq(A, y, rcond=None)[0]
+    summ["cta_fit_us"] = {"fixed": round(float(fit[0]), 2), "per_step": round(float(fit[1]), 3)}
+    summ["cta"] = {"span_us": round((t_hi - t_lo) / 1e3, 1), "sms": len(per_sm),
+                   "mean_busy_frac": round(sum(busy) / len(busy) / (t_hi - t_lo), 3),
+                   "mean_gap_us": round(sum(gaps) / max(1, len(gaps)) / 1e3, 2),
+                   "first_sm_done_us": round(min(ends) / 1e3, 1), "mean_cta_us": round(
+                       sum(b - a for v in per_sm.values() for a, b in v) / len(cta) / 1e3, 2)}
     print(json.dumps(summ))
 
 
