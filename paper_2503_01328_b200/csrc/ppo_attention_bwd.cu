@@ -118,7 +118,8 @@ struct Params {
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                    const __grid_constant__ CUtensorMap tm_dq, const Params p) {
+                    const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dqkv,
+                    const Params p) {
   using C = Cfg<D>;
   constexpr int kTileBytes = C::kTileBytes, kOffK = C::kOffK, kOffV = C::kOffV, kOffQ = C::kOffQ, kOffDO = C::kOffDO,
                 kOffDS = C::kOffDS, kOffStg = C::kOffStg, kOffLse = C::kOffLse, kOffDelta = C::kOffDelta,
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hd = blockIdx.x, jb = blockIdx.y;
   long long* cta_log = p.trace ? p.trace + 64 * 256 + 4 * (size_t(blockIdx.y) * gridDim.x + blockIdx.x) : nullptr;
+  if (threadIdx.x == 0) ATB_TRACE(48, 0);  // CTA start (SM clock)
   if (cta_log && threadIdx.x == 0) {  // diagnostics: CTA residency (globaltimer ns, SM id)
     long long t;
     unsigned sm;
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_qkv)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_do)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dq)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dqkv)) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tDV = tmem + kColDV, tDK = tmem + kColDK;
       constexpr uint32_t I_KK = idesc(0, 0), I_KMd = idesc(0, 1, D), I_MMd = idesc(1, 1, D);
       mbar_wait(&bars[B_KV], 0);
+      ATB_TRACE(48, 1);  // K, V landed
       tc_fence_after();
       uint32_t dbg_ph = 0;
       // diagnostics: serialise one GEMM and time it (events 16.. start, 17.. done)
@@ -409,15 +413,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // ---- epilogue: dV and scale * dK rows of this kv block into dqkv
     mbar_wait(&bars[B_DKV], 0);
+    if (warp == 4 && lane == 0) ATB_TRACE(48, 2);  // dK, dV complete
     tc_fence_after();
-    const size_t h = size_t(p.H) * D;
+    // staged in the (now idle) Q stages in the TMA box layout, then stored by TMA
     constexpr int kHalfD = D / 2;  // columns of dK / dV per warpgroup
-    __nv_bfloat16* out = p.dqkv + (size_t(jb) * kTile + row) * 3 * h + size_t(hd) * D + wg * kHalfD;
 #pragma unroll
     for (int m = 0; m < 2; ++m) {  // 0: dK (scaled), 1: dV
       const uint32_t col = m == 0 ? kColDK : kColDV;
       const float f = m == 0 ? p.scale : 1.f;
-      __nv_bfloat16* dst = out + (m == 0 ? h : 2 * h);
+      uint8_t* base = smem + kOffQ + m * kTileBytes;
 #pragma unroll
       for (int ch = 0; ch < kHalfD / 32; ++ch) {
         uint32_t r[32];
@@ -430,9 +434,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           w.y = pack_bf16(__uint_as_float(r[v8 * 8 + 2]) * f, __uint_as_float(r[v8 * 8 + 3]) * f);
           w.z = pack_bf16(__uint_as_float(r[v8 * 8 + 4]) * f, __uint_as_float(r[v8 * 8 + 5]) * f);
           w.w = pack_bf16(__uint_as_float(r[v8 * 8 + 6]) * f, __uint_as_float(r[v8 * 8 + 7]) * f);
-          *reinterpret_cast<uint4*>(dst + ch * 32 + v8 * 8) = w;
+          const int c = wg * kHalfD + ch * 32 + v8 * 8;  // first column of this 16-byte chunk
+          const int chunk = (c & 63) >> 3;
+          *reinterpret_cast<uint4*>(base + (c >> 6) * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4)) = w;
         }
       }
+    }
+    fence_proxy_async_smem();
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (warp == 4 && lane == 0) {
+      for (int m = 0; m < 2; ++m)
+        for (int half = 0; half < C::kHalves; ++half)
+          tma_store_3d(&tm_dqkv, smem + kOffQ + m * kTileBytes + half * kHalf, half * 64, (m + 1) * p.H + hd,
+                       jb * kTile);
+      tma_store_commit();
+      tma_store_wait_read<0>();  // the staging must outlive the reads, not the global writes
     }
   } else {
     // ===================================================== dQ drain: TMEM -> smem -> TMA reduce-add
@@ -482,8 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   }
 
+  if (warp == 4 && lane == 0) ATB_TRACE(48, 3);  // epilogue stores issued
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ATB_TRACE(48, 4);  // every role done
   if (warp == 12) {
     __syncwarp();
     tc_fence_after();
@@ -561,10 +579,10 @@ static int smem_optin() {
 }
 
 template <int D>
-static int launch_main(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const Params& prm,
-                       cudaStream_t st) {
+static int launch_main(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
+                       const Params& prm, cudaStream_t st) {
   if (int rc = smem_optin<D>()) return rc;
-  attn_bwd_kernel<D><<<dim3(prm.H, prm.s / kTile), kThreads, Cfg<D>::kSmemBytes, st>>>(a, b, c, prm);
+  attn_bwd_kernel<D><<<dim3(prm.H, prm.s / kTile), kThreads, Cfg<D>::kSmemBytes, st>>>(a, b, c, d, prm);
   PPO_LAUNCHED("attn_bwd_kernel");
   return PPO_OK;
 }
@@ -608,10 +626,12 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   float* lse2 = delta + size_t(H) * s;
 
   const int D = int(head_dim);
-  CUtensorMap tm_qkv, tm_do, tm_dq;
+  CUtensorMap tm_qkv, tm_do, tm_dq, tm_dqkv;
   if ((rc = make_map(enc, &tm_qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * heads, seq, 3 * h * 2, 64, kTile)))
     return rc;
   if ((rc = make_map(enc, &tm_do, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dout, D, heads, seq, h * 2, 64, kTile)))
+    return rc;
+  if ((rc = make_map(enc, &tm_dqkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dqkv, D, 3 * heads, seq, 3 * h * 2, 64, kTile)))
     return rc;
   if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, D, heads, seq, h * 4, 32, 32))) return rc;
 
@@ -623,7 +643,8 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
     return e ? std::atoi(e) : 0;
   }();
   Params prm{static_cast<__nv_bfloat16*>(dqkv), lse2, delta, dq_acc, s, H, scale, g_trace, exp_mode};
-  rc = D == 64 ? launch_main<64>(tm_qkv, tm_do, tm_dq, prm, st) : launch_main<128>(tm_qkv, tm_do, tm_dq, prm, st);
+  rc = D == 64 ? launch_main<64>(tm_qkv, tm_do, tm_dq, tm_dqkv, prm, st)
+               : launch_main<128>(tm_qkv, tm_do, tm_dq, tm_dqkv, prm, st);
   if (rc) return rc;
   const int sms = sm_count_current();
   launch_pdl(attn_bwd_dq_kernel, dim3(sms * 4), dim3(256), 0, st, static_cast<const float*>(dq_acc),

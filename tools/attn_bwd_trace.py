@@ -79,6 +79,10 @@ def main():
     if int(t[30, 0]) > 0:  # PPO_ATB_EXP bit 3: clocks per 128^3 GEMM, 16 back to back
         summ["gemm_form_clk"] = dict(zip(["S_KK", "dQ_MNMN", "dK_KMN", "dV_TMN", "T_K", "KK_acc"],
                                          [int(t[30, i]) for i in range(6)]))
+    life = [int(t[48, i]) - t0 for i in range(5)]  # start, K/V landed, dK/dV done, stores issued, all done
+    summ["cta00_clk"] = {"start_to_kv": life[1] - life[0], "kv_to_first_q": -life[1],
+                         "last_step_to_dkdv": life[2] - ev["m_dk"][n - 1], "epilogue": life[3] - life[2],
+                         "to_exit": life[4] - life[3]}
     summ["ideal_period_clk"] = 5 * 512
     summ["total_clk"] = ev["m_dk"][n - 1]
     # CTA residency: busy time per SM vs the kernel's span, gaps between CTAs on an SM
