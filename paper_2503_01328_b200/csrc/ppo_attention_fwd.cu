@@ -18,6 +18,7 @@
 // TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+D), O1 [256+D, 256+2D).
 // Warps: 0-3 softmax of q block i0, 4-7 of i1, 8 UMMA issue (converged, one lane issues),
 // 9 TMA producer, 10-11 register donors (setmaxnreg).
+#include <cstdlib>
 #include <type_traits>
 
 #include "ppo_common.cuh"
@@ -64,6 +65,7 @@ struct Params {
   int s, H;
   float scale;
   long long* trace;  // diagnostics: per-event SM clocks of the heaviest CTA of head 0, or null
+  int head_group;    // heads walked together (dispatch order), divides H
 };
 
 // diagnostics (ppo_attn_fwd_trace): event e of step j at trace[e * 256 + j]
@@ -81,9 +83,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kPolyPer8 = PPO_FWD_POLY;  // exponentials per 8 on the FMA pipe, the rest on the SFU
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hd = blockIdx.x;
+  // dispatch order: groups of head_group heads; inside a group the heaviest q-block pairs
+  // first (the in-order dispatch is then an LPT schedule), heads innermost, so concurrent
+  // CTAs share the K / V tiles of a few heads in L2 (C4: 40 heads x 16 MB of K, V)
   const int n_pairs = p.s / (2 * kTile);
-  const int pair = n_pairs - 1 - int(blockIdx.y);  // heaviest pairs first (LPT through dispatch order)
+  const int lin = int(blockIdx.y) * int(gridDim.x) + int(blockIdx.x);
+  const int per_group = p.head_group * n_pairs, grp = lin / per_group, rem = lin % per_group;
+  const int hd = grp * p.head_group + rem % p.head_group;
+  const int pair = n_pairs - 1 - rem / p.head_group;
   const int i0 = 2 * pair;
   const int n0 = i0 + 1, n1 = i0 + 2;  // kv blocks walked by q block i0 / i1
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -340,7 +347,13 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, 
   CUtensorMap tm;
   if ((rc = tc::make_map(enc, &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * H, s, 3 * h * 2, 64, kTile)))
     return rc;
-  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale, attnf::g_trace};
+  static const int group_env = [] {
+    const char* e = std::getenv("PPO_ATTN_HEAD_GROUP");  // A/B experiments
+    return e ? std::atoi(e) : 0;
+  }();
+  int group = group_env > 0 ? group_env : 8;
+  while (H % group) --group;
+  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale, attnf::g_trace, group};
   const dim3 grid(H, s / (2 * kTile));
   if (D == 64) {
     if ((rc = smem_optin<64>())) return rc;
