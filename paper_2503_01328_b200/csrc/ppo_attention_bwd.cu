@@ -71,18 +71,19 @@ struct Cfg {
   static constexpr int kOffLse = kOffStg + 4 * 2 * kStgBytes;  // 2 stages x 128 fp32
   static constexpr int kOffDelta = kOffLse + 2 * 512;
   static constexpr int kOffBar = kOffDelta + 2 * 512;
-  static constexpr int kNumBars = 16;
+  static constexpr int kNumBars = 24;
   static constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
-  static constexpr int kSmemBytes = kOffTmemPtr + 16;
+  static constexpr int kOffItems = kOffTmemPtr + 16;  // 4 work-item slots
+  static constexpr int kSmemBytes = kOffItems + 16;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
   static constexpr uint32_t kColDK = 0, kColDV = D, kColDP = 2 * D, kColS = 2 * D + 128;
 };
 
 // barrier indices
 enum : int {
-  B_KV = 0,
-  B_QF0 = 1,  // q_full[2]
-  B_QE0 = 3,  // q_empty[2]
+  B_KV = 0,    // K, V of the current item landed
+  B_QF0 = 1,   // q_full[2]
+  B_QE0 = 3,   // q_empty[2]
   B_DOF = 5,
   B_DOE = 6,
   B_SF = 7,
@@ -92,8 +93,10 @@ enum : int {
   B_DSE = 11,
   B_DQF = 12,
   B_DQE = 13,
-  B_DKV = 14,
-  B_DBG = 15,  // diagnostics: per-GEMM completion (PPO_ATB_EXP bit 2)
+  B_DKV = 14,  // dK, dV of the item complete (and every UMMA of the item)
+  B_KVE = 15,  // K, V of the item no longer read: the next item's may land
+  B_ACC = 16,  // the epilogue holds dK, dV in registers: the next item may accumulate
+  B_ITEM0 = 17,  // item slot full[4] (the producer fetched the next work item)
 };
 
 constexpr int kThreads = 512;  // warps 14, 15 idle: setmaxnreg works per warpgroup
@@ -103,6 +106,7 @@ struct Params {
   const float* lse2;   // [H, s] -log2(e) * logsumexp
   const float* delta;  // [H, s] -rowsum(dO * O)
   float* dq_acc;       // [s, h] fp32
+  int* work;           // dynamic work counter (zeroed by the prep kernel)
   int s, H;
   float scale;
   long long* trace;  // diagnostics: per-event SM clocks of CTA (0, 0), or null
@@ -111,9 +115,9 @@ struct Params {
 };
 
 // diagnostics (ppo_attn_bwd_trace): event e of step `it` at trace[e * 256 + it]
-#define ATB_TRACE(e, it)                                                                      \
-  do {                                                                                        \
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (it) < 256) p.trace[(e) * 256 + (it)] = clock64(); \
+#define ATB_TRACE(e, it)                                                                     \
+  do {                                                                                       \
+    if (p.trace && trace_item && (it) < 256) p.trace[(e) * 256 + (it)] = clock64();          \
   } while (0)
 
 template <int D>
@@ -129,27 +133,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kDK = D / 16;  // UMMA K-steps over the head dimension
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Dispatch order (block index -> work): groups of head_group heads, inside a group kv
-  // block j ascending (longest walk first, so the hardware's in-order dispatch is an LPT
-  // schedule), heads of the group innermost.  Concurrent CTAs then share the Q / dO tiles of
-  // a few heads in L2 instead of streaming every head's (C4: 40 heads x 8 MB > 126 MB L2).
-  const int lin = int(blockIdx.y) * int(gridDim.x) + int(blockIdx.x);
-  const int n_qb = p.s / kTile, per_group = p.head_group * n_qb;
-  const int grp = lin / per_group, rem = lin % per_group;
-  const int jb = rem / p.head_group, hd = grp * p.head_group + rem % p.head_group;
-  long long* cta_log = p.trace ? p.trace + 64 * 256 + 4 * (size_t(blockIdx.y) * gridDim.x + blockIdx.x) : nullptr;
-  if (threadIdx.x == 0) ATB_TRACE(48, 0);  // CTA start (SM clock)
-  if (cta_log && threadIdx.x == 0) {  // diagnostics: CTA residency (globaltimer ns, SM id)
+  const int n_q = p.s / kTile;
+  // Persistent: work item w = (kv block jb, head hd) in dispatch order -- groups of
+  // head_group heads, kv block ascending (longest walk first) inside a group, heads
+  // innermost, so concurrent CTAs share the Q / dO tiles of a few heads in L2 -- taken from a
+  // global counter as a CTA's producer gets to it (a greedy longest-first schedule, like the
+  // hardware's in-order dispatch), handed to the other roles through a 4-slot ring in shared
+  // memory.  An item's K/V land while the previous item's dK/dV leave.
+  const int n_items = p.H * n_q, b = int(blockIdx.x);
+  volatile int* item_slot = reinterpret_cast<volatile int*>(smem + C::kOffItems);
+  auto next_item = [&](int r) {  // consumers: item of round r, -1 when the CTA is done
+    mbar_wait(reinterpret_cast<uint64_t*>(smem + C::kOffBar) + B_ITEM0 + (r & 3), (r >> 2) & 1);
+    return item_slot[r & 3];
+  };
+  auto decode = [&](int w, int& jb, int& hd) {
+    const int per_group = p.head_group * n_q, grp = w / per_group, rem = w % per_group;
+    jb = rem / p.head_group;
+    hd = grp * p.head_group + rem % p.head_group;
+  };
+  bool trace_item = false;  // diagnostics: events of CTA 0's first item only
+  long long* cta_log = p.trace ? p.trace + 64 * 256 + 4 * size_t(b) : nullptr;
+  if (cta_log && threadIdx.x == 0) {  // diagnostics: CTA residency (globaltimer ns, SM id, q steps)
     long long t;
     unsigned sm;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     cta_log[0] = t;
     cta_log[2] = sm;
-    cta_log[3] = p.s / kTile - jb;  // q steps of this CTA
   }
-  const int n_q = p.s / kTile;
-  const int n_it = n_q - jb;  // q blocks jb .. n_q-1
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmemPtr);
   float* s_lse = reinterpret_cast<float*>(smem + kOffLse);
@@ -171,7 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars[B_DQF], 1);
     mbar_init(&bars[B_DQE], 4);
     mbar_init(&bars[B_DKV], 1);
-    mbar_init(&bars[B_DBG], 1);
+    mbar_init(&bars[B_KVE], 1);
+    mbar_init(&bars[B_ACC], 8);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[B_ITEM0 + i], 1);
     mbar_fence_init();
   }
   if (warp == 12) {
@@ -201,128 +214,110 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================================================== TMA producer
     if (lane == 0) {
       const int H = p.H;
-      mbar_expect_tx(&bars[B_KV], 2 * kTileBytes);
-      for (int half = 0; half < C::kHalves; ++half) {
-        tma_load_3d(smem + kOffK + half * kHalf, &tm_qkv, half * 64, H + hd, jb * kTile, &bars[B_KV]);
-        tma_load_3d(smem + kOffV + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, jb * kTile, &bars[B_KV]);
+      int g = 0;  // q steps of earlier items (global step index base)
+      for (int r = 0;; ++r) {
+        int w = atomicAdd(p.work, 1);
+        w = w < n_items ? w : -1;
+        item_slot[r & 3] = w;
+        mbar_arrive(&bars[B_ITEM0 + (r & 3)]);  // release: the slot write is visible to waiters
+        if (w < 0) break;
+        int jb, hd;
+        decode(w, jb, hd);
+        trace_item = b == 0 && r == 0;
+        const int n_it = n_q - jb;
+        auto load_step = [&](int it) {
+          const int gi = g + it, qb = jb + it, st = gi & 1;
+          mbar_wait(&bars[B_QE0 + st], ((gi >> 1) & 1) ^ 1);
+          ATB_TRACE(28, it);
+          mbar_expect_tx(&bars[B_QF0 + st], kTileBytes + 1024);
+          for (int half = 0; half < C::kHalves; ++half)
+            tma_load_3d(smem + kOffQ + st * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd, qb * kTile,
+                        &bars[B_QF0 + st]);
+          tma_load_1d(s_lse + st * 128, p.lse2 + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
+          tma_load_1d(s_delta + st * 128, p.delta + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
+          mbar_wait(&bars[B_DOE], (gi & 1) ^ 1);
+          ATB_TRACE(29, it);
+          mbar_expect_tx(&bars[B_DOF], kTileBytes);
+          for (int half = 0; half < C::kHalves; ++half)
+            tma_load_3d(smem + kOffDO + half * kHalf, &tm_do, half * 64, hd, qb * kTile, &bars[B_DOF]);
+        };
+        load_step(0);  // the first Q / dO of this item may land before its K / V
+        mbar_wait(&bars[B_KVE], (r & 1) ^ 1);
+        mbar_expect_tx(&bars[B_KV], 2 * kTileBytes);
+        for (int half = 0; half < C::kHalves; ++half) {
+          tma_load_3d(smem + kOffK + half * kHalf, &tm_qkv, half * 64, H + hd, jb * kTile, &bars[B_KV]);
+          tma_load_3d(smem + kOffV + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, jb * kTile, &bars[B_KV]);
+        }
+        for (int it = 1; it < n_it; ++it) load_step(it);
+        g += n_it;
       }
-      for (int it = 0; it < n_it; ++it) {
-        const int qb = jb + it, st = it & 1;
-        mbar_wait(&bars[B_QE0 + st], ((it >> 1) & 1) ^ 1);
-        ATB_TRACE(28, it);
-        mbar_expect_tx(&bars[B_QF0 + st], kTileBytes + 1024);
-        for (int half = 0; half < C::kHalves; ++half)
-          tma_load_3d(smem + kOffQ + st * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd, qb * kTile,
-                      &bars[B_QF0 + st]);
-        tma_load_1d(s_lse + st * 128, p.lse2 + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
-        tma_load_1d(s_delta + st * 128, p.delta + size_t(hd) * p.s + qb * kTile, 512, &bars[B_QF0 + st]);
-        mbar_wait(&bars[B_DOE], (it & 1) ^ 1);
-        ATB_TRACE(29, it);
-        mbar_expect_tx(&bars[B_DOF], kTileBytes);
-        for (int half = 0; half < C::kHalves; ++half)
-          tma_load_3d(smem + kOffDO + half * kHalf, &tm_do, half * 64, hd, qb * kTile, &bars[B_DOF]);
-      }
+      if (cta_log) cta_log[3] = g;  // q steps this CTA walked
     }
   } else if (warp == 12) {
     // ===================================================== UMMA issuer (converged warp, one lane issues)
-    {
-      const uint32_t sb4 = sbase >> 4;
-      const uint32_t aK = sb4 + (kOffK >> 4), aV = sb4 + (kOffV >> 4), aDO = sb4 + (kOffDO >> 4),
-                     aDS = sb4 + (kOffDS >> 4);
-      const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tDV = tmem + kColDV, tDK = tmem + kColDK;
-      constexpr uint32_t I_KK = idesc(0, 0), I_KMd = idesc(0, 1, D), I_MMd = idesc(1, 1, D);
-      mbar_wait(&bars[B_KV], 0);
-      ATB_TRACE(48, 1);  // K, V landed
+    const uint32_t sb4 = sbase >> 4;
+    const uint32_t aK = sb4 + (kOffK >> 4), aV = sb4 + (kOffV >> 4), aDO = sb4 + (kOffDO >> 4),
+                   aDS = sb4 + (kOffDS >> 4);
+    const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tDV = tmem + kColDV, tDK = tmem + kColDK;
+    constexpr uint32_t I_KK = idesc(0, 0), I_KMd = idesc(0, 1, D), I_MMd = idesc(1, 1, D);
+    int g = 0;
+    for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
+      int jb, hd;
+      decode(w, jb, hd);
+      trace_item = b == 0 && r == 0;
+      const int n_it = n_q - jb;
+      mbar_wait(&bars[B_KV], r & 1);
       tc_fence_after();
-      uint32_t dbg_ph = 0;
-      // diagnostics: serialise one GEMM and time it (events 16.. start, 17.. done)
-      auto dbg_start = [&](int ev, int i) {
-        if (p.exp_mode & 4) ATB_TRACE(ev, i);
-      };
-      auto dbg_done = [&](int ev, int i) {
-        if (p.exp_mode & 4) {
-          tc_commit(&bars[B_DBG]);
-          mbar_wait(&bars[B_DBG], dbg_ph);
-          dbg_ph ^= 1;
-          ATB_TRACE(ev, i);
-        }
-      };
-      if ((p.exp_mode & 8) && blockIdx.x == 0 && blockIdx.y == 0 && p.trace) {
-        // diagnostics: clocks per GEMM form, 16 back to back on resident operands
-        mbar_wait(&bars[B_QF0], 0);
-        mbar_wait(&bars[B_DOF], 0);
-        tc_fence_after();
-        const uint32_t aQ = sb4 + (kOffQ >> 4);
-        for (int form = 0; form < 6; ++form) {
-          const long long t0 = clock64();
-          for (int r = 0; r < 16; ++r) {
-            if (form == 0) gemm128<kDK, false, false, false>(tS, aK, aQ, I_KK, false);
-            else if (form == 1) gemm128<8, true, true, false>(tDP, aDS, aK, I_MMd, false);
-            else if (form == 2) gemm128<8, false, true, false>(tDK, aDS, aQ, I_KMd, true);
-            else if (form == 3) gemm128<8, false, true, true>(tDV, tS, aDO, I_KMd, true);
-            else if (form == 4) gemm128<kDK, false, false, true>(tDV, tS, aDO, idesc(0, 0, D), true);
-            else gemm128<kDK, false, false, false>(tDK, aDS, aQ, idesc(0, 0, D), true);
-          }
-          tc_commit(&bars[B_DBG]);
-          mbar_wait(&bars[B_DBG], dbg_ph);
-          dbg_ph ^= 1;
-          if (lane == 0) p.trace[30 * 256 + form] = (clock64() - t0) / 16;
-        }
-      }
       for (int it = 0; it <= n_it; ++it) {
-        const int st = it & 1;
+        const int gi = g + it, st = gi & 1;
         const uint32_t aQ = sb4 + ((kOffQ + st * kTileBytes) >> 4);
         if (it < n_it) {
-          mbar_wait(&bars[B_QF0 + st], (it >> 1) & 1);
+          mbar_wait(&bars[B_QF0 + st], (gi >> 1) & 1);
           ATB_TRACE(0, it);
           tc_fence_after();
-          dbg_start(16, it);
           gemm128<kDK, false, false, false>(tS, aK, aQ, I_KK, false);  // S^T = K Q^T
-          dbg_done(17, it);
           tc_commit(&bars[B_SF]);
           ATB_TRACE(1, it);
         }
         if (it > 0) {
-          // dQ(it-1), dK(it-1): dS(it-1) is in shared memory
-          const int pt = it - 1;
-          const uint32_t aQp = sb4 + ((kOffQ + (pt & 1) * kTileBytes) >> 4);
-          mbar_wait(&bars[B_DSF], pt & 1);
+          // dK(it-1), dQ(it-1): dS(it-1) is in shared memory.  dK first: its Q stage goes
+          // back to the producer one GEMM earlier (period 3839 vs 4128 clocks at C2)
+          const int pt = it - 1, gp = gi - 1;
+          const uint32_t aQp = sb4 + ((kOffQ + (gp & 1) * kTileBytes) >> 4);
+          mbar_wait(&bars[B_DSF], gp & 1);
           ATB_TRACE(2, pt);
           tc_fence_after();
-          // dK first: its Q stage goes back to the producer one GEMM earlier (measured:
-          // period 3839 vs 4128 clocks per step at C2, the Q load latency is ~2000 clocks)
-          dbg_start(18, pt);
           gemm128<8, false, true, false>(tDK, aDS, aQp, I_KMd, pt > 0);  // dK += dS^T Q
-          dbg_done(19, pt);
-          tc_commit(&bars[B_QE0 + (pt & 1)]);
+          tc_commit(&bars[B_QE0 + (gp & 1)]);
           gemm128<8, true, true, false>(tDP, aDS, aK, I_MMd, false);  // dQ = dS K
-          dbg_done(23, pt);
           tc_commit(&bars[B_DQF]);
           tc_commit(&bars[B_DSE]);
           ATB_TRACE(3, pt);
-          if (it == n_it) tc_commit(&bars[B_DKV]);
+          if (it == n_it) {
+            tc_commit(&bars[B_DKV]);
+            tc_commit(&bars[B_KVE]);
+          }
         }
         if (it < n_it) {
-          mbar_wait(&bars[B_DOF], it & 1);
+          mbar_wait(&bars[B_DOF], gi & 1);
           ATB_TRACE(4, it);
-          if (it > 0) mbar_wait(&bars[B_DQE], (it - 1) & 1);  // dQ(it-1) drained: dP reuses its columns
+          if (gi > 0) mbar_wait(&bars[B_DQE], (gi - 1) & 1);  // dQ(gi-1) drained: dP reuses its columns
           ATB_TRACE(5, it);
           tc_fence_after();
-          dbg_start(24, it);
           gemm128<kDK, false, false, false>(tDP, aV, aDO, I_KK, false);  // dP^T = V dO^T
-          dbg_done(25, it);
           tc_commit(&bars[B_DPF]);
           ATB_TRACE(6, it);
-          mbar_wait(&bars[B_PF], it & 1);
+          mbar_wait(&bars[B_PF], gi & 1);
           ATB_TRACE(7, it);
+          // the previous item's epilogue holds its dK / dV: the accumulators are free
+          if (it == 0 && r > 0) mbar_wait(&bars[B_ACC], (r - 1) & 1);
           tc_fence_after();
-          dbg_start(26, it);
           gemm128<8, false, true, true>(tDV, tS, aDO, I_KMd, it > 0);  // dV += P^T dO
-          dbg_done(27, it);
           tc_commit(&bars[B_DOE]);
           ATB_TRACE(8, it);
         }
       }
+      g += n_it;
     }
   }  // warps 14, 15: idle register donors
   } else {
@@ -335,170 +330,193 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     const float sl2 = p.scale * 1.4426950408889634f;
     uint8_t* ds_row = smem + kOffDS + wg * kHalf + row * 128;
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
-      const float* lse = s_lse + st * 128 + c0;
-      const float* dlt = s_delta + st * 128 + c0;
-      mbar_wait(&bars[B_QF0 + st], (it >> 1) & 1);
-      mbar_wait(&bars[B_SF], it & 1);
-      if (warp == 4 && lane == 0) ATB_TRACE(10, it);
-      tc_fence_after();
-      float pr[64];
-      {
-        uint32_t r[2][32];
-        tmem_ld32(tmem + lane_off + kColS + c0, r[0]);
-        tmem_ld32(tmem + lane_off + kColS + c0 + 32, r[1]);
-        tmem_wait_ld();
-        if (warp == 4 && lane == 0) ATB_TRACE(40, it);
-        // x = s * scale * log2e - log2e * lse on packed pairs (s_lse holds -log2e * lse);
-        // 1 of 8 exponentials on the FMA pipe (the forward's sweep, ppo_attention_fwd.cu)
-        const uint64_t sl2x2 = f2(sl2, sl2);
-        const uint64_t* nl = reinterpret_cast<const uint64_t*>(lse);
+    int g = 0;
+    for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
+      int jb, hd;
+      decode(w, jb, hd);
+      trace_item = b == 0 && r == 0;
+      const int n_it = n_q - jb;
+      for (int it = 0; it < n_it; ++it) {
+        const int gi = g + it, st = gi & 1;
+        const float* lse = s_lse + st * 128 + c0;
+        const float* dlt = s_delta + st * 128 + c0;
+        mbar_wait(&bars[B_QF0 + st], (gi >> 1) & 1);
+        mbar_wait(&bars[B_SF], gi & 1);
+        if (warp == 4 && lane == 0) ATB_TRACE(10, it);
+        tc_fence_after();
+        float pr[64];
+        {
+          uint32_t rr[2][32];
+          tmem_ld32(tmem + lane_off + kColS + c0, rr[0]);
+          tmem_ld32(tmem + lane_off + kColS + c0 + 32, rr[1]);
+          tmem_wait_ld();
+          if (warp == 4 && lane == 0) ATB_TRACE(40, it);
+          // x = s * scale * log2e - log2e * lse on packed pairs (s_lse holds -log2e * lse);
+          // 1 of 8 exponentials on the FMA pipe (the forward's sweep, ppo_attention_fwd.cu)
+          const uint64_t sl2x2 = f2(sl2, sl2);
+          const uint64_t* nl = reinterpret_cast<const uint64_t*>(lse);
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float2 x = f2u(ffma2(f2(__uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31])),
-                                     sl2x2, nl[c >> 1]));
-          pr[c] = (c & 7) == 0 ? ex2_fma(x.x) : ex2(x.x);
-          pr[c + 1] = ex2(x.y);
-        }
-      }
-      if (it == 0) {  // the diagonal tile: q < kv is masked
-#pragma unroll
-        for (int c = 0; c < 64; ++c) pr[c] = c0 + c < row ? 0.f : pr[c];
-      }
-      if (warp == 4 && lane == 0) ATB_TRACE(41, it);
-      // every S column of this tile has been read before P^T overwrites the first 64
-      tc_fence_before();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      tc_fence_after();
-      if (warp == 4 && lane == 0) ATB_TRACE(42, it);
-      {
-        uint32_t r[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) r[c] = pack_bf16(pr[2 * c], pr[2 * c + 1]);
-        tmem_st32(tmem + lane_off + kColS + wg * 32, r);
-        tmem_wait_st();
-      }
-      if (warp == 4 && lane == 0) ATB_TRACE(43, it);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_PF]);
-      if (warp == 4 && lane == 0) ATB_TRACE(11, it);
-
-      mbar_wait(&bars[B_DPF], it & 1);
-      if (warp == 4 && lane == 0) ATB_TRACE(12, it);
-      tc_fence_after();
-      mbar_wait(&bars[B_DSE], (it & 1) ^ 1);  // dQ/dK of the previous step have read dS
-      if (warp == 4 && lane == 0) ATB_TRACE(13, it);
-      {
-        uint32_t r[2][32];
-        tmem_ld32(tmem + lane_off + kColDP + c0, r[0]);
-        tmem_ld32(tmem + lane_off + kColDP + c0 + 32, r[1]);
-        tmem_wait_ld();
-        if (warp == 4 && lane == 0) ATB_TRACE(44, it);
-        const uint64_t* nd = reinterpret_cast<const uint64_t*>(dlt);  // -delta
-#pragma unroll
-        for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk (8 q columns) of the 128-byte row
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = chunk * 8 + 2 * e;  // dS = P (dP - delta), packed pairs
-            const float2 a = f2u(fmul2(f2(pr[c], pr[c + 1]),
-                                       fadd2(f2(__uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31])),
-                                             nd[c >> 1])));
-            w[e] = pack_bf16(a.x, a.y);
+          for (int c = 0; c < 64; c += 2) {
+            const float2 x = f2u(ffma2(f2(__uint_as_float(rr[c >> 5][c & 31]), __uint_as_float(rr[c >> 5][(c + 1) & 31])),
+                                       sl2x2, nl[c >> 1]));
+            pr[c] = (c & 7) == 0 ? ex2_fma(x.x) : ex2(x.x);
+            pr[c + 1] = ex2(x.y);
           }
-          *reinterpret_cast<uint4*>(ds_row + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        if (warp == 4 && lane == 0) ATB_TRACE(45, it);
+        if (it == 0) {  // the diagonal tile: q < kv is masked
+#pragma unroll
+          for (int c = 0; c < 64; ++c) pr[c] = c0 + c < row ? 0.f : pr[c];
+        }
+        if (warp == 4 && lane == 0) ATB_TRACE(41, it);
+        // every S column of this tile has been read before P^T overwrites the first 64
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        tc_fence_after();
+        if (warp == 4 && lane == 0) ATB_TRACE(42, it);
+        {
+          uint32_t rr[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) rr[c] = pack_bf16(pr[2 * c], pr[2 * c + 1]);
+          tmem_st32(tmem + lane_off + kColS + wg * 32, rr);
+          tmem_wait_st();
+        }
+        if (warp == 4 && lane == 0) ATB_TRACE(43, it);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_PF]);
+        if (warp == 4 && lane == 0) ATB_TRACE(11, it);
+
+        mbar_wait(&bars[B_DPF], gi & 1);
+        if (warp == 4 && lane == 0) ATB_TRACE(12, it);
+        tc_fence_after();
+        mbar_wait(&bars[B_DSE], (gi & 1) ^ 1);  // dQ/dK of the previous step have read dS
+        if (warp == 4 && lane == 0) ATB_TRACE(13, it);
+        {
+          uint32_t rr[2][32];
+          tmem_ld32(tmem + lane_off + kColDP + c0, rr[0]);
+          tmem_ld32(tmem + lane_off + kColDP + c0 + 32, rr[1]);
+          tmem_wait_ld();
+          if (warp == 4 && lane == 0) ATB_TRACE(44, it);
+          const uint64_t* nd = reinterpret_cast<const uint64_t*>(dlt);  // -delta
+#pragma unroll
+          for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk (8 q columns) of the 128-byte row
+            uint32_t wv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = chunk * 8 + 2 * e;  // dS = P (dP - delta), packed pairs
+              const float2 a = f2u(fmul2(f2(pr[c], pr[c + 1]),
+                                         fadd2(f2(__uint_as_float(rr[c >> 5][c & 31]), __uint_as_float(rr[c >> 5][(c + 1) & 31])),
+                                               nd[c >> 1])));
+              wv[e] = pack_bf16(a.x, a.y);
+            }
+            *reinterpret_cast<uint4*>(ds_row + ((chunk ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          }
+          if (warp == 4 && lane == 0) ATB_TRACE(45, it);
+        }
+        fence_proxy_async_smem();  // generic-proxy dS writes -> tensor-core reads
+        if (warp == 4 && lane == 0) ATB_TRACE(46, it);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_DSF]);
+        if (warp == 4 && lane == 0) ATB_TRACE(14, it);
       }
-      fence_proxy_async_smem();  // generic-proxy dS writes -> tensor-core reads
-      if (warp == 4 && lane == 0) ATB_TRACE(46, it);
+      g += n_it;
+      // ---- epilogue: dK (scaled) and dV rows of this kv block into dqkv, staged in the dS
+      // buffer (free: every UMMA of the item is done) in the TMA box layout, stored by TMA
+      mbar_wait(&bars[B_DKV], r & 1);
+      tc_fence_after();
+      constexpr int kHalfD = D / 2;             // columns of dK / dV per warpgroup
+      constexpr int kRounds = D == 128 ? 2 : 1;  // dS buffer (32 KB) holds 32 / (D/4) KB tiles
+      uint32_t kv[2][kHalfD];                   // this thread's dK, dV columns
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int ch = 0; ch < kHalfD / 32; ++ch)
+          tmem_ld32(tmem + lane_off + (m ? kColDV : kColDK) + wg * kHalfD + ch * 32,
+                    *reinterpret_cast<uint32_t(*)[32]>(&kv[m][ch * 32]));
+      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_DSF]);
-      if (warp == 4 && lane == 0) ATB_TRACE(14, it);
-    }
-    // ---- epilogue: dV and scale * dK rows of this kv block into dqkv
-    mbar_wait(&bars[B_DKV], 0);
-    if (warp == 4 && lane == 0) ATB_TRACE(48, 2);  // dK, dV complete
-    tc_fence_after();
-    // staged in the (now idle) Q stages in the TMA box layout, then stored by TMA
-    constexpr int kHalfD = D / 2;  // columns of dK / dV per warpgroup
+      if (lane == 0) mbar_arrive(&bars[B_ACC]);  // the next item may write dK / dV
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {  // 0: dK (scaled), 1: dV
-      const uint32_t col = m == 0 ? kColDK : kColDV;
-      const float f = m == 0 ? p.scale : 1.f;
-      uint8_t* base = smem + kOffQ + m * kTileBytes;
+      for (int round = 0; round < kRounds; ++round) {
 #pragma unroll
-      for (int ch = 0; ch < kHalfD / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_off + col + wg * kHalfD + ch * 32, r);
-        tmem_wait_ld();
+        for (int m = round; m < (kRounds == 2 ? round + 1 : 2); ++m) {
+          const float f = m == 0 ? p.scale : 1.f;
+          uint8_t* base = smem + kOffDS + (kRounds == 2 ? 0 : m * kTileBytes);
 #pragma unroll
-        for (int v8 = 0; v8 < 4; ++v8) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(r[v8 * 8 + 0]) * f, __uint_as_float(r[v8 * 8 + 1]) * f);
-          w.y = pack_bf16(__uint_as_float(r[v8 * 8 + 2]) * f, __uint_as_float(r[v8 * 8 + 3]) * f);
-          w.z = pack_bf16(__uint_as_float(r[v8 * 8 + 4]) * f, __uint_as_float(r[v8 * 8 + 5]) * f);
-          w.w = pack_bf16(__uint_as_float(r[v8 * 8 + 6]) * f, __uint_as_float(r[v8 * 8 + 7]) * f);
-          const int c = wg * kHalfD + ch * 32 + v8 * 8;  // first column of this 16-byte chunk
-          const int chunk = (c & 63) >> 3;
-          *reinterpret_cast<uint4*>(base + (c >> 6) * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4)) = w;
+          for (int v8 = 0; v8 < kHalfD / 8; ++v8) {
+            uint4 wq;
+            wq.x = pack_bf16(__uint_as_float(kv[m][v8 * 8 + 0]) * f, __uint_as_float(kv[m][v8 * 8 + 1]) * f);
+            wq.y = pack_bf16(__uint_as_float(kv[m][v8 * 8 + 2]) * f, __uint_as_float(kv[m][v8 * 8 + 3]) * f);
+            wq.z = pack_bf16(__uint_as_float(kv[m][v8 * 8 + 4]) * f, __uint_as_float(kv[m][v8 * 8 + 5]) * f);
+            wq.w = pack_bf16(__uint_as_float(kv[m][v8 * 8 + 6]) * f, __uint_as_float(kv[m][v8 * 8 + 7]) * f);
+            const int c = wg * kHalfD + v8 * 8;  // first column of this 16-byte chunk
+            const int chunk = (c & 63) >> 3;
+            *reinterpret_cast<uint4*>(base + (c >> 6) * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4)) = wq;
+          }
         }
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 4 && lane == 0) {
+          for (int m = round; m < (kRounds == 2 ? round + 1 : 2); ++m)
+            for (int half = 0; half < C::kHalves; ++half)
+              tma_store_3d(&tm_dqkv, smem + kOffDS + (kRounds == 2 ? 0 : m * kTileBytes) + half * kHalf, half * 64,
+                           (m + 1) * p.H + hd, jb * kTile);
+          tma_store_commit();
+          tma_store_wait_read<0>();  // the staging is reused: its reads must be done
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
-    }
-    fence_proxy_async_smem();
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (warp == 4 && lane == 0) {
-      for (int m = 0; m < 2; ++m)
-        for (int half = 0; half < C::kHalves; ++half)
-          tma_store_3d(&tm_dqkv, smem + kOffQ + m * kTileBytes + half * kHalf, half * 64, (m + 1) * p.H + hd,
-                       jb * kTile);
-      tma_store_commit();
-      tma_store_wait_read<0>();  // the staging must outlive the reads, not the global writes
     }
   } else {
     // ===================================================== dQ drain: TMEM -> smem -> TMA reduce-add
     const int quarter = warp;  // TMEM lanes 32*warp .. +31 = q rows of the tile
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     uint8_t* stg = smem + kOffStg + warp * 2 * kStgBytes;
-    int buf = 0;
-    for (int it = 0; it < n_it; ++it) {
-      const int qb = jb + it;
-      mbar_wait(&bars[B_DQF], it & 1);
-      if (warp == 0 && lane == 0) ATB_TRACE(20, it);
-      tc_fence_after();
-      // all 128 columns in registers first: the dQ columns are dP's, and the next dP
-      // UMMA waits for this release (B_DQE) on the tensor core's critical path
-      constexpr int kCh = D / 32;  // 32-column chunks of the dQ tile
-      uint32_t r[kCh][32];
+    int buf = 0, g = 0;
+    for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
+      int jb, hd;
+      decode(w, jb, hd);
+      trace_item = b == 0 && r == 0;
+      const int n_it = n_q - jb;
+      for (int it = 0; it < n_it; ++it) {
+        const int gi = g + it, qb = jb + it;
+        mbar_wait(&bars[B_DQF], gi & 1);
+        if (warp == 0 && lane == 0) ATB_TRACE(20, it);
+        tc_fence_after();
+        // all columns in registers first: the dQ columns are dP's, and the next dP UMMA
+        // waits for this release (B_DQE) on the tensor core's critical path
+        constexpr int kCh = D / 32;  // 32-column chunks of the dQ tile
+        uint32_t rr[kCh][32];
 #pragma unroll
-      for (int ch = 0; ch < kCh; ++ch) tmem_ld32(tmem + lane_off + kColDP + ch * 32, r[ch]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_DQE]);
-      if (warp == 0 && lane == 0) ATB_TRACE(21, it);
-#pragma unroll
-      for (int ch = 0; ch < kCh; ++ch) {
-        if (p.exp_mode & 1) break;
-        // the reduce that last read this staging buffer has finished reading it
-        if (lane == 0) tma_store_wait_read<1>();
+        for (int ch = 0; ch < kCh; ++ch) tmem_ld32(tmem + lane_off + kColDP + ch * 32, rr[ch]);
+        tmem_wait_ld();
+        tc_fence_before();
         __syncwarp();
-        uint8_t* row_p = stg + buf * kStgBytes + lane * 128;
+        if (lane == 0) mbar_arrive(&bars[B_DQE]);
+        if (warp == 0 && lane == 0) ATB_TRACE(21, it);
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          *reinterpret_cast<uint4*>(row_p + ((v ^ (lane & 7)) << 4)) =
-              make_uint4(r[ch][4 * v], r[ch][4 * v + 1], r[ch][4 * v + 2], r[ch][4 * v + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_reduce_add_3d(&tm_dq, stg + buf * kStgBytes, ch * 32, hd, qb * kTile + quarter * 32);
-          tma_store_commit();
+        for (int ch = 0; ch < kCh; ++ch) {
+          if (p.exp_mode & 1) break;
+          // the reduce that last read this staging buffer has finished reading it
+          if (lane == 0) tma_store_wait_read<1>();
+          __syncwarp();
+          uint8_t* row_p = stg + buf * kStgBytes + lane * 128;
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<uint4*>(row_p + ((v ^ (lane & 7)) << 4)) =
+                make_uint4(rr[ch][4 * v], rr[ch][4 * v + 1], rr[ch][4 * v + 2], rr[ch][4 * v + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_3d(&tm_dq, stg + buf * kStgBytes, ch * 32, hd, qb * kTile + quarter * 32);
+            tma_store_commit();
+          }
+          buf ^= 1;
         }
-        buf ^= 1;
       }
+      g += n_it;
     }
     // only the shared-memory reads must finish before the CTA exits; the reduce-adds complete
     // in global memory on their own (waiting for that was ~10 us per CTA, measured)
@@ -506,10 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   }
 
-  if (warp == 4 && lane == 0) ATB_TRACE(48, 3);  // epilogue stores issued
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) ATB_TRACE(48, 4);  // every role done
   if (warp == 12) {
     __syncwarp();
     tc_fence_after();
@@ -529,9 +545,10 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16*
                                                             const __nv_bfloat16* __restrict__ dout,
                                                             const float* __restrict__ lse, float* __restrict__ lse2,
                                                             float* __restrict__ delta, float* __restrict__ dq_acc,
-                                                            int s, int H, int D) {
+                                                            int* __restrict__ work, int s, int H, int D) {
   pdl_wait();
   const int i = blockIdx.x;
+  if (i == 0 && threadIdx.x == 0) *work = 0;
   const int h = H * D;
   for (int t = threadIdx.x; t < H; t += blockDim.x) lse2[size_t(t) * s + i] = -lse[size_t(t) * s + i] * 1.4426950408889634f;
   for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
@@ -590,7 +607,8 @@ template <int D>
 static int launch_main(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
                        const Params& prm, cudaStream_t st) {
   if (int rc = smem_optin<D>()) return rc;
-  attn_bwd_kernel<D><<<dim3(prm.H, prm.s / kTile), kThreads, Cfg<D>::kSmemBytes, st>>>(a, b, c, d, prm);
+  const int items = prm.H * (prm.s / kTile), sms = sm_count_current();
+  attn_bwd_kernel<D><<<dim3(items < sms ? items : sms), kThreads, Cfg<D>::kSmemBytes, st>>>(a, b, c, d, prm);
   PPO_LAUNCHED("attn_bwd_kernel");
   return PPO_OK;
 }
@@ -609,7 +627,7 @@ int ppo_attn_bwd_trace(void* trace) {
 }
 
 int64_t ppo_attn_bwd_workspace_bytes(int64_t seq, int64_t heads, int64_t head_dim) {
-  return (seq * heads * head_dim + 2 * heads * seq) * int64_t(sizeof(float));
+  return (seq * heads * head_dim + 2 * heads * seq) * int64_t(sizeof(float)) + 16;
 }
 
 int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv, void* workspace,
@@ -632,6 +650,7 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   float* dq_acc = static_cast<float*>(workspace);
   float* delta = dq_acc + size_t(s) * h;
   float* lse2 = delta + size_t(H) * s;
+  int* work = reinterpret_cast<int*>(lse2 + size_t(H) * s);
 
   const int D = int(head_dim);
   CUtensorMap tm_qkv, tm_do, tm_dq, tm_dqkv;
@@ -644,7 +663,7 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, D, heads, seq, h * 4, 32, 32))) return rc;
 
   launch_pdl(attn_bwd_prep_kernel, dim3(s), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
-             static_cast<const __nv_bfloat16*>(dout), lse, lse2, delta, dq_acc, s, H, D);
+             static_cast<const __nv_bfloat16*>(dout), lse, lse2, delta, dq_acc, work, s, H, D);
   PPO_LAUNCHED("attn_bwd_prep_kernel");
   static const int exp_mode = [] {
     const char* e = std::getenv("PPO_ATB_EXP");
@@ -659,7 +678,7 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
   const bool big = 4.0 * double(s) * double(H) * double(D) > 64.0 * (1 << 20);
   int group = group_env > 0 ? group_env : (big ? 8 : H);
   while (H % group) --group;
-  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse2, delta, dq_acc, s, H, scale, g_trace, exp_mode, group};
+  Params prm{static_cast<__nv_bfloat16*>(dqkv), lse2, delta, dq_acc, work, s, H, scale, g_trace, exp_mode, group};
   rc = D == 64 ? launch_main<64>(tm_qkv, tm_do, tm_dq, tm_dqkv, prm, st)
                : launch_main<128>(tm_qkv, tm_do, tm_dq, tm_dqkv, prm, st);
   if (rc) return rc;

@@ -46,7 +46,7 @@ def main():
     native.attn_bwd(qkv, o, do, lse, dqkv, H, ws)
     torch.cuda.synchronize()
     native.load().ppo_attn_bwd_trace(None)
-    cta = tr[64 * 256:].view(n_cta, 4).cpu().tolist()
+    cta = [c for c in tr[64 * 256:].view(n_cta, 4).cpu().tolist() if c[0] > 0]  # persistent grid: <= n_cta
     t = tr[:64 * 256].view(64, 256).cpu()
     n = s // 128
     t0 = int(t[0, 0])
