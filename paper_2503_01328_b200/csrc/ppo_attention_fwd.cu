@@ -19,6 +19,7 @@
 // Warps: 0-3 softmax of q block i0, 4-7 of i1, 8 UMMA issue (converged, one lane issues),
 // 9 TMA producer, 10-11 register donors (setmaxnreg).
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "ppo_common.cuh"
@@ -43,20 +44,24 @@ struct Cfg {
   static constexpr int kOffQ = 0;                      // q0, q1
   static constexpr int kOffKV = 2 * kTileBytes;        // 2 stages x (K, V)
   static constexpr int kOffBar = kOffKV + 4 * kTileBytes;
-  static constexpr int kNumBars = 16;
+  static constexpr int kNumBars = 24;
   static constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
-  static constexpr int kSmemBytes = kOffTmemPtr + 8;
+  static constexpr int kOffItems = kOffTmemPtr + 16;  // 4 work-item slots
+  static constexpr int kSmemBytes = kOffItems + 16;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
 };
 
 enum : int {
-  B_Q = 0,
+  B_Q = 0,     // Q of the current item landed
   B_KVF0 = 1,  // kv full[2]
   B_KVE0 = 3,  // kv empty[2]
   B_SF0 = 5,   // S full[2] (q block 0 / 1)
   B_PF0 = 7,   // P full[2]
   B_OD0 = 9,   // O done[2]: the PV of the last issued step has completed
+  B_QE = 11,   // Q of the item no longer read (its last S issued and done)
+  B_OE0 = 12,  // O[2] read by the item's epilogue: the next item may accumulate
+  B_ITEM0 = 14,  // item slot full[4]
 };
 
 struct Params {
@@ -64,14 +69,15 @@ struct Params {
   float* lse;  // [H, s] natural log
   int s, H;
   float scale;
-  long long* trace;  // diagnostics: per-event SM clocks of the heaviest CTA of head 0, or null
+  long long* trace;  // diagnostics: per-event SM clocks of CTA 0's first item, or null
   int head_group;    // heads walked together (dispatch order), divides H
+  int* work;         // [2]: work counter, finished CTAs (the last one resets both)
 };
 
 // diagnostics (ppo_attn_fwd_trace): event e of step j at trace[e * 256 + j]
 #define ATF_TRACE(e, j)                                                                          \
   do {                                                                                           \
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 256) p.trace[(e) * 256 + (j)] = clock64(); \
+    if (p.trace && trace_item && (j) < 256) p.trace[(e) * 256 + (j)] = clock64();           \
   } while (0)
 
 template <int D>
@@ -83,28 +89,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kPolyPer8 = PPO_FWD_POLY;  // exponentials per 8 on the FMA pipe, the rest on the SFU
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // dispatch order: groups of head_group heads; inside a group the heaviest q-block pairs
-  // first (the in-order dispatch is then an LPT schedule), heads innermost, so concurrent
-  // CTAs share the K / V tiles of a few heads in L2 (C4: 40 heads x 16 MB of K, V)
-  const int n_pairs = p.s / (2 * kTile);
-  const int lin = int(blockIdx.y) * int(gridDim.x) + int(blockIdx.x);
-  const int per_group = p.head_group * n_pairs, grp = lin / per_group, rem = lin % per_group;
-  const int hd = grp * p.head_group + rem % p.head_group;
-  const int pair = n_pairs - 1 - rem / p.head_group;
-  const int i0 = 2 * pair;
-  const int n0 = i0 + 1, n1 = i0 + 2;  // kv blocks walked by q block i0 / i1
+  // Persistent: work item w = (q-block pair, head) in dispatch order -- groups of head_group
+  // heads, the heaviest pairs first inside a group, heads innermost, so concurrent CTAs share
+  // the K / V tiles of a few heads in L2 (C4: 40 heads x 16 MB of K, V) -- taken from a global
+  // counter when the CTA's producer gets to it (greedy longest first), handed to the other
+  // roles through a 4-slot shared-memory ring.  The next item's Q and first K/V land while
+  // the previous item's O leaves.
+  const int n_pairs = p.s / (2 * kTile), n_items = p.H * n_pairs;
+  auto decode = [&](int w, int& i0, int& hd) {
+    const int per_group = p.head_group * n_pairs, grp = w / per_group, rem = w % per_group;
+    hd = grp * p.head_group + rem % p.head_group;
+    i0 = 2 * (n_pairs - 1 - rem / p.head_group);
+  };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::kOffTmemPtr);
+  volatile int* item_slot = reinterpret_cast<volatile int*>(smem + C::kOffItems);
+  auto next_item = [&](int r) {  // consumers: item of round r, -1 when the CTA is done
+    mbar_wait(&bars[B_ITEM0 + (r & 3)], (r >> 2) & 1);
+    return item_slot[r & 3];
+  };
+  bool trace_item = false;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
+    mbar_init(&bars[B_QE], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars[B_KVF0 + i], 1);
       mbar_init(&bars[B_KVE0 + i], 1);
       mbar_init(&bars[B_SF0 + i], 1);
       mbar_init(&bars[B_PF0 + i], 4);
       mbar_init(&bars[B_OD0 + i], 1);
+      mbar_init(&bars[B_OE0 + i], 4);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[B_ITEM0 + i], 1);
     mbar_fence_init();
   }
   if (warp == 8) {
@@ -125,20 +142,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===================================================== TMA producer
       if (lane == 0) {
         const int H = p.H;
-        mbar_expect_tx(&bars[B_Q], 2 * kTileBytes);
-        for (int q = 0; q < 2; ++q)
-          for (int half = 0; half < C::kHalves; ++half)
-            tma_load_3d(smem + C::kOffQ + q * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd,
-                        (i0 + q) * kTile, &bars[B_Q]);
-        for (int j = 0; j < n1; ++j) {
-          const int st = j & 1;
-          mbar_wait(&bars[B_KVE0 + st], ((j >> 1) & 1) ^ 1);
-          mbar_expect_tx(&bars[B_KVF0 + st], 2 * kTileBytes);
-          uint8_t* kv = smem + C::kOffKV + st * 2 * kTileBytes;
-          for (int half = 0; half < C::kHalves; ++half) {
-            tma_load_3d(kv + half * kHalf, &tm_qkv, half * 64, H + hd, j * kTile, &bars[B_KVF0 + st]);
-            tma_load_3d(kv + kTileBytes + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, j * kTile,
-                        &bars[B_KVF0 + st]);
+        int gk = 0;  // kv tiles loaded so far (ring index)
+        for (int r = 0;; ++r) {
+          int w = atomicAdd(&p.work[0], 1);
+          w = w < n_items ? w : -1;
+          item_slot[r & 3] = w;
+          mbar_arrive(&bars[B_ITEM0 + (r & 3)]);
+          if (w < 0) break;
+          int i0, hd;
+          decode(w, i0, hd);
+          mbar_wait(&bars[B_QE], (r & 1) ^ 1);  // the previous item's last S is done
+          mbar_expect_tx(&bars[B_Q], 2 * kTileBytes);
+          for (int q = 0; q < 2; ++q)
+            for (int half = 0; half < C::kHalves; ++half)
+              tma_load_3d(smem + C::kOffQ + q * kTileBytes + half * kHalf, &tm_qkv, half * 64, hd,
+                          (i0 + q) * kTile, &bars[B_Q]);
+          for (int j = 0; j < i0 + 2; ++j, ++gk) {
+            const int st = gk & 1;
+            mbar_wait(&bars[B_KVE0 + st], ((gk >> 1) & 1) ^ 1);
+            mbar_expect_tx(&bars[B_KVF0 + st], 2 * kTileBytes);
+            uint8_t* kv = smem + C::kOffKV + st * 2 * kTileBytes;
+            for (int half = 0; half < C::kHalves; ++half) {
+              tma_load_3d(kv + half * kHalf, &tm_qkv, half * 64, H + hd, j * kTile, &bars[B_KVF0 + st]);
+              tma_load_3d(kv + kTileBytes + half * kHalf, &tm_qkv, half * 64, 2 * H + hd, j * kTile,
+                          &bars[B_KVF0 + st]);
+            }
           }
         }
       }
@@ -149,44 +177,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tS0 = tmem + C::kColS0, tS1 = tmem + C::kColS1, tO0 = tmem + C::kColO0,
                      tO1 = tmem + C::kColO1;
       constexpr uint32_t I_S = idesc(0, 0, 128), I_PV = idesc(0, 1, D);
-      auto aK = [&](int j) { return sb4 + ((C::kOffKV + (j & 1) * 2 * kTileBytes) >> 4); };
-      auto aV = [&](int j) { return sb4 + ((C::kOffKV + (j & 1) * 2 * kTileBytes + kTileBytes) >> 4); };
-      auto kv_wait = [&](int j) { mbar_wait(&bars[B_KVF0 + (j & 1)], (j >> 1) & 1); };
-      mbar_wait(&bars[B_Q], 0);
-      kv_wait(0);
-      tc_fence_after();
-      gemm128<kDK, false, false, false>(tS0, aQ0, aK(0), I_S, false);  // S0(0)
-      tc_commit(&bars[B_SF0]);
-      gemm128<kDK, false, false, false>(tS1, aQ1, aK(0), I_S, false);  // S1(0)
-      tc_commit(&bars[B_SF0 + 1]);
-      for (int j = 0; j < n1; ++j) {
-        ATF_TRACE(0, j);
-        if (j < n0) {  // O0 += P0(j) V_j
-          mbar_wait(&bars[B_PF0], j & 1);
-          ATF_TRACE(1, j);
-          tc_fence_after();
-          gemm128<8, false, true, true>(tO0, tS0, aV(j), I_PV, j > 0);
-          tc_commit(&bars[B_OD0]);
-        }
-        if (j + 1 < n0) {  // S0(j+1): P0(j) in the same columns was read by the PV just issued
-          kv_wait(j + 1);
-          tc_fence_after();
-          gemm128<kDK, false, false, false>(tS0, aQ0, aK(j + 1), I_S, false);
-          tc_commit(&bars[B_SF0]);
-        }
-        ATF_TRACE(2, j);
-        mbar_wait(&bars[B_PF0 + 1], j & 1);  // O1 += P1(j) V_j
-        ATF_TRACE(3, j);
+      int gk = 0, g0 = 0, g1 = 0;  // kv tiles, PV steps of q block 0 / 1 (barrier phases)
+      auto aK = [&](int k) { return sb4 + ((C::kOffKV + (k & 1) * 2 * kTileBytes) >> 4); };
+      auto aV = [&](int k) { return sb4 + ((C::kOffKV + (k & 1) * 2 * kTileBytes + kTileBytes) >> 4); };
+      auto kv_wait = [&](int k) { mbar_wait(&bars[B_KVF0 + (k & 1)], (k >> 1) & 1); };
+      for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
+        int i0, hd;
+        decode(w, i0, hd);
+        trace_item = blockIdx.x == 0 && r == 0;
+        const int n0 = i0 + 1, n1 = i0 + 2;
+        mbar_wait(&bars[B_Q], r & 1);
+        kv_wait(gk);
         tc_fence_after();
-        gemm128<8, false, true, true>(tO1, tS1, aV(j), I_PV, j > 0);
-        tc_commit(&bars[B_OD0 + 1]);
-        tc_commit(&bars[B_KVE0 + (j & 1)]);  // K_j, V_j consumed
-        if (j + 1 < n1) {
-          kv_wait(j + 1);
+        gemm128<kDK, false, false, false>(tS0, aQ0, aK(gk), I_S, false);  // S0(0)
+        tc_commit(&bars[B_SF0]);
+        gemm128<kDK, false, false, false>(tS1, aQ1, aK(gk), I_S, false);  // S1(0)
+        tc_commit(&bars[B_SF0 + 1]);
+        for (int j = 0; j < n1; ++j) {
+          const int k = gk + j;
+          ATF_TRACE(0, j);
+          if (j < n0) {  // O0 += P0(j) V_j
+            mbar_wait(&bars[B_PF0], (g0 + j) & 1);
+            ATF_TRACE(1, j);
+            if (j == 0 && r > 0) mbar_wait(&bars[B_OE0], (r - 1) & 1);  // previous item's O0 read
+            tc_fence_after();
+            gemm128<8, false, true, true>(tO0, tS0, aV(k), I_PV, j > 0);
+            tc_commit(&bars[B_OD0]);
+          }
+          if (j + 1 < n0) {  // S0(j+1): P0(j) in the same columns was read by the PV just issued
+            kv_wait(k + 1);
+            tc_fence_after();
+            gemm128<kDK, false, false, false>(tS0, aQ0, aK(k + 1), I_S, false);
+            tc_commit(&bars[B_SF0]);
+          }
+          ATF_TRACE(2, j);
+          mbar_wait(&bars[B_PF0 + 1], (g1 + j) & 1);  // O1 += P1(j) V_j
+          ATF_TRACE(3, j);
+          if (j == 0 && r > 0) mbar_wait(&bars[B_OE0 + 1], (r - 1) & 1);
           tc_fence_after();
-          gemm128<kDK, false, false, false>(tS1, aQ1, aK(j + 1), I_S, false);
-          tc_commit(&bars[B_SF0 + 1]);
+          gemm128<8, false, true, true>(tO1, tS1, aV(k), I_PV, j > 0);
+          tc_commit(&bars[B_OD0 + 1]);
+          tc_commit(&bars[B_KVE0 + (k & 1)]);  // K_j, V_j consumed
+          if (j + 1 < n1) {
+            kv_wait(k + 1);
+            tc_fence_after();
+            gemm128<kDK, false, false, false>(tS1, aQ1, aK(k + 1), I_S, false);
+            tc_commit(&bars[B_SF0 + 1]);
+          } else {
+            tc_commit(&bars[B_QE]);  // every S of the item issued: Q may be replaced
+          }
         }
+        gk += n1;
+        g0 += n0;
+        g1 += n1;
       }
     }
     // warps 10, 11: idle register donors
@@ -195,119 +238,127 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================================================== softmax warpgroups
     const int wg = warp >> 2, quarter = warp & 3;
     const int row = quarter * 32 + lane;  // q row within the block (TMEM lane)
-    const int qi = i0 + wg, nk = qi + 1;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_off + (wg ? C::kColS1 : C::kColS0);
     const uint32_t tO = tmem + lane_off + (wg ? C::kColO1 : C::kColO0);
     const float sl2 = p.scale * 1.4426950408889634f;
-    float m = -INFINITY, l = 0.f;  // running max (log2 domain, already scaled) and sum
-    for (int j = 0; j < nk; ++j) {
-      mbar_wait(&bars[B_SF0 + wg], j & 1);
-      if (quarter == 0 && lane == 0) ATF_TRACE(10 + 4 * wg, j);
-      tc_fence_after();
-      uint32_t r[4][32];
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) tmem_ld32(tS + ch * 32, r[ch]);
-      tmem_wait_ld();
-      if (j == qi) {  // the diagonal block: kv column c > q row is masked
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > row) r[c >> 5][c & 31] = __float_as_uint(-INFINITY);
-      }
-      float mx;
-      {
-        float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 128; c += 8) {
-          a0 = fmax3(a0, __uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31]));
-          a1 = fmax3(a1, __uint_as_float(r[c >> 5][(c + 2) & 31]), __uint_as_float(r[c >> 5][(c + 3) & 31]));
-          a2 = fmax3(a2, __uint_as_float(r[c >> 5][(c + 4) & 31]), __uint_as_float(r[c >> 5][(c + 5) & 31]));
-          a3 = fmax3(a3, __uint_as_float(r[c >> 5][(c + 6) & 31]), __uint_as_float(r[c >> 5][(c + 7) & 31]));
-        }
-        mx = fmax3(a0, a1, fmaxf(a2, a3));
-      }
-      const float m_new = fmaxf(m, mx * sl2);
-      // move the maximum only when it grows by more than 8 (P stays <= 2^8 otherwise)
-      const bool move = m_new > m + 8.f;
-      const float alpha = move ? ex2(m - m_new) : 1.f;
-      if (move) m = m_new;
-      // x = s * scale * log2e - m on packed pairs; 3 of 8 exponentials on the FMA pipe
-      // (not in the diagonal step, whose masked -inf scores go through the SFU)
-      const uint64_t sl2x2 = f2(sl2, sl2), nm2 = f2(-m, -m);
-      uint64_t sum2 = f2(0.f, 0.f);
-      uint32_t pk[64];
-      auto exps = [&](auto poly) {  // poly: std::true_type off the diagonal
-#pragma unroll
-        for (int c = 0; c < 128; c += 2) {
-          const float2 x = f2u(ffma2(f2(__uint_as_float(r[c >> 5][c & 31]), __uint_as_float(r[c >> 5][(c + 1) & 31])),
-                                     sl2x2, nm2));
-          float2 e;
-          if (decltype(poly)::value && (c & 7) < 2 * (kPolyPer8 / 2)) {
-            e = ex2_fma2(x.x, x.y);
-          } else if (decltype(poly)::value && (c & 7) == 2 * (kPolyPer8 / 2) && (kPolyPer8 & 1)) {
-            e = make_float2(ex2_fma(x.x), ex2(x.y));
-          } else {
-            e = make_float2(ex2(x.x), ex2(x.y));
-          }
-          sum2 = fadd2(sum2, f2(e.x, e.y));
-          pk[c >> 1] = pack_bf16(e.x, e.y);
-        }
-      };
-      if (j == qi) exps(std::false_type{});  // masked -inf scores go through the SFU
-      else exps(std::true_type{});
-      const float2 sp = f2u(sum2);
-      const float sum = sp.x + sp.y;
-      l = l * alpha + sum;
-      if (quarter == 0 && lane == 0) ATF_TRACE(11 + 4 * wg, j);
-      // O rescale (rows whose maximum moved) once the previous PV of this block is done
-      if (j > 0 && __any_sync(0xffffffffu, move)) {
-        mbar_wait(&bars[B_OD0 + wg], (j - 1) & 1);
+    int gs = 0;  // steps of this q block in earlier items (barrier phases)
+    for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
+      int i0, hd;
+      decode(w, i0, hd);
+      trace_item = blockIdx.x == 0 && r == 0;
+      const int qi = i0 + wg, nk = qi + 1;
+      float m = -INFINITY, l = 0.f;  // running max (log2 domain, already scaled) and sum
+      for (int j = 0; j < nk; ++j) {
+        const int gj = gs + j;
+        mbar_wait(&bars[B_SF0 + wg], gj & 1);
+        if (quarter == 0 && lane == 0) ATF_TRACE(10 + 4 * wg, j);
         tc_fence_after();
+        uint32_t rr[4][32];
 #pragma unroll
-        for (int ch = 0; ch < D / 32; ++ch) {
-          uint32_t o[32];
-          tmem_ld32(tO + ch * 32, o);
-          tmem_wait_ld();
+        for (int ch = 0; ch < 4; ++ch) tmem_ld32(tS + ch * 32, rr[ch]);
+        tmem_wait_ld();
+        if (j == qi) {  // the diagonal block: kv column c > q row is masked
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-          tmem_st32(tO + ch * 32, o);
+          for (int c = 0; c < 128; ++c)
+            if (c > row) rr[c >> 5][c & 31] = __float_as_uint(-INFINITY);
         }
+        float mx;
+        {
+          float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 128; c += 8) {
+            a0 = fmax3(a0, __uint_as_float(rr[c >> 5][c & 31]), __uint_as_float(rr[c >> 5][(c + 1) & 31]));
+            a1 = fmax3(a1, __uint_as_float(rr[c >> 5][(c + 2) & 31]), __uint_as_float(rr[c >> 5][(c + 3) & 31]));
+            a2 = fmax3(a2, __uint_as_float(rr[c >> 5][(c + 4) & 31]), __uint_as_float(rr[c >> 5][(c + 5) & 31]));
+            a3 = fmax3(a3, __uint_as_float(rr[c >> 5][(c + 6) & 31]), __uint_as_float(rr[c >> 5][(c + 7) & 31]));
+          }
+          mx = fmax3(a0, a1, fmaxf(a2, a3));
+        }
+        const float m_new = fmaxf(m, mx * sl2);
+        // move the maximum only when it grows by more than 8 (P stays <= 2^8 otherwise)
+        const bool move = m_new > m + 8.f;
+        const float alpha = move ? ex2(m - m_new) : 1.f;
+        if (move) m = m_new;
+        // x = s * scale * log2e - m on packed pairs; a share of the exponentials on the FMA
+        // pipe (not in the diagonal step, whose masked -inf scores go through the SFU)
+        const uint64_t sl2x2 = f2(sl2, sl2), nm2 = f2(-m, -m);
+        uint64_t sum2 = f2(0.f, 0.f);
+        uint32_t pk[64];
+        auto exps = [&](auto poly) {  // poly: std::true_type off the diagonal
+#pragma unroll
+          for (int c = 0; c < 128; c += 2) {
+            const float2 x = f2u(ffma2(f2(__uint_as_float(rr[c >> 5][c & 31]), __uint_as_float(rr[c >> 5][(c + 1) & 31])),
+                                       sl2x2, nm2));
+            float2 e;
+            if (decltype(poly)::value && (c & 7) < 2 * (kPolyPer8 / 2)) {
+              e = ex2_fma2(x.x, x.y);
+            } else if (decltype(poly)::value && (c & 7) == 2 * (kPolyPer8 / 2) && (kPolyPer8 & 1)) {
+              e = make_float2(ex2_fma(x.x), ex2(x.y));
+            } else {
+              e = make_float2(ex2(x.x), ex2(x.y));
+            }
+            sum2 = fadd2(sum2, f2(e.x, e.y));
+            pk[c >> 1] = pack_bf16(e.x, e.y);
+          }
+        };
+        if (j == qi) exps(std::false_type{});  // masked -inf scores go through the SFU
+        else exps(std::true_type{});
+        const float2 sp = f2u(sum2);
+        l = l * alpha + (sp.x + sp.y);
+        if (quarter == 0 && lane == 0) ATF_TRACE(11 + 4 * wg, j);
+        // O rescale (rows whose maximum moved) once the previous PV of this block is done
+        if (j > 0 && __any_sync(0xffffffffu, move)) {
+          mbar_wait(&bars[B_OD0 + wg], (gj - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int ch = 0; ch < D / 32; ++ch) {
+            uint32_t o[32];
+            tmem_ld32(tO + ch * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+            tmem_st32(tO + ch * 32, o);
+          }
+        }
+        {
+          uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[0]);
+          uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[32]);
+          tmem_st32(tS, p0);
+          tmem_st32(tS + 32, p1);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_PF0 + wg]);
+        if (quarter == 0 && lane == 0) ATF_TRACE(12 + 4 * wg, j);
       }
-      {
-        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[0]);
-        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[32]);
-        tmem_st32(tS, p0);
-        tmem_st32(tS + 32, p1);
-      }
-      tmem_wait_st();
+      gs += nk;
+      // ---- epilogue: o = O / l (bf16) into the slab, lse = ln 2 * (m + log2 l)
+      mbar_wait(&bars[B_OD0 + wg], (gs - 1) & 1);
+      tc_fence_after();
+      uint32_t ov[D];
+#pragma unroll
+      for (int ch = 0; ch < D / 32; ++ch) tmem_ld32(tO + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[ch * 32]));
+      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_PF0 + wg]);
-      if (quarter == 0 && lane == 0) ATF_TRACE(12 + 4 * wg, j);
-    }
-    // ---- epilogue: o = O / l (bf16) into the slab, lse = ln 2 * (m + log2 l)
-    mbar_wait(&bars[B_OD0 + wg], (nk - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    const size_t h = size_t(p.H) * D;
-    const size_t q = size_t(qi) * kTile + row;
-    __nv_bfloat16* dst = p.o + q * h + size_t(hd) * D;
+      if (lane == 0) mbar_arrive(&bars[B_OE0 + wg]);  // the next item may accumulate into O
+      const float inv = 1.f / l;
+      const size_t h = size_t(p.H) * D;
+      const size_t q = size_t(qi) * kTile + row;
+      __nv_bfloat16* dst = p.o + q * h + size_t(hd) * D;
 #pragma unroll
-    for (int ch = 0; ch < D / 32; ++ch) {
-      uint32_t o[32];
-      tmem_ld32(tO + ch * 32, o);
-      tmem_wait_ld();
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
-        w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
-        w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
-        w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-        *reinterpret_cast<uint4*>(dst + ch * 32 + v * 8) = w;
+      for (int v = 0; v < D / 8; ++v) {
+        uint4 wq;
+        wq.x = pack_bf16(__uint_as_float(ov[8 * v + 0]) * inv, __uint_as_float(ov[8 * v + 1]) * inv);
+        wq.y = pack_bf16(__uint_as_float(ov[8 * v + 2]) * inv, __uint_as_float(ov[8 * v + 3]) * inv);
+        wq.z = pack_bf16(__uint_as_float(ov[8 * v + 4]) * inv, __uint_as_float(ov[8 * v + 5]) * inv);
+        wq.w = pack_bf16(__uint_as_float(ov[8 * v + 6]) * inv, __uint_as_float(ov[8 * v + 7]) * inv);
+        *reinterpret_cast<uint4*>(dst + v * 8) = wq;
       }
+      p.lse[size_t(hd) * p.s + q] = (m + __log2f(l)) * 0.69314718055994530942f;
     }
-    p.lse[size_t(hd) * p.s + q] = (m + __log2f(l)) * 0.69314718055994530942f;
   }
 
   tc_fence_before();
@@ -317,9 +368,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+  if (threadIdx.x == 0) {  // the last CTA out resets the work counter for the next launch
+    __threadfence();
+    if (atomicAdd(&p.work[1], 1) == int(gridDim.x) - 1) {
+      p.work[0] = 0;
+      p.work[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 long long* g_trace = nullptr;
+
+// Work counters: a ring of 256 zeroed pairs per device, created on the first call (which
+// must not be inside a stream capture -- Stage._attn_init makes one eagerly); a launch takes
+// the next pair and its last CTA resets it, so launches in flight on different streams
+// never share a counter.
+static int* work_slot(int* rc) {
+  static std::mutex mu;
+  static int* bufs[64] = {};
+  static unsigned next[64] = {};
+  *rc = PPO_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) {
+    *rc = set_error(PPO_EINVAL, "ppo_attn_fwd: device %d", dev);
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (!bufs[dev]) {
+    int* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 256 * 2 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(d, 0, 256 * 2 * sizeof(int));
+    if (e != cudaSuccess) {
+      *rc = cuda_error(e, "ppo_attn_fwd: work counters (the first call must not be inside a stream capture)");
+      return nullptr;
+    }
+    bufs[dev] = d;
+  }
+  return bufs[dev] + 2 * (next[dev]++ % 256);
+}
 
 template <int D>
 static int smem_optin() {
@@ -356,8 +444,11 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, 
   const bool big = 4.0 * double(s) * double(H) * double(D) > 64.0 * (1 << 20);
   int group = group_env > 0 ? group_env : (big ? 8 : H);
   while (H % group) --group;
-  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale, attnf::g_trace, group};
-  const dim3 grid(H, s / (2 * kTile));
+  int* work = work_slot(&rc);
+  if (rc) return rc;
+  Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale, attnf::g_trace, group, work};
+  const int items = H * (s / (2 * kTile)), sms = sm_count_current();
+  const dim3 grid(items < sms ? items : sms);
   if (D == 64) {
     if ((rc = smem_optin<64>())) return rc;
     attn_fwd_kernel<64><<<grid, kThreads, Cfg<64>::kSmemBytes, st>>>(tm, prm);
