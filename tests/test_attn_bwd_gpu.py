@@ -105,3 +105,31 @@ def test_attn_bwd_rejects_bad_shapes():
     o = torch.zeros(256, 192, device=DEV, dtype=torch.bfloat16)
     with pytest.raises(native.PpoError):
         native.attn_bwd(qkv, o, o, torch.zeros(heads, 256, device=DEV), torch.empty_like(qkv), heads, ws)
+
+
+@pytest.mark.parametrize("s,heads,D", [(8192, 16, 128), (8192, 32, 64)])
+def test_attention_matches_cudnn_grouped_persistent(s, heads, D):
+    """Shapes whose 4sh bytes exceed 64 MB: both kernels dispatch in head groups and every
+    persistent CTA walks several items.  Forward o / lse and backward dq / dk / dv against
+    cuDNN's fused kernels on the same inputs (o / lse of the forward under test fed to both
+    backwards)."""
+    h = heads * D
+    g = torch.Generator(device=DEV).manual_seed(s + heads)
+    qkv = torch.randn(s, 3 * h, device=DEV, generator=g).bfloat16()
+    do = torch.randn(s, h, device=DEV, generator=g).bfloat16()
+    o = torch.empty(s, h, device=DEV, dtype=torch.bfloat16)
+    lse = torch.empty(heads, s, device=DEV, dtype=torch.float32)
+    native.attn_fwd(qkv, o, lse, heads)
+    q, k, v = [t.transpose(1, 2) for t in qkv.view(1, s, 3, heads, D).unbind(2)]
+    res = torch.ops.aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+    torch.cuda.synchronize()
+    assert _rel(o, res[0].transpose(1, 2).reshape(s, h)) <= 1e-2
+    assert (lse - res[1].reshape(heads, s)).abs().max().item() <= 2e-3
+    o4 = o.view(1, s, heads, D).transpose(1, 2)
+    do4 = do.view(1, s, heads, D).transpose(1, 2)
+    dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
+        do4, q, k, v, o4, lse.view(1, heads, s, 1), res[6], res[7], None, res[2], res[3], res[4], res[5], 0.0, True)
+    dqkv = _run_ours(qkv, o, do, lse, heads)
+    for j, ref in enumerate((dq, dk, dv)):
+        got = dqkv[:, j * h:(j + 1) * h]
+        assert _rel(got, ref.transpose(1, 2).reshape(s, h)) <= 1e-2, (j, _rel(got, ref.transpose(1, 2).reshape(s, h)))
