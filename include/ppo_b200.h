@@ -237,16 +237,18 @@ int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
 /* ------------------------------------------------ K7: causal attention forward */
 /* Replaces the attention core priced by the reference's FLOP model (costs.py:144-161,
  * 12bs^2h per layer of the 12bsh(6h+s)).  One microbatch (b = 1), causal, MHA,
- * head_dim 128, seq a multiple of 256: from qkv[s, 3, heads, head_dim] (bf16, the QKV
+ * head_dim 64 or 128, seq a multiple of 256: from qkv[s, 3, heads, head_dim] (bf16, the QKV
  * GEMM's output) writes o[s, heads*head_dim] (bf16) and lse[heads, s] (fp32, natural
  * log of the row softmax denominators of scale*QK^T -- the statistics the backward
  * consumes).  o and lse may be views into the activation slab: the producer writes the
- * saved set directly (costs.py:99-105), no pack.  tcgen05 + TMEM + TMA, persistent
- * causal tile scheduler; the first call per seq must not be inside a stream capture. */
+ * saved set directly (costs.py:99-105), no pack.  Hand-written tcgen05 + TMEM + TMA kernel,
+ * persistent with a per-launch work counter (a ring of counters per device is created by the
+ * first call, which must not be inside a stream capture).  PPO_ATTN_FWD=cutlass selects the
+ * round-1 CUTLASS-collective kernel instead (A/B only). */
 int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t heads, int64_t head_dim, float scale,
                  void* stream);
-/* Diagnostics: later ppo_attn_fwd launches record per-event SM clocks of the heaviest CTA of
- * head 0 into trace (device, 32 x 256 int64; tools/attn_fwd_trace.py); NULL turns it off. */
+/* Diagnostics: later ppo_attn_fwd launches record per-event SM clocks of the first work item
+ * of CTA 0 into trace (device, 32 x 256 int64; tools/attn_fwd_trace.py); NULL turns it off. */
 int ppo_attn_fwd_trace(void* trace);
 
 /* ----------------------------------------------- K7b: causal attention backward */
