@@ -242,7 +242,7 @@ int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
  * log of the row softmax denominators of scale*QK^T -- the statistics the backward
  * consumes).  o and lse may be views into the activation slab: the producer writes the
  * saved set directly (costs.py:99-105), no pack.  Hand-written tcgen05 + TMEM + TMA kernel,
- * persistent with a per-launch work counter (a ring of counters per device is created by the
+ * persistent with a per-launch work counter (a ring of 8192 counters per device is created by the
  * first call, which must not be inside a stream capture).  PPO_ATTN_FWD=cutlass selects the
  * round-1 CUTLASS-collective kernel instead (A/B only). */
 int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t heads, int64_t head_dim, float scale,

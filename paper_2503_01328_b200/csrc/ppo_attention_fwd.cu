@@ -380,10 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 long long* g_trace = nullptr;
 
-// Work counters: a ring of 256 zeroed pairs per device, created on the first call (which
+// Work counters: a ring of 8192 zeroed pairs per device, created on the first call (which
 // must not be inside a stream capture -- Stage._attn_init makes one eagerly); a launch takes
 // the next pair and its last CTA resets it, so launches in flight on different streams
-// never share a counter.
+// (ranks sharing a GPU, each replaying graphs with up to a few hundred launches) never
+// share a counter.
+constexpr unsigned kWorkSlots = 8192;
+
 static int* work_slot(int* rc) {
   static std::mutex mu;
   static int* bufs[64] = {};
@@ -398,15 +401,15 @@ static int* work_slot(int* rc) {
   std::lock_guard<std::mutex> lock(mu);
   if (!bufs[dev]) {
     int* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, 256 * 2 * sizeof(int));
-    if (e == cudaSuccess) e = cudaMemset(d, 0, 256 * 2 * sizeof(int));
+    cudaError_t e = cudaMalloc(&d, kWorkSlots * 2 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(d, 0, kWorkSlots * 2 * sizeof(int));
     if (e != cudaSuccess) {
       *rc = cuda_error(e, "ppo_attn_fwd: work counters (the first call must not be inside a stream capture)");
       return nullptr;
     }
     bufs[dev] = d;
   }
-  return bufs[dev] + 2 * (next[dev]++ % 256);
+  return bufs[dev] + 2 * (next[dev]++ % kWorkSlots);
 }
 
 template <int D>
