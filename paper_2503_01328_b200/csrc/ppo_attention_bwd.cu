@@ -10,8 +10,10 @@
 // statistics in the saved set (costs.py:99-105), so the backward needs no recompute of
 // the forward statistics: P = exp(scale * Q K^T - lse).
 //
-// One CTA per (kv block j of 128 rows, head); it walks the q blocks i >= j (causal) and
-// keeps dK_j, dV_j in TMEM for the whole walk.  Per (i, j) tile, five 128x128x128 UMMAs
+// Persistent: one CTA per SM takes work items (kv block j of 128 rows, head) from a global
+// counter, longest walks first; an item walks the q blocks i >= j (causal) and keeps dK_j,
+// dV_j in TMEM for the whole walk, then stores them by TMA while the next item's K_j, V_j
+// land.  Per (i, j) tile, five 128x128x(16k) UMMAs
 // (tcgen05.mma.cta_group::1.kind::f16, fp32 accumulators in TMEM):
 //
 //   S^T  = K_j Q_i^T           A = K  smem K-major   B = Q  smem K-major   -> TMEM S
@@ -34,10 +36,11 @@
 //
 // Warp roles (512 threads): warps 0-3 drain dQ from TMEM into the reduce-add, warps 4-11
 // (two warpgroups, q columns 0-63 / 64-127) compute P = exp2(S*scale*log2e - lse*log2e)
-// and dS = P (dP - delta) and write P^T to TMEM and dS^T to shared memory, warp 12 issues
-// the UMMAs (one thread) and owns the TMEM allocation, warp 13 issues the TMA loads.
-// TMEM (512 columns x 128 lanes): dK [0,128), dV [128,256), dP / dQ [256,384),
-// S [384,512) with P^T (bf16 pairs) over S's first 64 columns.
+// and dS = P (dP - delta), write P^T to TMEM and dS^T to shared memory and run the dK/dV
+// epilogue, warp 12 issues the UMMAs (one thread) and owns the TMEM allocation, warp 13
+// fetches work items and issues the TMA loads, warps 14-15 donate registers.
+// TMEM (512 columns x 128 lanes, D = 128): dK [0,128), dV [128,256), dP / dQ [256,384),
+// S [384,512) with P^T (bf16 pairs) over S's first 64 columns (D = 64: Cfg<64>).
 #include <cuda.h>  // CUtensorMap; the encoder comes from cudaGetDriverEntryPoint
 
 #include <cstdlib>
