@@ -1,5 +1,5 @@
 """Pipeline timeline of the hand-written attention forward (K7) for the heaviest CTA of
-head 0 (the last q-block pair), from the kernel's diagnostic SM-clock events
+head 0 (the last q-block pair, work item 0), from the kernel's diagnostic SM-clock events
 (ppo_attn_fwd_trace): per kv step, when the UMMA thread reached / passed the P waits of
 q block 0 and 1, and when each softmax warpgroup saw S, finished the exponentials and
 released P.
@@ -14,8 +14,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-EVENTS = {0: "m_pv0_at", 1: "m_pv0_go", 2: "m_pv1_at", 3: "m_pv1_go", 10: "s0_S", 11: "s0_exp", 12: "s0_P",
-          14: "s1_S", 15: "s1_exp", 16: "s1_P"}
+EVENTS = {0: "m_pv0_at", 1: "m_pv0_go", 2: "m_pv1_at", 3: "m_pv1_go", 10: "s0_S", 13: "s0_ld", 20: "s0_max",
+          11: "s0_exp", 12: "s0_P", 14: "s1_S", 17: "s1_ld", 21: "s1_max", 15: "s1_exp", 16: "s1_P"}
 
 
 def main():
@@ -39,16 +39,19 @@ def main():
     torch.cuda.synchronize()
     native.load().ppo_attn_fwd_trace(None)
     t = tr.view(32, 256).cpu()
-    n = s // 128
+    kv = 128 if os.environ.get("PPO_ATTN_FWD_KV") == "128" else 64  # rows per kv step
+    n = s // kv
     t0 = int(t[10, 0])
     ev = {name: [int(t[e, j]) - t0 for j in range(n)] for e, name in EVENTS.items()}
     for j in list(range(4)) + [n - 2]:
         print(j, {k: v[j] for k, v in ev.items()})
     per = lambda a_, b_: round(sum(ev[b_][j] - ev[a_][j] for j in range(2, n - 2)) / (n - 4), 1)  # noqa: E731
     print(json.dumps({"step_clk": round((ev["s0_S"][n - 2] - ev["s0_S"][2]) / (n - 4), 1),
-                      "ideal_clk": 4 * 512, "wait_P0": per("m_pv0_at", "m_pv0_go"),
-                      "wait_P1": per("m_pv1_at", "m_pv1_go"), "sm0_S_to_exp": per("s0_S", "s0_exp"),
-                      "sm0_exp_to_P": per("s0_exp", "s0_P"), "sm1_S_to_exp": per("s1_S", "s1_exp"),
+                      "ideal_clk": 4 * 4 * kv, "wait_P0": per("m_pv0_at", "m_pv0_go"),
+                      "wait_P1": per("m_pv1_at", "m_pv1_go"), "sm0_S_to_ld": per("s0_S", "s0_ld"),
+                      "sm0_ld_to_max": per("s0_ld", "s0_max"), "sm0_max_to_exp": per("s0_max", "s0_exp"),
+                      "sm0_exp_to_P": per("s0_exp", "s0_P"), "sm1_S_to_ld": per("s1_S", "s1_ld"),
+                      "sm1_ld_to_max": per("s1_ld", "s1_max"), "sm1_max_to_exp": per("s1_max", "s1_exp"),
                       "sm1_exp_to_P": per("s1_exp", "s1_P")}))
 
 
