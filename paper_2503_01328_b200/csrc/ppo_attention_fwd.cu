@@ -74,10 +74,14 @@ struct Params {
   int* work;         // [2]: work counter, finished CTAs (the last one resets both)
 };
 
-// diagnostics (ppo_attn_fwd_trace): event e of step j at trace[e * 256 + j]
+// diagnostics (ppo_attn_fwd_trace; compiled in with -DPPO_ATTN_TRACE=1 only -- the probes
+// cost ~7% at C2, tools/variant_build.py): event e of step j of work item 0 at trace[e * 256 + j]
+#ifndef PPO_ATTN_TRACE
+#define PPO_ATTN_TRACE 0
+#endif
 #define ATF_TRACE(e, j)                                                                          \
   do {                                                                                           \
-    if (p.trace && trace_item && (j) < 256) p.trace[(e) * 256 + (j)] = clock64();           \
+    if (PPO_ATTN_TRACE && p.trace && trace_item && (j) < 256) p.trace[(e) * 256 + (j)] = clock64(); \
   } while (0)
 
 template <int D>
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float m_new = fmaxf(m, mx * sl2);
         if (quarter == 0 && lane == 0) ATF_TRACE(20 + wg, j);
+        if (quarter == 0 && lane == 0) ATF_TRACE(20 + wg, j);
         // move the maximum only when it grows by more than 8 (P stays <= 2^8 otherwise)
         const bool move = m_new > m + 8.f;
         const float alpha = move ? ex2(m - m_new) : 1.f;
@@ -309,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 sp = f2u(sum2);
         l = l * alpha + (sp.x + sp.y);
         if (quarter == 0 && lane == 0) ATF_TRACE(11 + 4 * wg, j);
+        if (lane == 0) ATF_TRACE(24 + 4 * wg + quarter, j);  // exponentials done, per warp
         // O rescale (rows whose maximum moved) once the previous PV of this block is done
         if (j > 0 && __any_sync(0xffffffffu, move)) {
           mbar_wait(&bars[B_OD0 + wg], (gj - 1) & 1);
@@ -380,347 +386,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ------------------------------------------------------------ K7 with 64-row kv tiles
-// The same items and roles, but every kv step is 64 rows and each q block has TWO S
-// buffers of 64 columns: S of step t + 2 is issued into the buffer P of step t has just
-// left (right after its PV), so a softmax warpgroup finds the next S already computed
-// when it releases P.  With 128-row steps and one S per q block (TMEM holds S0, S1, O0, O1
-// = 512 columns at D = 128) every step of a q block chained its exponentials behind its own
-// PV and the next S (period ~ softmax + 2 GEMMs); here the chain is broken and the step is
-// bound by the tensor core or the SFU, whichever is busier.
-// TMEM: S(b, u) at (2b + u) * 64, P(b, u) as bf16 over its first 32 columns, O0 [256,
-// 256 + D), O1 [256 + D, 256 + 2D).  Shared memory: Q0, Q1, 4 stages of (K, V) 64-row tiles.
-constexpr int kKv = 64;
-constexpr int kKvHalf = kKv * 128;  // one 64-row x 64-column bf16 box (8 KB)
-constexpr int kStages = 4;
-
-template <int D>
-struct Cfg64 {
-  static constexpr int kHalves = D / 64;
-  static constexpr int kQBytes = kHalves * kHalf;     // 128-row Q tile
-  static constexpr int kKvBytes = kHalves * kKvHalf;  // 64-row K or V tile
-  static constexpr int kOffQ = 0;
-  static constexpr int kOffKV = 2 * kQBytes;
-  static constexpr int kOffBar = kOffKV + kStages * 2 * kKvBytes;
-  static constexpr int kNumBars = 32;
-  static constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
-  static constexpr int kOffItems = kOffTmemPtr + 16;
-  static constexpr int kSmemBytes = kOffItems + 16;
-  static_assert(kSmemBytes <= 232448, "shared memory budget");
-  static constexpr uint32_t kColO0 = 256, kColO1 = 256 + D;
-};
-
-enum : int {
-  C_Q = 0,      // Q of the current item landed
-  C_QE = 1,     // Q no longer read (the item's last S done)
-  C_KVF = 2,    // kv stage full[4]
-  C_KVE = 6,    // kv stage empty[4]
-  C_SF = 10,    // S full[q block * 2 + buffer]
-  C_PF = 14,    // P full[q block * 2 + buffer] (4 warps)
-  C_OD = 18,    // O done[2]: the last issued PV of the q block completed
-  C_OE = 20,    // O read by the epilogue[2] (4 warps)
-  C_ITEM = 22,  // item slot full[4]
-};
-
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_fwd64_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
-                      const Params p) {
-  using C = Cfg64<D>;
-  constexpr int kDK = D / 16;
-  constexpr int kPolyPer8 = PPO_FWD_POLY;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_pairs = p.s / (2 * kTile), n_items = p.H * n_pairs;
-  auto decode = [&](int w, int& i0, int& hd) {
-    const int per_group = p.head_group * n_pairs, grp = w / per_group, rem = w % per_group;
-    hd = grp * p.head_group + rem % p.head_group;
-    i0 = 2 * (n_pairs - 1 - rem / p.head_group);
-  };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::kOffTmemPtr);
-  volatile int* item_slot = reinterpret_cast<volatile int*>(smem + C::kOffItems);
-  auto next_item = [&](int r) {
-    mbar_wait(&bars[C_ITEM + (r & 3)], (r >> 2) & 1);
-    return item_slot[r & 3];
-  };
-  bool trace_item = false;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[C_Q], 1);
-    mbar_init(&bars[C_QE], 1);
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&bars[C_KVF + i], 1);
-      mbar_init(&bars[C_KVE + i], 1);
-      mbar_init(&bars[C_SF + i], 1);
-      mbar_init(&bars[C_PF + i], 4);
-      mbar_init(&bars[C_ITEM + i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars[C_OD + i], 1);
-      mbar_init(&bars[C_OE + i], 4);
-    }
-    mbar_fence_init();
-  }
-  if (warp == 8) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_ptr))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  if (warp == 9 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_q)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_kv)) : "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_ptr;
-  const uint32_t sbase = smem_u32(smem);
-
-  if (warp >= 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-    if (warp == 9) {
-      // ===================================================== TMA producer
-      if (lane == 0) {
-        const int H = p.H;
-        int gk = 0;
-        for (int r = 0;; ++r) {
-          int w = atomicAdd(&p.work[0], 1);
-          w = w < n_items ? w : -1;
-          item_slot[r & 3] = w;
-          mbar_arrive(&bars[C_ITEM + (r & 3)]);
-          if (w < 0) break;
-          int i0, hd;
-          decode(w, i0, hd);
-          mbar_wait(&bars[C_QE], (r & 1) ^ 1);
-          mbar_expect_tx(&bars[C_Q], 2 * C::kQBytes);
-          for (int q = 0; q < 2; ++q)
-            for (int half = 0; half < C::kHalves; ++half)
-              tma_load_3d(smem + C::kOffQ + q * C::kQBytes + half * kHalf, &tm_q, half * 64, hd, (i0 + q) * kTile,
-                          &bars[C_Q]);
-          const int nt = 2 * (i0 + 2);
-          for (int t = 0; t < nt; ++t, ++gk) {
-            const int st = gk & (kStages - 1);
-            mbar_wait(&bars[C_KVE + st], ((gk / kStages) & 1) ^ 1);
-            mbar_expect_tx(&bars[C_KVF + st], 2 * C::kKvBytes);
-            uint8_t* kv = smem + C::kOffKV + st * 2 * C::kKvBytes;
-            for (int half = 0; half < C::kHalves; ++half) {
-              tma_load_3d(kv + half * kKvHalf, &tm_kv, half * 64, H + hd, t * kKv, &bars[C_KVF + st]);
-              tma_load_3d(kv + C::kKvBytes + half * kKvHalf, &tm_kv, half * 64, 2 * H + hd, t * kKv,
-                          &bars[C_KVF + st]);
-            }
-          }
-        }
-      }
-    } else if (warp == 8) {
-      // ===================================================== UMMA issuer (converged warp)
-      const uint32_t sb4 = sbase >> 4;
-      const uint32_t aQ0 = sb4 + (C::kOffQ >> 4), aQ1 = sb4 + ((C::kOffQ + C::kQBytes) >> 4);
-      const uint32_t tO0 = tmem + C::kColO0, tO1 = tmem + C::kColO1;
-      auto tS = [&](int b, int u) { return tmem + uint32_t((2 * b + u) * 64); };
-      constexpr uint32_t I_S = idesc(0, 0, kKv), I_PV = idesc(0, 1, D);
-      int gk = 0, g0 = 0, g1 = 0;  // kv tiles, steps of q block 0 / 1 (barrier phases, S buffers)
-      auto aK = [&](int k) { return sb4 + ((C::kOffKV + (k & (kStages - 1)) * 2 * C::kKvBytes) >> 4); };
-      auto aV = [&](int k) {
-        return sb4 + ((C::kOffKV + (k & (kStages - 1)) * 2 * C::kKvBytes + C::kKvBytes) >> 4);
-      };
-      auto kv_wait = [&](int k) { mbar_wait(&bars[C_KVF + (k & (kStages - 1))], (k / kStages) & 1); };
-      for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
-        int i0, hd;
-        decode(w, i0, hd);
-        trace_item = w == 0;
-        const int n0 = 2 * (i0 + 1), n1 = n0 + 2;
-        mbar_wait(&bars[C_Q], r & 1);
-        for (int t = 0; t < 2; ++t) {  // S of steps 0, 1 for both q blocks
-          kv_wait(gk + t);
-          tc_fence_after();
-          const int u0 = (g0 + t) & 1, u1 = (g1 + t) & 1;
-          gemm128<kDK, false, false, false, kKvHalf>(tS(0, u0), aQ0, aK(gk + t), I_S, false);
-          tc_commit(&bars[C_SF + u0]);
-          gemm128<kDK, false, false, false, kKvHalf>(tS(1, u1), aQ1, aK(gk + t), I_S, false);
-          tc_commit(&bars[C_SF + 2 + u1]);
-        }
-        for (int t = 0; t < n1; ++t) {
-          const int k = gk + t;
-          ATF_TRACE(0, t);
-          if (t < n0) {  // O0 += P0(t) V_t, then S0(t + 2) into the buffer P0(t) leaves
-            const int u = (g0 + t) & 1;
-            mbar_wait(&bars[C_PF + u], ((g0 + t) >> 1) & 1);
-            ATF_TRACE(1, t);
-            if (t == 0 && r > 0) mbar_wait(&bars[C_OE], (r - 1) & 1);
-            tc_fence_after();
-            gemm128<kKv / 16, false, true, true, kKvHalf>(tO0, tS(0, u), aV(k), I_PV, t > 0);
-            tc_commit(&bars[C_OD]);
-            if (t + 2 < n0) {
-              kv_wait(k + 2);
-              tc_fence_after();
-              gemm128<kDK, false, false, false, kKvHalf>(tS(0, u), aQ0, aK(k + 2), I_S, false);
-              tc_commit(&bars[C_SF + u]);
-            }
-          }
-          const int u = (g1 + t) & 1;
-          ATF_TRACE(2, t);
-          mbar_wait(&bars[C_PF + 2 + u], ((g1 + t) >> 1) & 1);
-          ATF_TRACE(3, t);
-          if (t == 0 && r > 0) mbar_wait(&bars[C_OE + 1], (r - 1) & 1);
-          tc_fence_after();
-          gemm128<kKv / 16, false, true, true, kKvHalf>(tO1, tS(1, u), aV(k), I_PV, t > 0);
-          tc_commit(&bars[C_OD + 1]);
-          tc_commit(&bars[C_KVE + (k & (kStages - 1))]);  // K_t, V_t consumed
-          if (t + 2 < n1) {
-            kv_wait(k + 2);
-            tc_fence_after();
-            gemm128<kDK, false, false, false, kKvHalf>(tS(1, u), aQ1, aK(k + 2), I_S, false);
-            tc_commit(&bars[C_SF + 2 + u]);
-          }
-          if (t + 3 == n1) tc_commit(&bars[C_QE]);  // the item's last S issued: Q may be replaced
-        }
-        gk += n1;
-        g0 += n0;
-        g1 += n1;
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-    // ===================================================== softmax warpgroups
-    const int wg = warp >> 2, quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t tSb = tmem + lane_off + uint32_t(wg * 128);
-    const uint32_t tO = tmem + lane_off + (wg ? C::kColO1 : C::kColO0);
-    const float sl2 = p.scale * 1.4426950408889634f;
-    int gs = 0;
-    for (int r = 0, w; (w = next_item(r)) >= 0; ++r) {
-      int i0, hd;
-      decode(w, i0, hd);
-      trace_item = w == 0;
-      const int qi = i0 + wg, nk = 2 * (qi + 1);
-      float m = -INFINITY, l = 0.f;
-      for (int t = 0; t < nk; ++t) {
-        const int gt = gs + t, u = gt & 1;
-        const uint32_t tS = tSb + uint32_t(u * 64);
-        mbar_wait(&bars[C_SF + 2 * wg + u], (gt >> 1) & 1);
-        if (quarter == 0 && lane == 0) ATF_TRACE(10 + 4 * wg, t);
-        tc_fence_after();
-        uint32_t rr[2][32];
-        tmem_ld32(tS, rr[0]);
-        tmem_ld32(tS + 32, rr[1]);
-        tmem_wait_ld();
-        if (quarter == 0 && lane == 0) ATF_TRACE(13 + 4 * wg, t);
-        const bool diag = t >= 2 * qi;
-        if (diag) {  // kv column t * 64 + c > q row qi * 128 + row is masked
-          const int lim = row - (t - 2 * qi) * kKv;
-#pragma unroll
-          for (int c = 0; c < kKv; ++c)
-            if (c > lim) rr[c >> 5][c & 31] = __float_as_uint(-INFINITY);
-        }
-        float mx;
-        {
-          float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < kKv; c += 8) {
-            a0 = fmax3(a0, __uint_as_float(rr[c >> 5][c & 31]), __uint_as_float(rr[c >> 5][(c + 1) & 31]));
-            a1 = fmax3(a1, __uint_as_float(rr[c >> 5][(c + 2) & 31]), __uint_as_float(rr[c >> 5][(c + 3) & 31]));
-            a2 = fmax3(a2, __uint_as_float(rr[c >> 5][(c + 4) & 31]), __uint_as_float(rr[c >> 5][(c + 5) & 31]));
-            a3 = fmax3(a3, __uint_as_float(rr[c >> 5][(c + 6) & 31]), __uint_as_float(rr[c >> 5][(c + 7) & 31]));
-          }
-          mx = fmax3(a0, a1, fmaxf(a2, a3));
-        }
-        const float m_new = fmaxf(m, mx * sl2);
-        if (quarter == 0 && lane == 0) ATF_TRACE(20 + wg, t);
-        const bool move = m_new > m + 8.f;  // lazy maximum: P stays <= 2^8 otherwise
-        const float alpha = move ? ex2(m - m_new) : 1.f;
-        if (move) m = m_new;
-        const uint64_t sl2x2 = f2(sl2, sl2), nm2 = f2(-m, -m);
-        uint64_t sum2 = f2(0.f, 0.f);
-        uint32_t pk[32];
-        auto exps = [&](auto poly) {
-#pragma unroll
-          for (int c = 0; c < kKv; c += 2) {
-            const float2 x = f2u(ffma2(f2(__uint_as_float(rr[c >> 5][c & 31]), __uint_as_float(rr[c >> 5][(c + 1) & 31])),
-                                       sl2x2, nm2));
-            float2 e;
-            if (decltype(poly)::value && (c & 7) < 2 * (kPolyPer8 / 2)) {
-              e = ex2_fma2(x.x, x.y);
-            } else if (decltype(poly)::value && (c & 7) == 2 * (kPolyPer8 / 2) && (kPolyPer8 & 1)) {
-              e = make_float2(ex2_fma(x.x), ex2(x.y));
-            } else {
-              e = make_float2(ex2(x.x), ex2(x.y));
-            }
-            sum2 = fadd2(sum2, f2(e.x, e.y));
-            pk[c >> 1] = pack_bf16(e.x, e.y);
-          }
-        };
-        if (diag) exps(std::false_type{});  // masked -inf scores go through the SFU
-        else exps(std::true_type{});
-        const float2 sp = f2u(sum2);
-        l = l * alpha + (sp.x + sp.y);
-        if (quarter == 0 && lane == 0) ATF_TRACE(11 + 4 * wg, t);
-        if (t > 0 && __any_sync(0xffffffffu, move)) {  // O rescale once the previous PV is done
-          mbar_wait(&bars[C_OD + wg], (gt - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int ch = 0; ch < D / 32; ++ch) {
-            uint32_t o[32];
-            tmem_ld32(tO + ch * 32, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-            tmem_st32(tO + ch * 32, o);
-          }
-        }
-        tmem_st32(tS, pk);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[C_PF + 2 * wg + u]);
-        if (quarter == 0 && lane == 0) ATF_TRACE(12 + 4 * wg, t);
-      }
-      gs += nk;
-      // ---- epilogue: o = O / l (bf16) into the slab, lse = ln 2 * (m + log2 l)
-      mbar_wait(&bars[C_OD + wg], (gs - 1) & 1);
-      tc_fence_after();
-      uint32_t ov[D];
-#pragma unroll
-      for (int ch = 0; ch < D / 32; ++ch) tmem_ld32(tO + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[ch * 32]));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[C_OE + wg]);
-      const float inv = 1.f / l;
-      const size_t h = size_t(p.H) * D;
-      const size_t q = size_t(qi) * kTile + row;
-      __nv_bfloat16* dst = p.o + q * h + size_t(hd) * D;
-#pragma unroll
-      for (int v = 0; v < D / 8; ++v) {
-        uint4 wq;
-        wq.x = pack_bf16(__uint_as_float(ov[8 * v + 0]) * inv, __uint_as_float(ov[8 * v + 1]) * inv);
-        wq.y = pack_bf16(__uint_as_float(ov[8 * v + 2]) * inv, __uint_as_float(ov[8 * v + 3]) * inv);
-        wq.z = pack_bf16(__uint_as_float(ov[8 * v + 4]) * inv, __uint_as_float(ov[8 * v + 5]) * inv);
-        wq.w = pack_bf16(__uint_as_float(ov[8 * v + 6]) * inv, __uint_as_float(ov[8 * v + 7]) * inv);
-        *reinterpret_cast<uint4*>(dst + v * 8) = wq;
-      }
-      p.lse[size_t(hd) * p.s + q] = (m + __log2f(l)) * 0.69314718055994530942f;
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 8) {
-    __syncwarp();
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&p.work[1], 1) == int(gridDim.x) - 1) {
-      p.work[0] = 0;
-      p.work[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
 long long* g_trace = nullptr;
 
 // Work counters: a ring of 8192 zeroed pairs per device, created on the first call (which
@@ -768,17 +433,11 @@ static int smem_optin(K kernel, int bytes, unsigned* done) {
 }
 
 template <int D>
-static int launch(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const Params& prm, dim3 grid, bool kv64,
-                  cudaStream_t st) {
-  static unsigned done128 = 0, done64 = 0;
+static int launch(const CUtensorMap& tm, const Params& prm, dim3 grid, cudaStream_t st) {
+  static unsigned done = 0;
   int rc;
-  if (kv64) {
-    if ((rc = smem_optin(attn_fwd64_kernel<D>, Cfg64<D>::kSmemBytes, &done64))) return rc;
-    attn_fwd64_kernel<D><<<grid, kThreads, Cfg64<D>::kSmemBytes, st>>>(tm_q, tm_kv, prm);
-  } else {
-    if ((rc = smem_optin(attn_fwd_kernel<D>, Cfg<D>::kSmemBytes, &done128))) return rc;
-    attn_fwd_kernel<D><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(tm_q, prm);
-  }
+  if ((rc = smem_optin(attn_fwd_kernel<D>, Cfg<D>::kSmemBytes, &done))) return rc;
+  attn_fwd_kernel<D><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(tm, prm);
   return PPO_OK;
 }
 
@@ -792,15 +451,9 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, 
   tc::EncodeTiled enc = tc::encoder(&rc);
   if (rc) return rc;
   const int64_t h = int64_t(H) * D;
-  CUtensorMap tm, tm_kv;
+  CUtensorMap tm;
   if ((rc = tc::make_map(enc, &tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * H, s, 3 * h * 2, 64, kTile)))
     return rc;
-  if ((rc = tc::make_map(enc, &tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, qkv, D, 3 * H, s, 3 * h * 2, 64, kKv)))
-    return rc;
-  static const bool kv64 = [] {
-    const char* e = std::getenv("PPO_ATTN_FWD_KV");  // A/B: 128-row kv steps (one S per q block)
-    return !(e && std::atoi(e) == 128);
-  }();
   static const int group_env = [] {
     const char* e = std::getenv("PPO_ATTN_HEAD_GROUP");  // A/B experiments
     return e ? std::atoi(e) : 0;
@@ -815,8 +468,7 @@ int attn_fwd_tcgen05(const void* qkv, void* o, float* lse, int s, int H, int D, 
   Params prm{static_cast<__nv_bfloat16*>(o), lse, s, H, scale, attnf::g_trace, group, work};
   const int items = H * (s / (2 * kTile)), sms = sm_count_current();
   const dim3 grid(items < sms ? items : sms);
-  if ((rc = D == 64 ? launch<64>(tm, tm_kv, prm, grid, kv64, st) : launch<128>(tm, tm_kv, prm, grid, kv64, st)))
-    return rc;
+  if ((rc = D == 64 ? launch<64>(tm, prm, grid, st) : launch<128>(tm, prm, grid, st))) return rc;
   PPO_LAUNCHED("attn_fwd_kernel");
   return PPO_OK;
 }

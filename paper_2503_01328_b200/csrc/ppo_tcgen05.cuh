@@ -173,8 +173,7 @@ __host__ __device__ constexpr uint32_t idesc(uint32_t a_mn, uint32_t b_mn, uint3
 // converged UMMA warp.  a4 / b4: shared-memory tile start >> 4 (descriptor address field),
 // or for kATmem the TMEM address of A (K = 16 per 8 columns of bf16 pairs).  Descriptor low
 // words are a4/b4 + compile-time constants (no carry: addresses < 2^18); the high word is
-// SBO = 1024 B, version 1, SWIZZLE_128B for both majors.  kBHalf: bytes between B's 64-wide
-// halves (a 64-row B tile, e.g. a 64-row K / V tile of K7's forward, has 8 KB halves).
+// SBO = 1024 B, version 1, SWIZZLE_128B for both majors.
 template <int kSteps, bool kAMn, bool kBMn, bool kATmem, int kBHalf = kHalf>
 __device__ __forceinline__ void gemm128(uint32_t d, uint32_t a4, uint32_t b4, uint32_t idesc, bool acc) {
   asm volatile("" : "+r"(a4), "+r"(b4));  // keep the per-k descriptors out of the loop-invariant pool

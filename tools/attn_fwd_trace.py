@@ -4,7 +4,10 @@ head 0 (the last q-block pair, work item 0), from the kernel's diagnostic SM-clo
 q block 0 and 1, and when each softmax warpgroup saw S, finished the exponentials and
 released P.
 
-    python tools/attn_fwd_trace.py [--s 4096 --heads 16]
+    python tools/variant_build.py trace ppo_attention_fwd.cu -DPPO_ATTN_TRACE=1
+    PPO_LIB_PATH=abtest/trace/libppo_b200.so python tools/attn_fwd_trace.py [--s 4096 --heads 16]
+
+(the probes are compiled out of the default build)
 """
 import argparse
 import json
@@ -15,7 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 EVENTS = {0: "m_pv0_at", 1: "m_pv0_go", 2: "m_pv1_at", 3: "m_pv1_go", 10: "s0_S", 13: "s0_ld", 20: "s0_max",
-          11: "s0_exp", 12: "s0_P", 14: "s1_S", 17: "s1_ld", 21: "s1_max", 15: "s1_exp", 16: "s1_P"}
+          11: "s0_exp", 12: "s0_P", 14: "s1_S", 17: "s1_ld", 21: "s1_max", 15: "s1_exp", 16: "s1_P",
+          24: "s0_exp_w0", 25: "s0_exp_w1", 26: "s0_exp_w2", 27: "s0_exp_w3", 28: "s1_exp_w4", 29: "s1_exp_w5",
+          30: "s1_exp_w6", 31: "s1_exp_w7"}
 
 
 def main():
@@ -39,7 +44,7 @@ def main():
     torch.cuda.synchronize()
     native.load().ppo_attn_fwd_trace(None)
     t = tr.view(32, 256).cpu()
-    kv = 128 if os.environ.get("PPO_ATTN_FWD_KV") == "128" else 64  # rows per kv step
+    kv = 128  # rows per kv step
     n = s // kv
     t0 = int(t[10, 0])
     ev = {name: [int(t[e, j]) - t0 for j in range(n)] for e, name in EVENTS.items()}
@@ -52,7 +57,9 @@ def main():
                       "sm0_ld_to_max": per("s0_ld", "s0_max"), "sm0_max_to_exp": per("s0_max", "s0_exp"),
                       "sm0_exp_to_P": per("s0_exp", "s0_P"), "sm1_S_to_ld": per("s1_S", "s1_ld"),
                       "sm1_ld_to_max": per("s1_ld", "s1_max"), "sm1_max_to_exp": per("s1_max", "s1_exp"),
-                      "sm1_exp_to_P": per("s1_exp", "s1_P")}))
+                      "sm1_exp_to_P": per("s1_exp", "s1_P"),
+                      "exp_done_per_warp_vs_w0": [per("s0_S", f"s0_exp_w{w}") for w in range(4)] +
+                      [per("s1_S", f"s1_exp_w{w}") for w in range(4, 8)]}))
 
 
 if __name__ == "__main__":
