@@ -543,50 +543,66 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // delta[hd, i] = -sum_d dO[i, hd*D + d] * O[i, hd*D + d] (fp32), lse2 = -log2(e) * lse
 // (negated: the main kernel adds them in packed FFMA2 / FADD2), and the fp32 dQ
-// accumulator row i zeroed.  One block per row; D/8 lanes per head.
+// accumulator row i zeroed.  Blocks stride over row pairs (both rows' loads in flight
+// before the reductions); D/8 lanes per head.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                             const __nv_bfloat16* __restrict__ dout,
                                                             const float* __restrict__ lse, float* __restrict__ lse2,
                                                             float* __restrict__ delta, float* __restrict__ dq_acc,
                                                             int* __restrict__ work, int s, int H, int D) {
   pdl_wait();
-  const int i = blockIdx.x;
-  if (i == 0 && threadIdx.x == 0) *work = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *work = 0;
   const int h = H * D;
-  for (int t = threadIdx.x; t < H; t += blockDim.x) lse2[size_t(t) * s + i] = -lse[size_t(t) * s + i] * 1.4426950408889634f;
-  for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
-    const int e = e0 + threadIdx.x * 8;
-    const bool ok = e < h;
-    float acc = 0.f;
-    if (ok) {
-      float a[8], b[8];
-      unpack8(*reinterpret_cast<const uint4*>(o + size_t(i) * h + e), a);
-      unpack8(*reinterpret_cast<const uint4*>(dout + size_t(i) * h + e), b);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < H * s; t += gridDim.x * blockDim.x)
+    lse2[t] = -lse[t] * 1.4426950408889634f;
+  for (int i0 = 2 * blockIdx.x; i0 < s; i0 += 2 * gridDim.x) {
+    for (int e0 = 0; e0 < h; e0 += blockDim.x * 8) {  // block-uniform trip count (shuffles below)
+      const int e = e0 + threadIdx.x * 8;
+      const bool ok = e < h;
+      uint4 ov[2], dv[2];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc = fmaf(a[k], b[k], acc);
-    }
-    for (int off = D / 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (ok) {
-      if ((threadIdx.x & (D / 8 - 1)) == 0) delta[size_t(e / D) * s + i] = -acc;
-      float4* z = reinterpret_cast<float4*>(dq_acc + size_t(i) * h + e);
-      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < 2; ++r)
+        if (ok && i0 + r < s) {
+          ov[r] = *reinterpret_cast<const uint4*>(o + size_t(i0 + r) * h + e);
+          dv[r] = *reinterpret_cast<const uint4*>(dout + size_t(i0 + r) * h + e);
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int i = i0 + r;
+        float acc = 0.f;
+        if (ok && i < s) {
+          float a[8], b[8];
+          unpack8(ov[r], a);
+          unpack8(dv[r], b);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = fmaf(a[k], b[k], acc);
+        }
+        for (int off = D / 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (ok && i < s) {
+          if ((threadIdx.x & (D / 8 - 1)) == 0) delta[size_t(e / D) * s + i] = -acc;
+          float4* z = reinterpret_cast<float4*>(dq_acc + size_t(i) * h + e);
+          z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
     }
   }
 }
 
-// dqkv[:, 0:h] = bf16(scale * dq_acc)
+// dqkv[:, 0:h] = bf16(scale * dq_acc).  One row per block iteration (32-bit column index,
+// no 64-bit division per vector); dq_acc is dead afterwards (streaming loads).
 __global__ void __launch_bounds__(256) attn_bwd_dq_kernel(const float* __restrict__ dq_acc,
                                                           __nv_bfloat16* __restrict__ dqkv, int s, int h, float scale) {
   pdl_wait();
-  const size_t n8 = size_t(s) * h / 8;
-  for (size_t v = blockIdx.x * size_t(blockDim.x) + threadIdx.x; v < n8; v += size_t(gridDim.x) * blockDim.x) {
-    const size_t e = v * 8;
-    const size_t row = e / h, col = e % h;
-    const float4 a = reinterpret_cast<const float4*>(dq_acc)[2 * v];
-    const float4 b = reinterpret_cast<const float4*>(dq_acc)[2 * v + 1];
-    float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale, b.x * scale, b.y * scale, b.z * scale, b.w * scale};
-    *reinterpret_cast<uint4*>(dqkv + row * 3 * h + col) = pack8(f);
+  const int nv = h >> 3;
+  for (int row = blockIdx.x; row < s; row += gridDim.x) {
+    const float4* src = reinterpret_cast<const float4*>(dq_acc + size_t(row) * h);
+    uint4* dst = reinterpret_cast<uint4*>(dqkv + size_t(row) * 3 * h);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const float4 a = __ldcs(src + 2 * v), b = __ldcs(src + 2 * v + 1);
+      float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale, b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+      dst[v] = pack8(f);
+    }
   }
 }
 
@@ -665,7 +681,8 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
     return rc;
   if ((rc = make_map(enc, &tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dq_acc, D, heads, seq, h * 4, 32, 32))) return rc;
 
-  launch_pdl(attn_bwd_prep_kernel, dim3(s), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
+  const int sms = sm_count_current();
+  launch_pdl(attn_bwd_prep_kernel, dim3(s / 2), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(o),
              static_cast<const __nv_bfloat16*>(dout), lse, lse2, delta, dq_acc, work, s, H, D);
   PPO_LAUNCHED("attn_bwd_prep_kernel");
   static const int exp_mode = [] {
@@ -676,17 +693,20 @@ int ppo_attn_bwd(const void* qkv, const void* o, const void* dout, const float* 
     const char* e = std::getenv("PPO_ATB_HEAD_GROUP");  // A/B experiments
     return e ? std::atoi(e) : 0;
   }();
-  // group heads only when one operand pair of all heads (4 s h bytes) outgrows a half of L2;
-  // below that the all-heads LPT order packs the SMs better (C2 forward 66 vs 70 us)
-  const bool big = 4.0 * double(s) * double(H) * double(D) > 64.0 * (1 << 20);
-  int group = group_env > 0 ? group_env : (big ? 8 : H);
+  // Heads dispatched together: the largest group whose per-head L2 working set (Q and dO
+  // bf16, the fp32 dQ accumulator: 8 s D bytes per head) stays within ~0.7 of L2 (88 MB),
+  // so the q-block tiles every kv block of a head re-reads and the dQ reduce targets stay
+  // on chip.  C4 (s = 16384, 40 heads): groups of 2 / 4 / 5 / 8 measured 6542 / 6570 /
+  // 6516 / 6686 us; C3 picks 8, C2 all 16 heads.
+  int group = group_env > 0 ? group_env : H;
+  if (group_env <= 0)
+    while (group > 1 && double(group) * 8.0 * double(s) * double(D) > 88.0 * (1 << 20)) --group;
   while (H % group) --group;
   Params prm{static_cast<__nv_bfloat16*>(dqkv), lse2, delta, dq_acc, work, s, H, scale, g_trace, exp_mode, group};
   rc = D == 64 ? launch_main<64>(tm_qkv, tm_do, tm_dq, tm_dqkv, prm, st)
                : launch_main<128>(tm_qkv, tm_do, tm_dq, tm_dqkv, prm, st);
   if (rc) return rc;
-  const int sms = sm_count_current();
-  launch_pdl(attn_bwd_dq_kernel, dim3(sms * 4), dim3(256), 0, st, static_cast<const float*>(dq_acc),
+  launch_pdl(attn_bwd_dq_kernel, dim3(s < sms * 16 ? s : sms * 16), dim3(256), 0, st, static_cast<const float*>(dq_acc),
              static_cast<__nv_bfloat16*>(dqkv), s, int(h), scale);
   PPO_LAUNCHED("attn_bwd_dq_kernel");
   return PPO_OK;

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run_one(s, H, D=128, eager=0):
+def run_one(s, H, D=128, eager=0, profile=0):
     import torch
 
     from bench import _graph_time_us
@@ -45,6 +45,23 @@ def run_one(s, H, D=128, eager=0):
         torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
             t["do4"], t["q"], t["k"], t["v"], r[0], r[1], r[6], r[7], None, r[2], r[3], r[4], r[5], 0.0, True)
 
+    if profile:  # per-kernel device time (CUPTI via torch.profiler), eager launches
+        from torch.profiler import ProfilerActivity, profile as prof
+        res = {}
+        for name, fn in (("ours", ours), ("cudnn", cudnn)):
+            for i in range(4):
+                fn(sets[i % 2])
+            torch.cuda.synchronize()
+            with prof(activities=[ProfilerActivity.CUDA]) as p:
+                for i in range(profile):
+                    fn(sets[i % 2])
+                torch.cuda.synchronize()
+            per = {}
+            for e in p.events():
+                if e.device_type.name == "CUDA" and e.device_time_total > 0:
+                    per.setdefault(e.name[:60], []).append(e.device_time_total)
+            res[name] = {k: round(sum(v) / len(v), 2) for k, v in per.items() if len(v) >= profile}
+        return {"s": s, "heads": H, "per_kernel_us": res}
     if eager:  # for ncu: plain launches of ours only
         for i in range(eager):
             ours(sets[i % 2])
@@ -62,10 +79,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="4096x16,8192x32,16384x40")
     ap.add_argument("--eager", type=int, default=0, help="only launch ours N times (for ncu)")
+    ap.add_argument("--profile", type=int, default=0, help="per-kernel times over N eager launches")
     a = ap.parse_args()
     for shp in a.shapes.split(","):
         s, H = map(int, shp.split("x"))
-        print(json.dumps(run_one(s, H, eager=a.eager)), flush=True)
+        print(json.dumps(run_one(s, H, eager=a.eager, profile=a.profile)), flush=True)
 
 
 if __name__ == "__main__":
