@@ -247,8 +247,10 @@ int ppo_gemm_set_swizzle(int op, int64_t M, int64_t N, int64_t K, int swizzle);
  * round-1 CUTLASS-collective kernel instead (A/B only). */
 int ppo_attn_fwd(const void* qkv, void* o, float* lse, int64_t seq, int64_t heads, int64_t head_dim, float scale,
                  void* stream);
-/* Diagnostics: later ppo_attn_fwd launches record per-event SM clocks of the first work item
- * of CTA 0 into trace (device, 32 x 256 int64; tools/attn_fwd_trace.py); NULL turns it off. */
+/* Diagnostics: later ppo_attn_fwd launches record per-event SM clocks of work item 0 into
+ * trace (device, 32 x 256 int64; tools/attn_fwd_trace.py); NULL turns it off.  The probes
+ * are compiled in only with -DPPO_ATTN_TRACE=1 (tools/variant_build.py); in the default
+ * library the call is accepted and records nothing. */
 int ppo_attn_fwd_trace(void* trace);
 
 /* ----------------------------------------------- K7b: causal attention backward */
