@@ -107,10 +107,11 @@ def test_attn_bwd_rejects_bad_shapes():
         native.attn_bwd(qkv, o, o, torch.zeros(heads, 256, device=DEV), torch.empty_like(qkv), heads, ws)
 
 
-@pytest.mark.parametrize("s,heads,D", [(8192, 16, 128), (8192, 32, 64)])
+@pytest.mark.parametrize("s,heads,D", [(8192, 16, 128), (8192, 32, 64), (16384, 40, 128)])
 def test_attention_matches_cudnn_grouped_persistent(s, heads, D):
-    """Shapes whose 4sh bytes exceed 64 MB: both kernels dispatch in head groups and every
-    persistent CTA walks several items.  Forward o / lse and backward dq / dk / dv against
+    """Shapes where both kernels dispatch in head groups (forward: 4sh bytes > 64 MB;
+    backward: groups whose Q, dO and fp32 dQ fit ~0.7 of L2 -- 5 of 40 heads at the C4
+    shape, the last case) and every persistent CTA walks several items.  Forward o / lse and backward dq / dk / dv against
     cuDNN's fused kernels on the same inputs (o / lse of the forward under test fed to both
     backwards)."""
     h = heads * D
